@@ -1,0 +1,320 @@
+"""bench.py -- time-to-fixpoint of the B200 propagation engine.
+
+Metric (BASELINE.json): time-to-fixpoint & GB/s per round vs the HBM
+roofline; speedup vs the CPU reference.  One "step" = one full propagation
+of one instance to its fixpoint (or infeasibility / round limit) from its
+start bounds.
+
+Default workload: config C2 -- synthetic 1M x 1M,
+power-law row lengths (x_min 4.25, beta 1.5, cap 10k, ~12M entries), mixed
+bounds incl. infinities, 50% integer, seed 20090778, on one B200.  The
+instance (~200 MB in HBM) is larger than L2 and L2 is flushed between steps.
+
+  value     device time-to-fixpoint per step (ms, CUDA events around the
+            graph launch; inputs resident in HBM), max over ranks
+  e2e       the same solve through the C-ABI entry point pg_propagate with
+            pinned HOST buffers: H2D upload + on-device setup + solve + D2H
+  roofline  the dominant kernel (k_tiles) timed alone with CUDA events:
+            algorithmic bytes / mean launch time vs MEASURED_PEAKS hbm_gbs
+  cpu_baseline  the reference's own cpu_seq (compiled from its sources into
+            oracle/_ref; 1 core), best of a bounded number of solves
+
+--gpus N > 1: a single instance stays on one GPU (north star), so N ranks run
+N independent replicas (weak scaling); value = max over ranks.
+--impl reference: the reference's cpu_par (oracle/_ref, all host threads) on
+the same instance, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "time-to-fixpoint & GB/s per round vs HBM roofline; geomean speedup vs CPU ref"
+
+
+def b_round(m, n, nnz):
+    """SURVEY.md 8(d) algorithmic bytes of one full propagation round."""
+    return 12 * nnz + 4 * (m + 1) + 16 * m + 33 * n
+
+
+def hbm_peak():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _loop(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._loop, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 2 + i and s[2 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_init():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def make_instance(config, seed):
+    from paper_2009_07785_b200 import generators as G
+    return G.config_instance(config, seed)
+
+
+def pinned_copy(inst):
+    """Instance arrays in page-locked host memory (the e2e H2D source)."""
+    import torch
+
+    from paper_2009_07785_b200.model import ProblemInstance
+
+    def pin(a):
+        t = torch.empty(a.shape, dtype={np.int32: torch.int32, np.float64: torch.float64,
+                                        np.uint8: torch.uint8}[a.dtype.type], pin_memory=True)
+        t.numpy()[...] = a
+        return t.numpy()
+
+    return ProblemInstance.from_arrays(pin(inst.matrix.row_ptr), pin(inst.matrix.col_idx),
+                                       pin(inst.matrix.values), pin(inst.lhs), pin(inst.rhs),
+                                       pin(inst.bounds.lower), pin(inst.bounds.upper),
+                                       pin(inst.integral), num_cols=inst.num_cols(),
+                                       name=inst.name)
+
+
+def run_reference(args, inst, rank, world):
+    """The reference's own cpu_par (all host threads) on the same workload."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2009_07785_b200.model import EngineConfig
+
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable":
+                          "oracle/_ref/libpropgate_ref.so not built (needs /root/reference at build time)"}))
+        return
+    threads = os.cpu_count() or 1
+    cfg = EngineConfig(worker_count=threads)
+    for _ in range(args.warmup):
+        O.ref_propagate_parallel(inst, cfg)
+    times, res = [], None
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        res = O.ref_propagate_parallel(inst, cfg)
+        times.append(res.elapsed_ns / 1e6)
+    wall = (time.perf_counter() - t0) * 1e3 / args.steps
+    ms = float(np.mean(times))
+    m, n, nnz = inst.num_rows(), inst.num_cols(), inst.matrix.nnz()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(ms, 4), "unit": "ms",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.config, "instance": inst.name, "m": m,
+                                        "n": n, "nnz": nnz, "engine": "propagate_parallel (cpu_par)"},
+        "rounds": res.rounds_executed, "status": res.status.name,
+        "rounds_per_s": round(res.rounds_executed / (ms / 1e3), 2),
+        "gbs_per_round": round(b_round(m, n, nnz) * res.rounds_executed / (ms / 1e3) / 1e9, 3),
+        "wall_ms_per_step": round(wall, 3),
+        "cpu_baseline": {"value": round(ms, 4), "unit": "ms", "cores": threads,
+                         "kind": "reference", "sample": f"{args.steps} full solves of {inst.name}"},
+        "e2e": {"value": round(ms, 4), "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(inst, budget_s=25.0):
+    """cpu_seq of the reference (1 core), best of up to 3 solves within ~budget."""
+    from oracle import oracle as O
+    from paper_2009_07785_b200.model import EngineConfig
+
+    ref = O.ref_available()
+    fn = O.ref_propagate_sequential if ref else O.propagate_sequential
+    cfg = EngineConfig()
+    best, res, t0, runs = None, None, time.perf_counter(), 0
+    while runs < 3 and (runs == 0 or time.perf_counter() - t0 < budget_s):
+        res = fn(inst, cfg)
+        runs += 1
+        v = res.elapsed_ns / 1e6
+        best = v if best is None else min(best, v)
+    return {"value": round(best, 3), "unit": "ms", "cores": 1,
+            "kind": "reference" if ref else "port",
+            "sample": f"cpu_seq best of {runs} full solves of {inst.name} "
+                      f"({res.status.name}, {res.rounds_executed} rounds)",
+            "status": res.status.name, "rounds": res.rounds_executed}, res
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world, rank, local = dist_init()
+    inst = make_instance(args.config, args.seed)
+    if args.impl == "reference":
+        run_reference(args, inst, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    from paper_2009_07785_b200.engine import Session, propagate_gpu
+    from paper_2009_07785_b200.model import EngineConfig
+
+    cfg = EngineConfig(device=local)
+    m, n, nnz = inst.num_rows(), inst.num_cols(), inst.matrix.nnz()
+    sess = Session(inst, cfg)
+    info = sess.info()
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
+
+    for _ in range(args.warmup):
+        r = sess.run()
+    launches_per_round = 1 + (3 if info["nlong"] else 0) + 1
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    step_ms, rounds = [], []
+    with ClockSampler(local) as clk:
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.zero_()
+            torch.cuda.synchronize()
+            r = sess.run()
+            step_ms.append(r.elapsed_ns / 1e6)
+            rounds.append(r.rounds_executed)
+        barrier()
+        wall_ms = (time.perf_counter() - t0) * 1e3
+    total_ms = float(np.sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms = total_ms / args.steps
+    R = rounds[-1]
+    gpu_launches = sum(1 + rr * launches_per_round for rr in rounds)
+
+    # dominant kernel alone (roofline)
+    k_ns, k_bytes = sess.time_round_kernel(reps=20)
+    peak, peak_kind = hbm_peak()
+    achieved = k_bytes / (k_ns * 1e-9) / 1e9
+
+    # e2e through the C-ABI with pinned host buffers
+    pinned = pinned_copy(inst)
+    e2e = []
+    for i in range(args.e2e_steps + 1):
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        re = propagate_gpu(pinned, cfg)
+        e2e.append((time.perf_counter() - t1) * 1e3)
+    e2e_ms = float(np.median(e2e[1:]))
+    assert re.status == r.status and re.rounds_executed == R
+
+    line = {
+        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": args.config, "instance": inst.name, "m": m, "n": n, "nnz": nnz,
+                   "parallelism": "replicas" if world > 1 else "single-gpu",
+                   "l2": "flushed between steps (256 MB write); instance > L2",
+                   "tiles": info["num_tiles"], "long_rows": info["nlong"]},
+        "rounds": R, "status": r.status.name,
+        "rounds_per_s": round(R / (ms / 1e3), 1),
+        "ms_per_round": round(ms / max(R, 1), 5),
+        "gbs_per_round": round(b_round(m, n, nnz) * R / (ms / 1e3) / 1e9, 1),
+        "round_roofline_frac": round(b_round(m, n, nnz) * R / (ms / 1e3) / 1e9 / peak, 4),
+        "round_roofline_frac_8tbs": round(b_round(m, n, nnz) * R / (ms / 1e3) / 8e12 * 1e9 / 1e9, 4),
+        "wall_ms_per_step": round(wall_ms / args.steps, 3),
+        "roofline": {"kernel": "k_tiles", "bound": "hbm", "achieved": round(achieved, 1),
+                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": None,
+                     "bytes_per_launch": k_bytes, "launch_us": round(k_ns / 1e3, 3),
+                     "share_of_round": round(k_ns / 1e6 / (ms / max(R, 1)), 3)},
+        "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
+                "h2d_bytes_per_step": int(12 * nnz + 4 * (m + 1) + 16 * m + 17 * n),
+                "d2h_bytes_per_step": int(16 * n + 8 * R)},
+        "gpu_launches": int(gpu_launches),
+        "clocks": clk.summary(),
+    }
+    if rank == 0 and not args.no_cpu_baseline:
+        cb, cres = cpu_baseline(inst)
+        line["cpu_baseline"] = cb
+        line["speedup_vs_cpu_seq"] = round(cb["value"] / ms, 2)
+        line["e2e_speedup_vs_cpu_seq"] = round(cb["value"] / e2e_ms, 2)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    sess.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,170 @@
+"""Python mirror of the reference propagator API over the CUDA C-ABI.
+
+  propagate_gpu(instance, cfg)          ~ propagate_parallel  (par_engine.hpp:41-42)
+                                          with cpu_seq verdicts when cfg.row_check
+  propagate_round_gpu(instance, snap)   ~ propagate_round_parallel (par_engine.hpp:33-36)
+  partition_row_blocks(matrix, cfg)     ~ partition_row_blocks (par_engine.hpp:12-13)
+  Session(instance, cfg)                matrix resident in HBM; re-propagate new
+                                        start bounds (B&B warm start) and node batches
+
+Errors follow the reference: an invalid EngineConfig raises ValueError (the
+reference throws std::invalid_argument, core/src/model.cpp:21-35);
+Infeasible / RoundLimit are statuses, not exceptions.  Every call goes to the
+CUDA library; there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import abi
+from .model import (EngineConfig, PropagationResult, ProblemInstance, VariableBounds,
+                    new_c_result, result_from_c)
+
+
+def _lib():
+    return abi.load_library()
+
+
+def validate(cfg: EngineConfig) -> None:
+    c = cfg.to_c()
+    abi.check(_lib().pg_config_validate(C.byref(c)), "EngineConfig.validate")
+
+
+def propagate_gpu(instance: ProblemInstance, cfg: EngineConfig | None = None) -> PropagationResult:
+    cfg = cfg or EngineConfig()
+    c = cfg.to_c()
+    p = instance.to_c()
+    r, lo, up, prc = new_c_result(instance.num_cols(), cfg.round_limit)
+    abi.check(_lib().pg_propagate(C.byref(p), C.byref(c), C.byref(r)), "pg_propagate")
+    return result_from_c(r, lo, up, prc)
+
+
+@dataclass
+class RoundSnapshot:
+    """par_engine.hpp:18-21"""
+    bounds_in: VariableBounds
+    bounds_out: VariableBounds | None = None
+
+
+@dataclass
+class RoundOutcome:
+    """par_engine.hpp:23-27"""
+    changed: bool = False
+    infeasible: bool = False
+    changes: int = 0
+
+
+def propagate_round_gpu(instance: ProblemInstance, snap: RoundSnapshot,
+                        cfg: EngineConfig | None = None) -> RoundOutcome:
+    cfg = cfg or EngineConfig()
+    c = cfg.to_c()
+    p = instance.to_c()
+    n = instance.num_cols()
+    lb_in = np.ascontiguousarray(snap.bounds_in.lower, dtype=np.float64)
+    ub_in = np.ascontiguousarray(snap.bounds_in.upper, dtype=np.float64)
+    lo = np.empty(n)
+    up = np.empty(n)
+    ch, inf, cnt = C.c_int32(), C.c_int32(), C.c_int64()
+    abi.check(_lib().pg_round(C.byref(p), C.byref(c), abi.ptr(lb_in, C.c_double),
+                              abi.ptr(ub_in, C.c_double), abi.ptr(lo, C.c_double),
+                              abi.ptr(up, C.c_double), C.byref(ch), C.byref(inf), C.byref(cnt)),
+              "pg_round")
+    snap.bounds_out = VariableBounds(lo, up)
+    return RoundOutcome(bool(ch.value), bool(inf.value), int(cnt.value))
+
+
+def partition_row_blocks(instance: ProblemInstance, cfg: EngineConfig | None = None):
+    cfg = cfg or EngineConfig()
+    c = cfg.to_c()
+    p = instance.to_c()
+    m = instance.num_rows()
+    starts = np.zeros(m + 1, dtype=np.int32)
+    kinds = np.zeros(max(m, 1), dtype=np.int32)
+    nb = C.c_int32()
+    abi.check(_lib().pg_partition_row_blocks(C.byref(p), C.byref(c), abi.ptr(starts, C.c_int32),
+                                             abi.ptr(kinds, C.c_int32), C.byref(nb)),
+              "pg_partition_row_blocks")
+    return starts[: nb.value + 1].copy(), kinds[: nb.value].copy()
+
+
+class Session:
+    """One problem resident on the device (pg_session_*)."""
+
+    INFO_FIELDS = ("m", "n", "nnz", "num_tiles", "nlong", "nchunks", "tile_rows", "tile_nnz",
+                   "long_nnz")
+
+    def __init__(self, instance: ProblemInstance, cfg: EngineConfig | None = None):
+        self.cfg = cfg or EngineConfig()
+        self.instance = instance
+        self._h = C.c_void_p()
+        c = self.cfg.to_c()
+        p = instance.to_c()
+        abi.check(_lib().pg_session_create(C.byref(p), C.byref(c), C.byref(self._h)),
+                  "pg_session_create")
+
+    def close(self):
+        if self._h:
+            _lib().pg_session_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def propagate(self, lower=None, upper=None) -> PropagationResult:
+        n = self.instance.num_cols()
+        r, lo, up, prc = new_c_result(n, self.cfg.round_limit)
+        lp = up_ = None
+        if lower is not None:
+            lower = np.ascontiguousarray(lower, dtype=np.float64)
+            upper = np.ascontiguousarray(upper, dtype=np.float64)
+            lp, up_ = abi.ptr(lower, C.c_double), abi.ptr(upper, C.c_double)
+        abi.check(_lib().pg_session_propagate(self._h, lp, up_, C.byref(r)), "pg_session_propagate")
+        return result_from_c(r, lo, up, prc)
+
+    def run(self, download=False) -> PropagationResult:
+        """Solve from the device-resident start bounds (nothing crosses PCIe
+        unless download=True)."""
+        n = self.instance.num_cols()
+        r, lo, up, prc = new_c_result(n, self.cfg.round_limit)
+        if not download:
+            r.lower = C.cast(None, C.POINTER(C.c_double))
+            r.upper = C.cast(None, C.POINTER(C.c_double))
+        abi.check(_lib().pg_session_run(self._h, C.byref(r)), "pg_session_run")
+        return result_from_c(r, lo, up, prc)
+
+    def propagate_batch(self, lower: np.ndarray, upper: np.ndarray):
+        K, n = lower.shape
+        lower = np.ascontiguousarray(lower, dtype=np.float64)
+        upper = np.ascontiguousarray(upper, dtype=np.float64)
+        lo = np.empty_like(lower)
+        up = np.empty_like(upper)
+        st = np.zeros(K, dtype=np.int32)
+        rd = np.zeros(K, dtype=np.int32)
+        abi.check(_lib().pg_session_propagate_batch(
+            self._h, K, abi.ptr(lower, C.c_double), abi.ptr(upper, C.c_double),
+            abi.ptr(lo, C.c_double), abi.ptr(up, C.c_double), abi.ptr(st, C.c_int32),
+            abi.ptr(rd, C.c_int32)), "pg_session_propagate_batch")
+        return lo, up, st, rd
+
+    def time_round_kernel(self, reps=10):
+        mean_ns, nbytes = C.c_double(), C.c_double()
+        abi.check(_lib().pg_session_time_round_kernel(self._h, reps, C.byref(mean_ns),
+                                                      C.byref(nbytes)), "time_round_kernel")
+        return mean_ns.value, nbytes.value
+
+    def info(self) -> dict:
+        v = np.zeros(len(self.INFO_FIELDS), dtype=np.int64)
+        abi.check(_lib().pg_session_info(self._h, abi.ptr(v, C.c_int64), v.shape[0]), "info")
+        return dict(zip(self.INFO_FIELDS, (int(x) for x in v)))
