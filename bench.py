@@ -14,7 +14,7 @@ instance (~200 MB in HBM) is larger than L2 and L2 is flushed between steps.
             graph launch; inputs resident in HBM), max over ranks
   e2e       the same solve through the C-ABI entry point pg_propagate with
             pinned HOST buffers: H2D upload + on-device setup + solve + D2H
-  roofline  the dominant kernel (k_tiles) timed alone with CUDA events:
+  roofline  the dominant kernel (k_round) timed alone with CUDA events:
             algorithmic bytes / mean launch time vs MEASURED_PEAKS hbm_gbs
   cpu_baseline  the reference's own cpu_seq (compiled from its sources into
             oracle/_ref; 1 core), best of a bounded number of solves
@@ -231,7 +231,7 @@ def main():
 
     for _ in range(args.warmup):
         r = sess.run()
-    launches_per_round = 1 + (3 if info["nlong"] else 0) + 1
+    launches_per_round = 1 + (1 if info["segments"] else 0) + 1
 
     def barrier():
         torch.cuda.synchronize()
@@ -284,7 +284,8 @@ def main():
         "config": {"workload": args.config, "instance": inst.name, "m": m, "n": n, "nnz": nnz,
                    "parallelism": "replicas" if world > 1 else "single-gpu",
                    "l2": "flushed between steps (256 MB write); instance > L2",
-                   "tiles": info["num_tiles"], "long_rows": info["nlong"]},
+                   "warp_tiles": info["num_tiles"], "segment_rows": info["seg_rows"],
+                   "segments": info["segments"]},
         "rounds": R, "status": r.status.name,
         "rounds_per_s": round(R / (ms / 1e3), 1),
         "ms_per_round": round(ms / max(R, 1), 5),
@@ -292,7 +293,7 @@ def main():
         "round_roofline_frac": round(b_round(m, n, nnz) * R / (ms / 1e3) / 1e9 / peak, 4),
         "round_roofline_frac_8tbs": round(b_round(m, n, nnz) * R / (ms / 1e3) / 8e12 * 1e9 / 1e9, 4),
         "wall_ms_per_step": round(wall_ms / args.steps, 3),
-        "roofline": {"kernel": "k_tiles", "bound": "hbm", "achieved": round(achieved, 1),
+        "roofline": {"kernel": "k_round", "bound": "hbm", "achieved": round(achieved, 1),
                      "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": None,
                      "bytes_per_launch": k_bytes, "launch_us": round(k_ns / 1e3, 3),

@@ -100,7 +100,7 @@ def default_config() -> PgConfig:
     c.scalar_mode = PG_WIDE64
     c.device = 0
     c.loop_mode = PG_LOOP_GRAPH
-    c.flags = PG_FLAG_ROWCHECK
+    c.flags = PG_FLAG_ROWCHECK | PG_FLAG_WORKLIST
     return c
 
 
@@ -131,11 +131,13 @@ _lib = None
 _gen = None
 
 
-def load_library(path: str = LIB_PATH):
-    """Load the product library; raises if it is absent (no fallback)."""
+def load_library(path: str | None = None):
+    """Load the product library; raises if it is absent (no fallback).
+    PG_LIB overrides the path (build variants for experiments)."""
     global _lib
     if _lib is not None:
         return _lib
+    path = path or os.environ.get("PG_LIB") or LIB_PATH
     if not os.path.exists(path):
         raise EngineError(
             f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "

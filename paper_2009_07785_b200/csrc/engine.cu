@@ -4,13 +4,16 @@
 // Session = one problem resident in HBM:
 //   row_ptr  int32[m+1]     col  int32[nnz] (bit 31 = integral flag)
 //   vals     f64[nnz]       lhs/rhs f64[m] (normalised to +-inf)
-//   key_in   {i64,i64}[n]   snapshot bounds as ordered-bits keys
-//   key_out  {i64,i64}[n]   merge target of the round (atomicMax/atomicMin)
+//   snap     Snap[n]        32 B snapshot record {lo, up, q, flags} per column
+//   key_out  {i64,i64}[n]   merge target of the round (atomicMax/atomicMin on
+//                           ordered-bits keys)
 //   lo0/up0  f64[n]         normalised start bounds
-// plus the tile table of short rows and the chunk table of long rows.
+// Rows are stored sorted by length.  Short rows (<= min(16, nnz_budget)
+// entries) form warp tiles; longer rows are split into segments of
+// nnz_budget entries (the chunks of cpu_par's wide-row sums).
 //
 // The round loop (par_engine.cpp:228-267) runs on the device: a CUDA graph
-//   k_reset -> WHILE(cond) { k_tiles, k_long_*, k_commit }
+//   k_reset -> WHILE(cond) { k_round, k_seg_cand, k_commit }
 // where k_commit's last CTA writes per_round_changes[r] and clears `cond`
 // on Infeasible / Converged / RoundLimit.  One graph launch per solve; no
 // host synchronisation per round.
@@ -25,6 +28,8 @@
 #include <vector>
 
 #include "../../include/propgate_b200.h"
+#include <cub/device/device_scan.cuh>
+
 #include "kernels.cuh"
 
 using namespace pgb;
@@ -106,31 +111,43 @@ struct pg_session {
   double* d_vals = nullptr;
   double* d_lhs = nullptr;
   double* d_rhs = nullptr;
-  longlong2* d_key_in = nullptr;
+  Snap* d_snap = nullptr;
+  uint8_t* d_integral = nullptr;
+  int32_t* d_row_done = nullptr;
   longlong2* d_key_out = nullptr;
   double* d_lo0 = nullptr;
   double* d_up0 = nullptr;
   double* d_lo_res = nullptr;
   double* d_up_res = nullptr;
-  int2* d_tiles = nullptr;
-  LongChunk* d_chunks = nullptr;
-  int32_t* d_long_rows = nullptr;
-  int32_t* d_long_first = nullptr;
-  Act* d_partial = nullptr;
-  Act* d_long_act = nullptr;
+  TileDesc* d_tiles = nullptr;
+  SegGroup* d_groups = nullptr;
+  SegDesc* d_segs = nullptr;
+  int32_t* d_srow = nullptr;
+  int32_t* d_sfirst = nullptr;
+  int32_t* d_chunk_seg = nullptr;
+  SegPartial* d_partial = nullptr;
+  Act* d_row_act = nullptr;
+  int32_t* d_worklist = nullptr;
   DevState* d_st = nullptr;
   long long* d_per_round = nullptr;
+  // worklist index and dirty sets
+  int32_t* d_col_ptr = nullptr;
+  int32_t* d_col_item = nullptr;
+  uint8_t* d_flags = nullptr;  // tile | segment-row marks, two buffers each
+  Dirty dirty{};
 
   // host mirrors
   DevState* h_st = nullptr;  // pinned
-  int32_t num_tiles = 0, nlong = 0, nchunks = 0;
-  int64_t tile_rows = 0, tile_nnz = 0, long_nnz = 0;
+  int32_t num_tiles = 0, nseg = 0, nsrow = 0, ngroups = 0;
+  int64_t tile_rows = 0, tile_nnz = 0, seg_nnz = 0;
 
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraphConditionalHandle cond = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 
   ~pg_session() {
     if (dev >= 0) cudaSetDevice(dev);
@@ -138,9 +155,13 @@ struct pg_session {
     if (graph) cudaGraphDestroy(graph);
     if (ev0) cudaEventDestroy(ev0);
     if (ev1) cudaEventDestroy(ev1);
-    void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_key_in, d_key_out, d_lo0, d_up0,
-                    d_lo_res, d_up_res, d_tiles, d_chunks, d_long_rows, d_long_first, d_partial,
-                    d_long_act, d_st, d_per_round};
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
+    if (stream2) cudaStreamDestroy(stream2);
+    void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
+                    d_lo_res, d_up_res, d_tiles, d_groups, d_segs, d_srow, d_sfirst, d_chunk_seg, d_partial,
+                    d_row_act, d_worklist, d_st, d_per_round, d_col_ptr, d_col_item,
+                    d_flags};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (h_st) cudaFreeHost(h_st);
@@ -153,42 +174,75 @@ struct pg_session {
   }
 
   // ---- one round of kernels, enqueued on `stream` ------------------------------
+  RoundArgs round_args() const {
+    RoundArgs A;
+    A.tiles = d_tiles;
+    A.num_tiles = num_tiles;
+    A.segs = d_segs;
+    A.nseg = nseg;
+    A.groups = d_groups;
+    A.ngroups = ngroups;
+    A.srow = d_srow;
+    A.sfirst = d_sfirst;
+    A.chunk_seg = d_chunk_seg;
+    A.row_done = d_row_done;
+    A.partial = d_partial;
+    A.row_act = d_row_act;
+    A.worklist = d_worklist;
+    A.row_ptr = d_row_ptr;
+    A.colx = d_colx;
+    A.vals = d_vals;
+    A.lhs = d_lhs;
+    A.rhs = d_rhs;
+    A.snap = d_snap;
+    A.key_out = (long long*)d_key_out;
+    A.st = d_st;
+    A.dirty = dirty;
+    return A;
+  }
+
   void enqueue_round(bool use_graph, cudaEvent_t k1_begin = nullptr, cudaEvent_t k1_end = nullptr) {
     const bool rowcheck = (cfg.flags & PG_FLAG_ROWCHECK) != 0;
+    RoundArgs A = round_args();
+    // timing-only switches (results are wrong with them): 0x100 no segment
+    // groups, 0x200 no warp tiles
     if (k1_begin) PG_CUDA(cudaEventRecord(k1_begin, stream));
-    if (num_tiles > 0) {
+    // segment groups and warp tiles are independent: two branches of the round
+    if (ngroups > 0 && num_tiles > 0) {
+      PG_CUDA(cudaEventRecord(ev_fork, stream));
+      PG_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
+    }
+    if (ngroups > 0 && !(cfg.flags & 0x100u)) {
+      cudaStream_t sg = num_tiles > 0 ? stream2 : stream;
+      const int grid = std::max(1, std::min(ngroups, num_sms * 2));
       if (rowcheck)
-        k_tiles<true><<<num_tiles, kTileThreads, 0, stream>>>(d_tiles, d_row_ptr, d_colx, d_vals,
-                                                              d_lhs, d_rhs, d_key_in,
-                                                              (long long*)d_key_out, d_st, dcfg);
+        k_round<true><<<grid, kRoundThreads, sizeof(SegGroupSmem), sg>>>(A, dcfg);
       else
-        k_tiles<false><<<num_tiles, kTileThreads, 0, stream>>>(d_tiles, d_row_ptr, d_colx, d_vals,
-                                                               d_lhs, d_rhs, d_key_in,
-                                                               (long long*)d_key_out, d_st, dcfg);
+        k_round<false><<<grid, kRoundThreads, sizeof(SegGroupSmem), sg>>>(A, dcfg);
+    }
+    if (num_tiles > 0 && !(cfg.flags & 0x200u)) {
+      const int grid = std::max(1, std::min((num_tiles + kTWarps - 1) / kTWarps, num_sms * 3));
+      if (rowcheck)
+        k_tiles<true><<<grid, kTWarps * 32, sizeof(TileWarpSmem) * kTWarps, stream>>>(A, dcfg);
+      else
+        k_tiles<false><<<grid, kTWarps * 32, sizeof(TileWarpSmem) * kTWarps, stream>>>(A, dcfg);
+    }
+    if (ngroups > 0 && num_tiles > 0) {
+      PG_CUDA(cudaEventRecord(ev_join, stream2));
+      PG_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
     }
     if (k1_end) PG_CUDA(cudaEventRecord(k1_end, stream));
-    if (nlong > 0) {
-      k_long_partial<<<(nchunks * 32 + 255) / 256, 256, 0, stream>>>(d_chunks, nchunks, d_colx,
-                                                                     d_vals, d_key_in, d_partial);
-      if (rowcheck)
-        k_long_combine<true><<<(nlong + 127) / 128, 128, 0, stream>>>(
-            d_long_rows, d_long_first, nlong, d_partial, d_long_act, d_lhs, d_rhs, d_st, dcfg);
-      else
-        k_long_combine<false><<<(nlong + 127) / 128, 128, 0, stream>>>(
-            d_long_rows, d_long_first, nlong, d_partial, d_long_act, d_lhs, d_rhs, d_st, dcfg);
-      k_long_cand<<<nchunks, 256, 0, stream>>>(d_chunks, d_long_rows, d_long_act, d_colx, d_vals,
-                                                d_lhs, d_rhs, d_key_in, (long long*)d_key_out,
-                                                d_st, dcfg);
-    }
+    if (nseg > 0)
+      k_seg_cand<<<std::min(nseg, num_sms * 8), 256, 0, stream>>>(A, dcfg);
     k_commit<<<grid_for(n, kCommitThreads), kCommitThreads, 0, stream>>>(
-        d_key_in, d_key_out, n, d_st, d_per_round, dcfg, cond, use_graph ? 1 : 0);
+        d_snap, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0);
     PG_CUDA(cudaGetLastError());
   }
 
   void enqueue_reset(bool use_graph, bool check_crossed) {
     k_reset<<<grid_for(n, kCommitThreads), kCommitThreads, 0, stream>>>(
-        d_lo0, d_up0, d_key_in, d_key_out, n, d_st, dcfg, check_crossed ? 1 : 0, cond,
-        use_graph ? 1 : 0);
+        d_lo0, d_up0, d_integral, d_snap, d_key_out, n, d_st, dcfg, dirty, check_crossed ? 1 : 0,
+        cond, use_graph ? 1 : 0);
     PG_CUDA(cudaGetLastError());
   }
 
@@ -291,38 +345,59 @@ struct pg_session {
 
 namespace {
 
-void build_tables(pg_session* s, const int32_t* rp, std::vector<int2>& tiles,
-                  std::vector<LongChunk>& chunks, std::vector<int32_t>& long_rows,
-                  std::vector<int32_t>& long_first) {
+struct Tables {
+  std::vector<TileDesc> tiles;
+  std::vector<SegGroup> groups;
+  std::vector<SegDesc> segs;
+  std::vector<int32_t> srow, sfirst, chunk_seg, seg_group;
+};
+
+// Tables over the length-sorted rows: warp tiles of short rows, segments of
+// long rows (chunks of nnz_budget, as wide_row_activities), the latter
+// sorted by length so that a warp's 32 segments have near-equal work.
+void build_tables(pg_session* s, const int32_t* rp, Tables& T) {
   const int64_t chunk = s->cfg.nnz_budget;
-  const int64_t long_t = std::min<int64_t>(chunk, kTileNnz);
-  int32_t i = 0;
+  const int64_t short_max = std::min<int64_t>(chunk, kShortMax);
   const int32_t m = s->m;
-  while (i < m) {
-    const int64_t len = (int64_t)rp[i + 1] - rp[i];
-    if (len > long_t) {
-      const int32_t slot = (int32_t)long_rows.size();
-      long_rows.push_back(i);
-      long_first.push_back((int32_t)chunks.size());
-      for (int64_t k = rp[i]; k < rp[i + 1]; k += chunk)
-        chunks.push_back({slot, (int32_t)k, (int32_t)std::min<int64_t>(k + chunk, rp[i + 1]), 0});
-      s->long_nnz += len;
-      ++i;
-      continue;
-    }
+  int32_t i = 0;
+  while (i < m && (int64_t)rp[i + 1] - rp[i] <= short_max) {
     const int32_t start = i;
     int64_t acc = 0;
-    while (i < m && i - start < kTileRows) {
+    while (i < m && i - start < 32) {
       const int64_t l = (int64_t)rp[i + 1] - rp[i];
-      if (l > long_t || acc + l > kTileNnz) break;
+      if (l > short_max || acc + l > kWNnz) break;
       acc += l;
       ++i;
     }
-    tiles.push_back(make_int2(start, i));
+    T.tiles.push_back({start, i - start, rp[start], (int32_t)acc});
     s->tile_rows += i - start;
     s->tile_nnz += acc;
   }
-  long_first.push_back((int32_t)chunks.size());
+  for (; i < m; ++i) {
+    const int32_t slot = (int32_t)T.srow.size();
+    T.srow.push_back(i);
+    T.sfirst.push_back((int32_t)T.segs.size());
+    for (int64_t k = rp[i]; k < rp[i + 1]; k += chunk) {
+      const int32_t len = (int32_t)std::min<int64_t>(chunk, rp[i + 1] - k);
+      T.segs.push_back({(int32_t)k, len, (int32_t)T.segs.size(), slot});
+    }
+    s->seg_nnz += (int64_t)rp[i + 1] - rp[i];
+  }
+  T.sfirst.push_back((int32_t)T.segs.size());
+  std::stable_sort(T.segs.begin(), T.segs.end(),
+                   [](const SegDesc& x, const SegDesc& y) { return x.len > y.len; });
+  // groups: 8 segments when long (shorter per-group critical path), else 32
+  for (size_t q = 0; q < T.segs.size();) {
+    const int32_t g = T.segs[q].len > kLongSeg ? 8 : 32;
+    const int32_t cnt = (int32_t)std::min<size_t>(g, T.segs.size() - q);
+    T.groups.push_back({(int32_t)q, cnt});
+    q += cnt;
+  }
+  T.chunk_seg.assign(T.segs.size(), 0);
+  for (size_t q = 0; q < T.segs.size(); ++q) T.chunk_seg[T.segs[q].out] = (int32_t)q;
+  T.seg_group.assign(T.segs.size(), 0);
+  for (size_t g = 0; g < T.groups.size(); ++g)
+    for (int32_t q = 0; q < T.groups[g].count; ++q) T.seg_group[T.groups[g].first + q] = (int32_t)g;
 }
 
 pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
@@ -345,6 +420,15 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->dev = cfg->device;
     PG_CUDA(cudaSetDevice(s->dev));
     s->num_sms = prop.multiProcessorCount;
+    PG_CUDA(cudaFuncSetAttribute(k_round<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(SegGroupSmem)));
+    PG_CUDA(cudaFuncSetAttribute(k_round<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sizeof(SegGroupSmem)));
+    PG_CUDA(cudaFuncSetAttribute(k_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(TileWarpSmem) * kTWarps)));
+    PG_CUDA(cudaFuncSetAttribute(k_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(sizeof(TileWarpSmem) * kTWarps)));
+
     s->m = p->num_rows;
     s->n = p->num_cols;
     s->nnz = p->nnz;
@@ -358,71 +442,151 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->dcfg.flags = cfg->flags;
     PG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
     PG_CUDA(cudaEventCreate(&s->ev0));
+    PG_CUDA(cudaStreamCreateWithFlags(&s->stream2, cudaStreamNonBlocking));
+    PG_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
+    PG_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
     PG_CUDA(cudaEventCreate(&s->ev1));
 
-    std::vector<int2> tiles;
-    std::vector<LongChunk> chunks;
-    std::vector<int32_t> long_rows, long_first;
-    build_tables(s, p->row_ptr, tiles, chunks, long_rows, long_first);
-    s->num_tiles = (int32_t)tiles.size();
-    s->nlong = (int32_t)long_rows.size();
-    s->nchunks = (int32_t)chunks.size();
-
+    // Rows sorted by length (stable counting sort): consecutive rows of a
+    // tile then have near-uniform lengths.  Row order is not observable --
+    // candidates merge by exact max/min and each row is summed on its own.
     const int32_t m = s->m, n = s->n;
     const int64_t nnz = s->nnz;
-    s->d_row_ptr = dalloc<int32_t>(m + 1);
-    s->d_colx = dalloc<int32_t>(nnz);
-    s->d_vals = dalloc<double>(nnz);
-    s->d_lhs = dalloc<double>(m);
-    s->d_rhs = dalloc<double>(m);
-    s->d_key_in = dalloc<longlong2>(n);
+    std::vector<int32_t> perm(m), srp(m + 1);
+    {
+      constexpr int32_t kCap = 1 << 16;
+      std::vector<int64_t> cnt(kCap + 2, 0);
+      for (int32_t i = 0; i < m; ++i)
+        ++cnt[std::min<int64_t>((int64_t)p->row_ptr[i + 1] - p->row_ptr[i], kCap) + 1];
+      for (int32_t b = 1; b <= kCap + 1; ++b) cnt[b] += cnt[b - 1];
+      for (int32_t i = 0; i < m; ++i)
+        perm[cnt[std::min<int64_t>((int64_t)p->row_ptr[i + 1] - p->row_ptr[i], kCap)]++] = i;
+      // rows at or beyond the cap: order them by length too
+      const int64_t first_cap = cnt[kCap - 1];
+      std::stable_sort(perm.begin() + first_cap, perm.end(), [&](int32_t x, int32_t y) {
+        return p->row_ptr[x + 1] - p->row_ptr[x] < p->row_ptr[y + 1] - p->row_ptr[y];
+      });
+      srp[0] = 0;
+      for (int32_t i = 0; i < m; ++i) srp[i + 1] = srp[i] + (p->row_ptr[perm[i] + 1] - p->row_ptr[perm[i]]);
+    }
+    Tables T;
+    build_tables(s, srp.data(), T);
+    s->num_tiles = (int32_t)T.tiles.size();
+    s->nseg = (int32_t)T.segs.size();
+    s->nsrow = (int32_t)T.srow.size();
+    s->ngroups = (int32_t)T.groups.size();
+
+    s->d_row_ptr = dalloc<int32_t>((size_t)m + 1 + 4);  // +16 B: bulk-copy tail
+    s->d_colx = dalloc<int32_t>(nnz + 4);  // +16 B: bulk copies round up to 16 B
+    s->d_vals = dalloc<double>(nnz + 2);
+    s->d_lhs = dalloc<double>((size_t)m + 2);
+    s->d_rhs = dalloc<double>((size_t)m + 2);
+    s->d_snap = dalloc<Snap>(n);
+    s->d_integral = dalloc<uint8_t>(n);
     s->d_key_out = dalloc<longlong2>(n);
     s->d_lo0 = dalloc<double>(n);
     s->d_up0 = dalloc<double>(n);
     s->d_lo_res = dalloc<double>(n);
     s->d_up_res = dalloc<double>(n);
-    s->d_tiles = dalloc<int2>(tiles.size());
-    s->d_chunks = dalloc<LongChunk>(chunks.size());
-    s->d_long_rows = dalloc<int32_t>(long_rows.size());
-    s->d_long_first = dalloc<int32_t>(long_first.size());
-    s->d_partial = dalloc<Act>(chunks.size());
-    s->d_long_act = dalloc<Act>(long_rows.size());
+    s->d_tiles = dalloc<TileDesc>(T.tiles.size());
+    s->d_groups = dalloc<SegGroup>(T.groups.size());
+    s->d_segs = dalloc<SegDesc>(T.segs.size());
+    s->d_srow = dalloc<int32_t>(T.srow.size());
+    s->d_sfirst = dalloc<int32_t>(T.sfirst.size());
+    s->d_chunk_seg = dalloc<int32_t>(T.chunk_seg.size());
+    s->d_partial = dalloc<SegPartial>(T.segs.size());
+    s->d_row_act = dalloc<Act>(T.srow.size());
+    s->d_worklist = dalloc<int32_t>(T.segs.size());
+    s->d_row_done = dalloc<int32_t>(T.srow.size());
     s->d_st = dalloc<DevState>(1);
     s->d_per_round = dalloc<long long>(cfg->round_limit);
     PG_CUDA(cudaMallocHost(&s->h_st, sizeof(DevState)));
-    uint8_t* d_integral = dalloc<uint8_t>(n);
+
+    // staging copies of the caller's arrays (original row order)
+    int32_t* t_rp = dalloc<int32_t>(m + 1);
+    int32_t* t_cols = dalloc<int32_t>(nnz);
+    double* t_vals = dalloc<double>(nnz);
+    double* t_lhs = dalloc<double>(m);
+    double* t_rhs = dalloc<double>(m);
+    int32_t* t_perm = dalloc<int32_t>(m);
+    uint8_t* d_integral = s->d_integral;
 
     cudaStream_t st = s->stream;
     PG_CUDA(cudaMemsetAsync(s->d_st, 0, sizeof(DevState), st));
-    PG_CUDA(cudaMemcpyAsync(s->d_row_ptr, p->row_ptr, sizeof(int32_t) * (m + 1),
+    PG_CUDA(cudaMemsetAsync(s->d_row_done, 0, sizeof(int32_t) * std::max<size_t>(1, T.srow.size()), st));
+    PG_CUDA(cudaMemsetAsync(s->d_colx, 0, sizeof(int32_t) * (nnz + 4), st));
+    PG_CUDA(cudaMemsetAsync(s->d_vals, 0, sizeof(double) * (nnz + 2), st));
+    PG_CUDA(cudaMemcpyAsync(t_rp, p->row_ptr, sizeof(int32_t) * (m + 1), cudaMemcpyHostToDevice, st));
+    PG_CUDA(cudaMemcpyAsync(s->d_row_ptr, srp.data(), sizeof(int32_t) * (m + 1),
                             cudaMemcpyHostToDevice, st));
+    if (m) PG_CUDA(cudaMemcpyAsync(t_perm, perm.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
     if (nnz) {
-      PG_CUDA(cudaMemcpyAsync(s->d_colx, p->col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
-      PG_CUDA(cudaMemcpyAsync(s->d_vals, p->values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
+      PG_CUDA(cudaMemcpyAsync(t_cols, p->col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
+      PG_CUDA(cudaMemcpyAsync(t_vals, p->values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
     }
     if (m) {
-      PG_CUDA(cudaMemcpyAsync(s->d_lhs, p->lhs, sizeof(double) * m, cudaMemcpyHostToDevice, st));
-      PG_CUDA(cudaMemcpyAsync(s->d_rhs, p->rhs, sizeof(double) * m, cudaMemcpyHostToDevice, st));
-      k_normalize<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_lhs, m, cfg->infinity_threshold);
-      k_normalize<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_rhs, m, cfg->infinity_threshold);
+      PG_CUDA(cudaMemcpyAsync(t_lhs, p->lhs, sizeof(double) * m, cudaMemcpyHostToDevice, st));
+      PG_CUDA(cudaMemcpyAsync(t_rhs, p->rhs, sizeof(double) * m, cudaMemcpyHostToDevice, st));
     }
     if (n) PG_CUDA(cudaMemcpyAsync(d_integral, p->integral, n, cudaMemcpyHostToDevice, st));
-    if (nnz) k_pack_cols<<<s->grid_for(nnz, 256), 256, 0, st>>>(s->d_colx, d_integral, nnz);
-    if (!tiles.empty())
-      PG_CUDA(cudaMemcpyAsync(s->d_tiles, tiles.data(), sizeof(int2) * tiles.size(),
-                              cudaMemcpyHostToDevice, st));
-    if (!chunks.empty()) {
-      PG_CUDA(cudaMemcpyAsync(s->d_chunks, chunks.data(), sizeof(LongChunk) * chunks.size(),
-                              cudaMemcpyHostToDevice, st));
-      PG_CUDA(cudaMemcpyAsync(s->d_long_rows, long_rows.data(), sizeof(int32_t) * long_rows.size(),
-                              cudaMemcpyHostToDevice, st));
+    if (m) {
+      k_permute_rows<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
+          t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, d_integral, s->d_colx,
+          s->d_vals, s->d_lhs, s->d_rhs, m, cfg->infinity_threshold);
+      PG_CUDA(cudaGetLastError());
     }
-    PG_CUDA(cudaMemcpyAsync(s->d_long_first, long_first.data(), sizeof(int32_t) * long_first.size(),
-                            cudaMemcpyHostToDevice, st));
+    auto up = [&](void* dst, const void* src, size_t bytes) {
+      if (bytes) PG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+    };
+    up(s->d_tiles, T.tiles.data(), sizeof(TileDesc) * T.tiles.size());
+    up(s->d_groups, T.groups.data(), sizeof(SegGroup) * T.groups.size());
+    up(s->d_segs, T.segs.data(), sizeof(SegDesc) * T.segs.size());
+    up(s->d_srow, T.srow.data(), sizeof(int32_t) * T.srow.size());
+    up(s->d_sfirst, T.sfirst.data(), sizeof(int32_t) * T.sfirst.size());
+    up(s->d_chunk_seg, T.chunk_seg.data(), sizeof(int32_t) * T.chunk_seg.size());
+    // worklist index: column -> work items (device counting sort by column)
+    {
+      Dirty& D = s->dirty;
+      D.num_tiles = s->num_tiles;
+      D.nsrow = s->nsrow;
+      D.enabled = (cfg->flags & PG_FLAG_WORKLIST) != 0;
+      const size_t nflags = 2 * ((size_t)s->num_tiles + s->nsrow);
+      s->d_flags = dalloc<uint8_t>(nflags);
+      D.tile_flag = s->d_flags;
+      D.srow_flag = D.tile_flag + 2 * (size_t)s->num_tiles;
+      if (D.enabled) {
+        s->d_col_ptr = dalloc<int32_t>((size_t)n + 1);
+        s->d_col_item = dalloc<int32_t>(nnz);
+        int32_t* code = dalloc<int32_t>(m);
+        int32_t* cnt = dalloc<int32_t>((size_t)n + 1);
+        PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)n + 1), st));
+        k_row_codes<<<s->grid_for(std::max<int64_t>(s->num_tiles, m), 256), 256, 0, st>>>(
+            s->d_tiles, s->num_tiles, (int)s->tile_rows, m, code);
+        if (m) k_csc_count<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
+            s->d_row_ptr, s->d_colx, m, cnt);
+        size_t tmp_bytes = 0;
+        PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, s->d_col_ptr, n + 1, st));
+        void* tmp = dalloc<unsigned char>(tmp_bytes);
+        PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, s->d_col_ptr, n + 1, st));
+        PG_CUDA(cudaMemcpyAsync(cnt, s->d_col_ptr, sizeof(int32_t) * ((size_t)n + 1),
+                                cudaMemcpyDeviceToDevice, st));
+        if (m) k_csc_fill<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
+            s->d_row_ptr, s->d_colx, code, m, cnt, s->d_col_item);
+        PG_CUDA(cudaGetLastError());
+        PG_CUDA(cudaStreamSynchronize(st));
+        cudaFree(tmp);
+        cudaFree(code);
+        cudaFree(cnt);
+        D.col_ptr = s->d_col_ptr;
+        D.col_item = s->d_col_item;
+      }
+    }
     s->upload_bounds(p->lower, p->upper);
     PG_CUDA(cudaGetLastError());
     PG_CUDA(cudaStreamSynchronize(st));
-    cudaFree(d_integral);
+    for (void* q : {(void*)t_rp, (void*)t_cols, (void*)t_vals, (void*)t_lhs, (void*)t_rhs,
+                    (void*)t_perm})
+      cudaFree(q);
     if (cfg->loop_mode == PG_LOOP_GRAPH) s->build_graph();
     return s;
   } catch (...) {
@@ -463,7 +627,7 @@ void pg_config_default(pg_config* c) {
   c->scalar_mode = PG_WIDE64;
   c->device = 0;
   c->loop_mode = PG_LOOP_GRAPH;
-  c->flags = PG_FLAG_ROWCHECK;
+  c->flags = PG_FLAG_ROWCHECK | PG_FLAG_WORKLIST;
 }
 
 int pg_config_validate(const pg_config* cfg) {
@@ -657,8 +821,10 @@ int pg_session_time_round_kernel(pg_session* s, int32_t reps, double* mean_ns, d
     *mean_ns = total * 1e6 / reps;
     // algorithmic bytes of one k_tiles launch: vals+col per entry, row_ptr,
     // lhs/rhs per row, tile descriptors, one snapshot read per column
-    *bytes = 12.0 * (double)s->tile_nnz + 4.0 * (double)(s->tile_rows + s->num_tiles) +
-             16.0 * (double)s->tile_rows + 8.0 * s->num_tiles + 16.0 * (double)s->n;
+    // algorithmic bytes of one k_round launch (SURVEY.md 8(d) terms it owns):
+    // vals + col per entry, row_ptr, lhs/rhs, one {lb, ub} read per column
+    *bytes = 12.0 * (double)s->nnz + 4.0 * (double)(s->m + 1) + 16.0 * (double)s->m +
+             16.0 * (double)s->n;
     return PG_OK;
   });
 }
@@ -668,8 +834,8 @@ int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info) {
     g_err = "NULL argument";
     return PG_EINVAL;
   }
-  const int64_t v[] = {s->m, s->n, s->nnz, s->num_tiles, s->nlong, s->nchunks,
-                       s->tile_rows, s->tile_nnz, s->long_nnz};
+  const int64_t v[] = {s->m, s->n, s->nnz, s->num_tiles, s->nsrow, s->nseg,
+                       s->tile_rows, s->tile_nnz, s->seg_nnz};
   for (int i = 0; i < n_info && i < (int)(sizeof(v) / sizeof(v[0])); ++i) info[i] = v[i];
   return PG_OK;
 }

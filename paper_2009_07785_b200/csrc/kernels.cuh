@@ -1,21 +1,25 @@
 // kernels.cuh -- the round-synchronous propagation round on sm_100a.
 //
-// One round (par_engine.cpp:174-200 run_round + process_block :126-171):
-//   k_tiles        rows of <= long_t entries, CSR-stream tiles of <= 1024
-//                  entries: coalesced loads of vals/col, one 16 B gather of
-//                  the {lb,ub} key pair per entry, activities summed per row in
-//                  entry order from shared memory (bit-exact with cpu_par),
-//                  candidates + tighten vs the snapshot, 64-bit atomic
-//                  max/min commit of accepted sides.
-//   k_long_partial one warp per nnz_budget chunk of a long row: chunk
-//                  partial activity in entry order (wide_row_activities,
-//                  par_engine.cpp:99-123).
-//   k_long_combine pairwise tree of the chunk partials in index order.
-//   k_long_cand    one CTA per chunk: candidates of the long row.
-//   k_commit       per variable: changes / crossing check / snapshot update
-//                  (par_engine.cpp:191-197), then the last CTA takes the
-//                  round decision (par_engine.cpp:248-266) and sets the CUDA
-//                  graph's WHILE condition: no host round trip per round.
+// One round = run_round + process_block of the reference
+// (par_engine.cpp:126-200), in three launches:
+//
+//   k_round   persistent, work-stealing over two kinds of items:
+//             * segment groups (longest first): 32 segments of long rows
+//               (chunks of nnz_budget entries, wide_row_activities,
+//               par_engine.cpp:99-123); the CTA's 8 warps stage 32 entries of
+//               every segment through shared memory, one lane per segment
+//               sums in entry order;
+//             * short-row tiles: 8 warp tiles of <= 32 rows / <= 128 entries,
+//               one lane per row sums in entry order.
+//             Then the exact candidate pipeline for the entries that pass an
+//             exactness-preserving filter, committed by 64-bit atomics.
+//   k_seg_cand  pass 2 over the segments of long rows that may tighten.
+//   k_commit  per variable: change count, crossing check, next snapshot
+//             record; the last CTA takes the round decision and sets the CUDA
+//             graph's WHILE condition (no host round trip per round).
+//
+// All activity sums follow cpu_par's order exactly, so results are
+// bit-identical to the reference (tests/test_gpu_parity.py).
 #pragma once
 
 #include <math_constants.h>
@@ -24,11 +28,13 @@
 
 namespace pgb {
 
-constexpr int kTileNnz = 1024;
-constexpr int kTileRows = 256;
-constexpr int kTileThreads = 256;
-constexpr int kItems = kTileNnz / kTileThreads;
+#ifndef PG_ROUND_MINB
+#define PG_ROUND_MINB 2
+#endif
+
 constexpr int kCommitThreads = 256;
+constexpr int kRoundThreads = 256;
+constexpr int kRoundWarps = kRoundThreads / 32;
 
 // Device-resident loop state.
 struct DevState {
@@ -41,19 +47,121 @@ struct DevState {
   uint32_t ticket;                   // last-CTA election in k_commit
   uint32_t ticket_reset;             // last-CTA election in k_reset
   int32_t crossed;
-  int32_t pad;
+  int32_t wl_count;                  // pass-2 worklist length of the current round
+  int32_t work;                      // k_round work-stealing counter
+  int32_t full;                      // 1: every work item is dirty (first round)
+  int32_t frac_any;                  // an integral column has a fractional start bound
+  int32_t frac_tmp;                  // k_reset's accumulator of frac_any
 };
 
-struct LongChunk {
-  int32_t slot;   // long-row slot
-  int32_t k0;     // first entry
-  int32_t k1;     // one past last entry
-  int32_t pad;
+// Device-side worklist (PG_FLAG_WORKLIST): a round only
+// visits work items containing a row with a variable changed in the previous
+// round.  Exact under snapshot semantics: a row none of whose bounds changed
+// yields the same candidates, already accepted or rejected against the same
+// bounds (the reference's marking, seq_engine.cpp:29,37-38,77, by analogy).
+// The commit marks, with plain idempotent stores, the warp tile or the
+// segment row of every row containing a changed column; k_round skips
+// clean tiles and segment groups none of whose rows is marked.
+struct Dirty {
+  const int32_t* col_ptr;   // [n+1] column -> its work-item codes
+  const int32_t* col_item;  // code >= 0: warp tile; code < 0: segment row -1-code
+  uint8_t* tile_flag;       // [2][num_tiles], by round parity
+  uint8_t* srow_flag;       // [2][nsrow]
+  int32_t num_tiles, nsrow;
+  int32_t enabled;
 };
 
-// ---- helpers ------------------------------------------------------------------
-__device__ __forceinline__ longlong2 ld_key(const longlong2* p) { return __ldg(p); }
+// Per-column snapshot record, gathered with one 256-bit load per entry.
+//   lo, up  the round's input bounds (bounds_in of par_engine.cpp:162)
+//   q       filter coefficient (see entry_x), +inf = always examine
+//   flags   bit 0: integral column
+struct __align__(32) Snap {
+  double lo;
+  double up;
+  double q;
+  long long flags;
+};
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void ld_snap(const Snap* p, double& lo, double& up, double& q) {
+  long long f;
+  asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];"
+      : "=d"(lo), "=d"(up), "=d"(q), "=l"(f)
+      : "l"(p));
+}
+
+// ---- exactness-preserving filters -----------------------------------------------
+// (only compute candidates that may improve.)  For an entry
+// with slack S = rhs - min_activity, the rhs-side candidate of the bound it
+// touches (ub for a > 0, lb for a < 0) equals lb + S/a resp. ub - S/|a|, and
+// tighten() can accept it only if S < |a| (ub - lb - thr), where thr >=
+// abs + rel (the smallest possible step, propcore.hpp:168) for continuous
+// variables and thr = integrality_eps for integral ones with integral bounds
+// (floor(c + eps) < ub - step forces c < ub - eps).  Symmetrically for the
+// lhs side with S = max_activity - lhs.  The tests keep a margin of 2^-40
+// times the operand magnitudes, far above the few-ulp rounding error of the
+// reference pipeline, so whatever they skip the reference would have
+// rejected too.  q precomputes, per column,
+//   q = (ub - lb - thr) + 2^-40 (|lb| + |ub|)
+// (+inf for an infinite bound or an integral column with a fractional
+// bound), so an entry's term is x = |a| q.
+constexpr double kMargin = 0x1p-40;
+
+__device__ __forceinline__ double column_q(double lo, double up, bool integral,
+                                           const DevCfg& c) {
+  if (isinf(lo) || isinf(up)) return CUDART_INF;
+  if (integral && (lo != floor(lo) || up != ceil(up))) return CUDART_INF;
+  const double thr = integral ? c.int_eps : c.imp_abs + c.imp_rel;
+  return ((up - lo) - thr) + (fabs(lo) + fabs(up)) * kMargin;
+}
+
+// Row thresholds: an entry can tighten through the rhs side only if
+// x >= tr (or, with exactly one infinite min-contribution, if it is that
+// entry), likewise lhs.  A side that cannot tighten anything (infinite side,
+// or two or more infinite contributions) is switched off.
+struct RowFilter {
+  double tr, tl;
+  uint8_t mode;  // bit0 rhs threshold on, bit1 lhs threshold on, bit2 rhs one-inf, bit3 lhs one-inf
+};
+
+__device__ __forceinline__ RowFilter row_filter(const Act& act, double lhs, double rhs) {
+  RowFilter f = {0.0, 0.0, 0};
+  if (!isinf(rhs)) {
+    if (act.min_i == 0) {
+      f.tr = (rhs - act.min_f) - (fabs(rhs) + fabs(act.min_f)) * kMargin;
+      if (isnan(f.tr)) f.tr = -CUDART_INF;  // must not skip anything
+      f.mode |= 1;
+    } else if (act.min_i == 1) {
+      f.mode |= 4;
+    }
+  }
+  if (!isinf(lhs)) {
+    if (act.max_i == 0) {
+      f.tl = (act.max_f - lhs) - (fabs(lhs) + fabs(act.max_f)) * kMargin;
+      if (isnan(f.tl)) f.tl = -CUDART_INF;
+      f.mode |= 2;
+    } else if (act.max_i == 1) {
+      f.mode |= 8;
+    }
+  }
+  return f;
+}
+
+__device__ __forceinline__ bool row_may(const RowFilter& f, double xmax) {
+  return (f.mode & 12) || ((f.mode & 1) && !(f.tr > xmax)) || ((f.mode & 2) && !(f.tl > xmax));
+}
+
+// pmin_inf / pmax_inf: the entry's min/max contribution is infinite
+__device__ __forceinline__ bool entry_may(const RowFilter& f, double x, bool pmin_inf,
+                                          bool pmax_inf) {
+  return ((f.mode & 1) && !(f.tr > x)) || ((f.mode & 2) && !(f.tl > x)) ||
+         ((f.mode & 4) && pmin_inf) || ((f.mode & 8) && pmax_inf);
+}
+
+// ---- exact candidate pipeline ---------------------------------------------------
 __device__ __forceinline__ void commit_side(long long* key_out, int j, int kind, double cl,
                                             double cu) {
   // merge_lower / merge_upper (par_engine.cpp:56-71) as exact 64-bit max/min
@@ -69,187 +177,626 @@ __device__ __forceinline__ void commit_side(long long* key_out, int j, int kind,
   }
 }
 
-// ---- K1: tiles of short rows --------------------------------------------------
+// residual -> candidates -> tighten vs the snapshot -> merge
+// (propcore.hpp:78-208, par_engine.cpp:158-168).  Returns true on EmptyDomain.
+__device__ __forceinline__ bool entry_pipeline(const Act& act, double a, double lo, double up,
+                                               double lhs, double rhs, int32_t cx,
+                                               long long* key_out, const DevCfg& c) {
+  double min_res, max_res, cl, cu;
+  residual(act, a, lo, up, min_res, max_res);
+  candidates(a, lhs, rhs, min_res, max_res, cx < 0, c, cl, cu);
+  const int kind = tighten(lo, up, cl, cu, c);
+  if (kind == 4) return true;  // EmptyDomain: flag, skip the merge (par_engine.cpp:163-166)
+  if (kind) commit_side(key_out, cx & 0x7fffffff, kind, cl, cu);
+  return false;
+}
+
+// min/max contributions (NaN = infinite) and the filter term of one entry
+__device__ __forceinline__ void entry_terms(double a, const Snap* snap, int32_t cx,
+                                            double& pmin, double& pmax, double& x) {
+  double lo, up, q;
+  ld_snap(snap + (cx & 0x7fffffff), lo, up, q);
+  contrib(a, lo, up, pmin, pmax);
+  x = fabs(a) * q;
+}
+
+// ---- work items of k_round ------------------------------------------------------
+constexpr int kShortMax = 16;   // rows up to this length go to warp tiles
+constexpr int kWItems = 4;
+constexpr int kWNnz = 32 * kWItems;
+constexpr int kLongSeg = 256;     // segments longer than this form groups of 8
+
+struct TileDesc {
+  int32_t r0;  // first row (sorted row space)
+  int32_t nr;  // rows (<= 32)
+  int32_t k0;  // first entry
+  int32_t nz;  // entries (<= kWNnz)
+};
+
+struct SegDesc {
+  int32_t k0;
+  int32_t len;
+  int32_t out;    // partial index = first chunk of the row + chunk number
+  int32_t rslot;  // segment-row slot
+};
+
+struct SegGroup {
+  int32_t first;  // first segment (segments sorted by length, descending)
+  int32_t count;  // 32, or 8 for long segments (shorter tail per group)
+};
+
+struct SegPartial {
+  double min_f;
+  double max_f;
+  double xmax;
+  int32_t min_i;
+  int32_t max_i;
+};
+
+// transposed staging of a segment group: [entry][segment], padded
+constexpr int kSegStage = 2304;  // >= 64 x 33 and >= 256 x 9
+struct SegGroupSmem {
+  double pmin[kSegStage];
+  double pmax[kSegStage];
+  double xmax[32];
+  int32_t cmin[32], cmax[32];
+  SegDesc desc[32];
+};
+
+struct RoundArgs {
+  const TileDesc* tiles;  // warp tiles of short rows (sorted row space)
+  int32_t num_tiles;
+  const SegDesc* segs;    // segments sorted by length, descending
+  int32_t nseg;
+  const SegGroup* groups;
+  int32_t ngroups;
+  const int32_t* srow;    // segment-row slot -> sorted row
+  const int32_t* sfirst;  // segment-row slot -> first partial (+1 sentinel)
+  const int32_t* chunk_seg;  // partial index -> segment index
+  int32_t* row_done;      // per segment row: chunks finished this round
+  SegPartial* partial;
+  Act* row_act;
+  int32_t* worklist;
+  const int32_t* row_ptr;
+  const int32_t* colx;
+  const double* vals;
+  const double* lhs;
+  const double* rhs;
+  const Snap* snap;
+  long long* key_out;
+  DevState* st;
+  Dirty dirty;
+};
+
+// finite contributions (0 for an infinite bound: adding +-0 to a sum that
+// starts at +0 is exact) and infinity flags, propcore.hpp:50-62
+__device__ __forceinline__ void entry_terms_clean(double a, const Snap* snap, int32_t cx,
+                                                  double& pmin, double& pmax, double& x,
+                                                  bool& imin, bool& imax) {
+  double lo, up, q;
+  ld_snap(snap + (cx & 0x7fffffff), lo, up, q);
+  const double bmin = a > 0 ? lo : up;
+  const double bmax = a > 0 ? up : lo;
+  imin = isinf(bmin);
+  imax = isinf(bmax);
+  pmin = imin ? 0.0 : __dmul_rn(a, bmin);
+  pmax = imax ? 0.0 : __dmul_rn(a, bmax);
+  x = fabs(a) * q;
+}
+
+// Row of a segment finished: tree over its chunk partials (in chunk order,
+// par_engine.cpp:117-121), row check, filter; rows that may tighten push
+// their segments onto the pass-2 worklist.
 template <bool kRowCheck>
-__global__ void __launch_bounds__(kTileThreads)
-    k_tiles(const int2* __restrict__ tiles, const int32_t* __restrict__ row_ptr,
-            const int32_t* __restrict__ colx, const double* __restrict__ vals,
-            const double* __restrict__ lhs, const double* __restrict__ rhs,
-            const longlong2* __restrict__ key_in, long long* __restrict__ key_out,
-            DevState* __restrict__ st, const DevCfg cfg) {
-  __shared__ double s_pmin[kTileNnz];
-  __shared__ double s_pmax[kTileNnz];
-  __shared__ Act s_act[kTileRows];
-  __shared__ double s_lhs[kTileRows];
-  __shared__ double s_rhs[kTileRows];
-  __shared__ int32_t s_rp[kTileRows + 1];
-  __shared__ uint8_t s_row[kTileNnz];
-  __shared__ int32_t s_inf;
+__device__ void finish_seg_row(const RoundArgs& A, int rs, const DevCfg& cfg) {
+  const int first = A.sfirst[rs];
+  int np = A.sfirst[rs + 1] - first;
+  const int nch = np;
+  volatile SegPartial* P = A.partial + first;
+  double xmax = -CUDART_INF;
+  for (int i = 0; i < np; ++i) xmax = fmax(xmax, P[i].xmax);
+  while (np > 1) {
+    int out = 0;
+    for (int i = 0; i + 1 < np; i += 2) {
+      const Act a = {P[i].min_f, P[i].max_f, P[i].min_i, P[i].max_i};
+      const Act b = {P[i + 1].min_f, P[i + 1].max_f, P[i + 1].min_i, P[i + 1].max_i};
+      const Act r = act_combine(a, b);
+      P[out].min_f = r.min_f;
+      P[out].max_f = r.max_f;
+      P[out].min_i = r.min_i;
+      P[out].max_i = r.max_i;
+      ++out;
+    }
+    if (np & 1) {
+      P[out].min_f = P[np - 1].min_f;
+      P[out].max_f = P[np - 1].max_f;
+      P[out].min_i = P[np - 1].min_i;
+      P[out].max_i = P[np - 1].max_i;
+      ++out;
+    }
+    np = out;
+  }
+  const Act act = {P[0].min_f, P[0].max_f, P[0].min_i, P[0].max_i};
+  A.row_act[rs] = act;
+  const int row = A.srow[rs];
+  const double l = A.lhs[row], h = A.rhs[row];
+  if (kRowCheck && row_infeasible(act, l, h, cfg)) A.st->infeasible = 1;
+  if (row_may(row_filter(act, l, h), xmax)) {
+    const int pos = atomicAdd(&A.st->wl_count, nch);
+    for (int i = 0; i < nch; ++i) A.worklist[pos + i] = A.chunk_seg[first + i];
+  }
+}
 
+// One group of G segments of near-equal length by the whole CTA: the 8
+// warps stage SC = (256/G) x 8 entries of every segment per step
+// (coalesced runs per segment), one lane per segment sums them in entry
+// order.  G = 8 for long segments keeps the per-group critical path short.
+template <bool kRowCheck, int G>
+__device__ void seg_group(const RoundArgs& A, SegGroupSmem& S, const SegGroup grp,
+                          const uint8_t* sflag, const DevCfg& cfg) {
+  constexpr int TPS = kRoundThreads / G;  // threads per segment
+  constexpr int E = 8;                    // entries per thread per step
+  constexpr int SC = TPS * E;             // entries per segment per step
+  constexpr int LD = G + 1;               // padded stride
+  static_assert(SC * LD <= kSegStage, "staging too small");
   const int tid = threadIdx.x;
-  const int2 tl = tiles[blockIdx.x];
-  const int r0 = tl.x;
-  const int nr = tl.y - tl.x;
-  if (tid == 0) s_inf = 0;
-  for (int i = tid; i <= nr; i += kTileThreads) s_rp[i] = row_ptr[r0 + i];
+  if (tid < G) S.desc[tid] = tid < grp.count ? A.segs[grp.first + tid] : SegDesc{0, 0, -1, -1};
   __syncthreads();
-  const int k0 = s_rp[0];
-  const int nz = s_rp[nr] - k0;
-
-  // phase 1: coalesced entry loads + one 16 B snapshot gather per entry
-  double a[kItems], lo[kItems], up[kItems];
-  int32_t cx[kItems];
+  const int L = S.desc[0].len;  // sorted descending
+  const int ls = tid / TPS, sub = tid % TPS;
+  const int my_k0 = S.desc[ls].k0, my_len = S.desc[ls].len;
+  double smin = 0.0, smax = 0.0;  // chain sums (lanes < G of warp 0)
+  double xm = -CUDART_INF;
+  int cmin = 0, cmax = 0;
+  for (int c0 = 0; c0 < L; c0 += SC) {
+    double av[E];
+    int32_t cv[E];
 #pragma unroll
-  for (int q = 0; q < kItems; ++q) {
-    const int e = tid + q * kTileThreads;
-    if (e < nz) {
-      cx[q] = __ldg(colx + k0 + e);
-      a[q] = __ldg(vals + k0 + e);
+    for (int j = 0; j < E; ++j) {
+      const int i = c0 + sub + TPS * j;
+      if (i < my_len) {
+        cv[j] = __ldg(A.colx + my_k0 + i);
+        av[j] = __ldg(A.vals + my_k0 + i);
+      }
     }
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+      const int i = c0 + sub + TPS * j;
+      if (i < my_len) {
+        double pmin, pmax, x;
+        bool imin, imax;
+        entry_terms_clean(av[j], A.snap, cv[j], pmin, pmax, x, imin, imax);
+        S.pmin[(sub + TPS * j) * LD + ls] = pmin;
+        S.pmax[(sub + TPS * j) * LD + ls] = pmax;
+        xm = fmax(xm, x);
+        cmin += imin;
+        cmax += imax;
+      }
+    }
+    __syncthreads();
+    if (tid < G) {
+      const int n = min(SC, S.desc[tid].len - c0);
+      for (int i = 0; i < n; ++i) {
+        smin = __dadd_rn(smin, S.pmin[i * LD + tid]);
+        smax = __dadd_rn(smax, S.pmax[i * LD + tid]);
+      }
+    }
+    __syncthreads();
   }
+  // per-segment reduction of the order-free parts over its TPS threads
 #pragma unroll
-  for (int q = 0; q < kItems; ++q) {
-    const int e = tid + q * kTileThreads;
-    if (e < nz) {
-      const longlong2 kk = ld_key(key_in + (cx[q] & 0x7fffffff));
-      lo[q] = key_dec(kk.x);
-      up[q] = key_dec(kk.y);
-      double pmin, pmax;
-      contrib(a[q], lo[q], up[q], pmin, pmax);
-      s_pmin[e] = pmin;
-      s_pmax[e] = pmax;
-    }
+  for (int o = 1; o < TPS && o < 32; o <<= 1) {
+    xm = fmax(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+    cmin += __shfl_xor_sync(0xffffffffu, cmin, o);
+    cmax += __shfl_xor_sync(0xffffffffu, cmax, o);
+  }
+  if (sub == 0) {
+    S.xmax[ls] = xm;
+    S.cmin[ls] = cmin;
+    S.cmax[ls] = cmax;
   }
   __syncthreads();
-
-  // phase 2: one thread per row, sum in entry order (propcore.hpp:50-63)
-  for (int r = tid; r < nr; r += kTileThreads) {
-    const int b = s_rp[r] - k0, e = s_rp[r + 1] - k0;
-    Act act = {0.0, 0.0, 0, 0};
-    for (int k = b; k < e; ++k) {
-      act_add(act, s_pmin[k], s_pmax[k]);
-      s_row[k] = (uint8_t)r;
-    }
-    s_act[r] = act;
-    const double l = lhs[r0 + r], h = rhs[r0 + r];
-    s_lhs[r] = l;
-    s_rhs[r] = h;
-    if (kRowCheck && row_infeasible(act, l, h, cfg)) s_inf = 1;
-  }
-  __syncthreads();
-
-  // phase 3: candidates vs the frozen snapshot, atomic commit
-#pragma unroll
-  for (int q = 0; q < kItems; ++q) {
-    const int e = tid + q * kTileThreads;
-    if (e < nz) {
-      const int r = s_row[e];
-      const Act act = s_act[r];
-      double min_res, max_res, cl, cu;
-      residual(act, a[q], lo[q], up[q], min_res, max_res);
-      candidates(a[q], s_lhs[r], s_rhs[r], min_res, max_res, cx[q] < 0, cfg, cl, cu);
-      const int kind = tighten(lo[q], up[q], cl, cu, cfg);
-      if (kind == 4) {
-        s_inf = 1;  // EmptyDomain: flag, skip the merge (par_engine.cpp:163-166)
-      } else if (kind) {
-        commit_side(key_out, cx[q] & 0x7fffffff, kind, cl, cu);
+  // with the worklist, a dirty group may hold clean rows: only dirty rows are
+  // finished (a clean multi-chunk row may be missing chunks of clean groups)
+  if (tid < G && S.desc[tid].out >= 0 && (!sflag || sflag[S.desc[tid].rslot])) {
+    const SegDesc d = S.desc[tid];
+    const Act acc = {smin, smax, S.cmin[tid], S.cmax[tid]};
+    const double xmax = S.xmax[tid];
+    const int first = A.sfirst[d.rslot];
+    const int nch = A.sfirst[d.rslot + 1] - first;
+    if (nch == 1) {
+      // the segment is the whole row: finish it here
+      A.row_act[d.rslot] = acc;
+      const int row = A.srow[d.rslot];
+      const double l = A.lhs[row], h = A.rhs[row];
+      if (kRowCheck && row_infeasible(acc, l, h, cfg)) A.st->infeasible = 1;
+      if (row_may(row_filter(acc, l, h), xmax)) {
+        const int pos = atomicAdd(&A.st->wl_count, 1);
+        A.worklist[pos] = grp.first + tid;
+      }
+    } else {
+      volatile SegPartial* P = A.partial + d.out;
+      P->min_f = acc.min_f;
+      P->max_f = acc.max_f;
+      P->xmax = xmax;
+      P->min_i = acc.min_i;
+      P->max_i = acc.max_i;
+      __threadfence();
+      if (atomicAdd(&A.row_done[d.rslot], 1) == nch - 1) {
+        __threadfence();
+        A.row_done[d.rslot] = 0;
+        finish_seg_row<kRowCheck>(A, d.rslot, cfg);
       }
     }
   }
   __syncthreads();
-  if (tid == 0 && s_inf) st->infeasible = 1;
 }
 
-// ---- long rows ----------------------------------------------------------------
-// One warp per chunk; lanes load 32 entries at a time (coalesced) and the
-// products are folded in entry order through warp shuffles.
-__global__ void __launch_bounds__(256)
-    k_long_partial(const LongChunk* __restrict__ chunks, int nchunks,
-                   const int32_t* __restrict__ colx, const double* __restrict__ vals,
-                   const longlong2* __restrict__ key_in, Act* __restrict__ partial) {
-  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (w >= nchunks) return;
-  const LongChunk ch = chunks[w];
-  Act acc = {0.0, 0.0, 0, 0};
-  for (int base = ch.k0; base < ch.k1; base += 32) {
-    const int k = base + lane;
-    double pmin = 0.0, pmax = 0.0;
-    if (k < ch.k1) {
-      const int32_t c = __ldg(colx + k);
-      const double a = __ldg(vals + k);
-      const longlong2 kk = ld_key(key_in + (c & 0x7fffffff));
-      contrib(a, key_dec(kk.x), key_dec(kk.y), pmin, pmax);
-    }
-    const int cnt = min(32, ch.k1 - base);
-    for (int s = 0; s < cnt; ++s) {
-      const double vmin = __shfl_sync(0xffffffffu, pmin, s);
-      const double vmax = __shfl_sync(0xffffffffu, pmax, s);
-      act_add(acc, vmin, vmax);
+// number of set bits of the 128-bit mask m[0..3] in [b, e)
+__device__ __forceinline__ int popc_range(const unsigned (&m)[kWItems], int b, int e) {
+  int c = 0;
+#pragma unroll
+  for (int q = 0; q < kWItems; ++q) {
+    const int lo = max(b - 32 * q, 0), hi = min(e - 32 * q, 32);
+    if (lo < hi) {
+      const unsigned keep = (hi == 32 ? 0xffffffffu : ((1u << hi) - 1u)) & ~((1u << lo) - 1u);
+      c += __popc(m[q] & keep);
     }
   }
-  if (lane == 0) partial[w] = acc;
+  return c;
 }
 
-// Pairwise tree over a long row's chunk partials in index order
-// (par_engine.cpp:117-121); optional Step-2 row check.
+// ---- short rows: warp tiles with per-warp asynchronous staging -------------------
+// Each warp owns a contiguous run of warp tiles (<= 32 consecutive rows of
+// <= kShortMax entries, <= 128 entries) and pipelines them three deep:
+//   tile i+2: TMA bulk copies of its vals/col streams -> shared memory
+//   tile i+1: cp.async gathers of the 16 B {lb, ub} snapshot of every entry
+//   tile i:   compute (one lane per row, sums in entry order)
+// Neither stage holds registers, so a warp keeps ~256 gathers in flight with
+// no CTA barrier.  Rows are stored sorted by length (session init).
+constexpr int kTWarps = 4;
+constexpr int kTStages = 3;
+
+struct __align__(16) TileStage {
+  double vals[kWNnz + 2];   // +2 / +4: the bulk copies start 16 B aligned
+  int32_t cols[kWNnz + 4];
+  double2 rec[kWNnz];       // {lb, ub} of every entry's column
+  int32_t rp[36];           // row_ptr slice of the tile's rows
+  double lhs[34];
+  double rhs[34];
+  TileDesc d;
+};
+
+struct TileWarpSmem {
+  TileStage stage[kTStages];
+  uint64_t bar[kTStages];
+  double pmin[kWNnz];       // finite min contributions (0 for infinite ones)
+  double pmax[kWNnz];
+  double x[kWNnz];          // filter terms
+  double minf[32], maxf[32], lhs[32], rhs[32], tr[32], tl[32];
+  int32_t mini[32], maxi[32];
+  int32_t rp[33];
+  uint8_t row[kWNnz];
+  uint8_t qe[kWNnz];        // queue: entry index
+  uint8_t mode[32];
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+// lane 0: bulk copies of tile t's entry streams and row data into a stage
+// (device arrays carry >= 16 B of tail padding for the widened ranges)
+__device__ __forceinline__ void tile_issue_tma(const RoundArgs& A, TileStage& S, uint64_t* bar,
+                                               const TileDesc d) {
+  S.d = d;
+  const int kv = d.k0 & ~1, kc = d.k0 & ~3, k1 = d.k0 + d.nz;
+  const uint32_t bv = (uint32_t)(((k1 - kv) * 8 + 15) & ~15);
+  const uint32_t bc = (uint32_t)(((k1 - kc) * 4 + 15) & ~15);
+  const int rr = d.r0 & ~3, rd = d.r0 & ~1;
+  const uint32_t br = (uint32_t)(((d.r0 + d.nr + 1 - rr) * 4 + 15) & ~15);
+  const uint32_t bs = (uint32_t)(((d.r0 + d.nr - rd) * 8 + 15) & ~15);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  mbar_expect_tx(bar, bv + bc + br + 2 * bs);
+  bulk_g2s(S.vals, A.vals + kv, bv, bar);
+  bulk_g2s(S.cols, A.colx + kc, bc, bar);
+  bulk_g2s(S.rp, A.row_ptr + rr, br, bar);
+  bulk_g2s(S.lhs, A.lhs + rd, bs, bar);
+  bulk_g2s(S.rhs, A.rhs + rd, bs, bar);
+}
+
+// all lanes: 16 B snapshot gathers of a staged tile (one cp.async group)
+__device__ __forceinline__ void tile_issue_gathers(const RoundArgs& A, TileStage& S, int lane) {
+  const int oc = S.d.k0 & 3;
+#pragma unroll
+  for (int q = 0; q < kWItems; ++q) {
+    const int e = lane + 32 * q;
+    if (e < S.d.nz) cp_async16(&S.rec[e], &A.snap[S.cols[oc + e] & 0x7fffffff].lo);
+  }
+  cp_async_commit();
+}
+
+// filter coefficient of a column computed from its bounds (column_q);
+// frac_any = some integral column may carry a fractional bound
+__device__ __forceinline__ double column_q_fast(double lo, double up, bool integral,
+                                                bool frac_any, const DevCfg& c) {
+  if (isinf(lo) || isinf(up)) return CUDART_INF;
+  if (frac_any && integral && (lo != floor(lo) || up != ceil(up))) return CUDART_INF;
+  const double thr = integral ? c.int_eps : c.imp_abs + c.imp_rel;
+  return ((up - lo) - thr) + (fabs(lo) + fabs(up)) * kMargin;
+}
+
 template <bool kRowCheck>
-__global__ void k_long_combine(const int32_t* __restrict__ long_rows,
-                               const int32_t* __restrict__ long_first_chunk, int nlong,
-                               Act* __restrict__ partial, Act* __restrict__ long_act,
-                               const double* __restrict__ lhs, const double* __restrict__ rhs,
-                               DevState* __restrict__ st, const DevCfg cfg) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nlong) return;
-  Act* P = partial + long_first_chunk[s];
-  int np = long_first_chunk[s + 1] - long_first_chunk[s];
-  while (np > 1) {
-    int out = 0;
-    for (int i = 0; i + 1 < np; i += 2) P[out++] = act_combine(P[i], P[i + 1]);
-    if (np & 1) P[out++] = P[np - 1];
-    np = out;
+__device__ void tile_compute(const RoundArgs& A, TileWarpSmem& W, const TileStage& S,
+                             bool frac_any, bool& inf_flag, const DevCfg& cfg) {
+  const int lane = threadIdx.x & 31;
+  const TileDesc d = S.d;
+  const int nr = d.nr, nz = d.nz;
+  const int ov = d.k0 & 1, oc = d.k0 & 3, orp = d.r0 & 3, ors = d.r0 & 1;
+  W.rp[lane] = S.rp[orp + min(lane, nr)] - d.k0;
+  if (lane == 0) W.rp[nr] = nz;
+
+  // phase 1: contributions and filter terms from the staged entries
+  unsigned mmin[kWItems], mmax[kWItems];
+#pragma unroll
+  for (int q = 0; q < kWItems; ++q) {
+    const int e = lane + 32 * q;
+    bool imin = false, imax = false;
+    if (e < nz) {
+      const double a = S.vals[ov + e];
+      const int32_t cx = S.cols[oc + e];
+      const double2 r = S.rec[e];
+      const double bmin = a > 0 ? r.x : r.y;
+      const double bmax = a > 0 ? r.y : r.x;
+      imin = isinf(bmin);
+      imax = isinf(bmax);
+      W.pmin[e] = imin ? 0.0 : __dmul_rn(a, bmin);
+      W.pmax[e] = imax ? 0.0 : __dmul_rn(a, bmax);
+      W.x[e] = fabs(a) * column_q_fast(r.x, r.y, cx < 0, frac_any, cfg);
+    }
+    mmin[q] = __ballot_sync(0xffffffffu, imin);
+    mmax[q] = __ballot_sync(0xffffffffu, imax);
   }
-  const Act act = P[0];
-  long_act[s] = act;
-  if (kRowCheck) {
-    const int row = long_rows[s];
-    if (row_infeasible(act, lhs[row], rhs[row], cfg)) st->infeasible = 1;
+  __syncwarp();
+
+  // phase 2: one lane per row, sums in entry order (propcore.hpp:50-63)
+  bool may = false;
+  if (lane < nr) {
+    const int b = W.rp[lane], e = W.rp[lane + 1];
+    double smin = 0.0, smax = 0.0, xmax = -CUDART_INF;
+    for (int k = b; k < e; ++k) {
+      smin = __dadd_rn(smin, W.pmin[k]);
+      smax = __dadd_rn(smax, W.pmax[k]);
+      xmax = fmax(xmax, W.x[k]);
+      W.row[k] = (uint8_t)lane;
+    }
+    const Act act = {smin, smax, popc_range(mmin, b, e), popc_range(mmax, b, e)};
+    const double l = S.lhs[ors + lane], h = S.rhs[ors + lane];
+    if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
+    const RowFilter f = row_filter(act, l, h);
+    may = row_may(f, xmax);
+    W.minf[lane] = act.min_f;
+    W.maxf[lane] = act.max_f;
+    W.mini[lane] = act.min_i;
+    W.maxi[lane] = act.max_i;
+    W.lhs[lane] = l;
+    W.rhs[lane] = h;
+    W.tr[lane] = f.tr;
+    W.tl[lane] = f.tl;
+    W.mode[lane] = f.mode;
   }
+  const unsigned may_rows = __ballot_sync(0xffffffffu, may);
+  __syncwarp();
+  if (may_rows == 0) return;  // no row of this tile can tighten anything
+
+  // phase 3: entry filter, compaction into a warp queue, dense exact pipeline
+  int qn = 0;
+#pragma unroll
+  for (int q = 0; q < kWItems; ++q) {
+    const int e = lane + 32 * q;
+    bool pass = false;
+    if (e < nz) {
+      const int r = W.row[e];
+      if ((may_rows >> r) & 1u) {
+        const RowFilter f = {W.tr[r], W.tl[r], W.mode[r]};
+        pass = entry_may(f, W.x[e], (mmin[q] >> lane) & 1u, (mmax[q] >> lane) & 1u);
+      }
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, pass);
+    if (pass) W.qe[qn + __popc(m & ((1u << lane) - 1u))] = (uint8_t)e;
+    qn += __popc(m);
+  }
+  __syncwarp();
+  for (int i = lane; i < qn; i += 32) {
+    const int e = W.qe[i];
+    const int r = W.row[e];
+    const double2 rc = S.rec[e];
+    const Act act = {W.minf[r], W.maxf[r], W.mini[r], W.maxi[r]};
+    if (entry_pipeline(act, S.vals[ov + e], rc.x, rc.y, W.lhs[r], W.rhs[r], S.cols[oc + e],
+                       A.key_out, cfg))
+      inf_flag = true;
+  }
+  __syncwarp();
 }
 
+template <bool kRowCheck>
+__global__ void __launch_bounds__(kTWarps * 32) k_tiles(const RoundArgs A, const DevCfg cfg) {
+  extern __shared__ __align__(16) unsigned char tiles_smem[];
+  TileWarpSmem& W = reinterpret_cast<TileWarpSmem*>(tiles_smem)[threadIdx.x >> 5];
+  const int lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * kTWarps + (threadIdx.x >> 5);
+  const int nw = gridDim.x * kTWarps;
+  // contiguous run of tiles of this warp (static: no global counter)
+  const int per = (A.num_tiles + nw - 1) / nw;
+  const int tb = min(gw * per, A.num_tiles), te = min(tb + per, A.num_tiles);
+  if (tb >= te) return;
+  const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
+  const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
+  const uint8_t* tflag = A.dirty.tile_flag + (size_t)par * A.dirty.num_tiles;
+  const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
+  // next tile at or after t that must be processed (-1 = none)
+  auto next_tile = [&](int t) -> int {
+    if (full) return t < te ? t : -1;
+    for (; t < te; t += 32) {
+      const bool d = t + lane < te && tflag[t + lane];
+      const unsigned m = __ballot_sync(0xffffffffu, d);
+      if (m) return t + __ffs(m) - 1;
+    }
+    return -1;
+  };
+  if (lane == 0)
+    for (int i = 0; i < kTStages; ++i) mbar_init(&W.bar[i], 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncwarp();
+
+  // descriptors of a 32-tile window, one per lane (one coalesced load per window)
+  int wbase = -1;
+  TileDesc wdesc = {0, 0, 0, 0};
+  auto desc_of = [&](int t) -> TileDesc {
+    if (wbase < 0 || t >= wbase + 32) {
+      wbase = t;
+      if (t + lane < te) wdesc = A.tiles[t + lane];
+    }
+    const int src = t - wbase;
+    TileDesc d;
+    d.r0 = __shfl_sync(0xffffffffu, wdesc.r0, src);
+    d.nr = __shfl_sync(0xffffffffu, wdesc.nr, src);
+    d.k0 = __shfl_sync(0xffffffffu, wdesc.k0, src);
+    d.nz = __shfl_sync(0xffffffffu, wdesc.nz, src);
+    return d;
+  };
+  int tq[kTStages];  // tiles in the pipeline: [0] compute, [1] gathers, [2] TMA
+  tq[0] = next_tile(tb);
+  if (tq[0] < 0) return;
+  tq[1] = next_tile(tq[0] + 1);
+  {
+    const TileDesc d0 = desc_of(tq[0]);
+    const TileDesc d1 = tq[1] >= 0 ? desc_of(tq[1]) : d0;
+    if (lane == 0) {
+      tile_issue_tma(A, W.stage[0], &W.bar[0], d0);
+      if (tq[1] >= 0) tile_issue_tma(A, W.stage[1], &W.bar[1], d1);
+    }
+  }
+  mbar_wait(&W.bar[0], 0);
+  tile_issue_gathers(A, W.stage[0], lane);
+  bool inf_flag = false;
+  for (int i = 0; tq[0] >= 0; ++i) {
+    const int s0 = i % kTStages, s1 = (i + 1) % kTStages, s2 = (i + 2) % kTStages;
+    if (tq[1] >= 0) {
+      mbar_wait(&W.bar[s1], (uint32_t)(((i + 1) / kTStages) & 1));
+      tile_issue_gathers(A, W.stage[s1], lane);
+      tq[2] = next_tile(tq[1] + 1);
+      if (tq[2] >= 0) {
+        const TileDesc d2 = desc_of(tq[2]);
+        if (lane == 0) tile_issue_tma(A, W.stage[s2], &W.bar[s2], d2);
+      }
+      cp_async_wait<1>();
+    } else {
+      tq[2] = -1;
+      cp_async_wait<0>();
+    }
+    __syncwarp();
+    tile_compute<kRowCheck>(A, W, W.stage[s0], frac_any, inf_flag, cfg);
+    tq[0] = tq[1];
+    tq[1] = tq[2];
+  }
+  if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
+}
+
+template <bool kRowCheck>
+__global__ void __launch_bounds__(kRoundThreads, PG_ROUND_MINB) k_round(const RoundArgs A, const DevCfg cfg) {
+  extern __shared__ __align__(16) unsigned char round_smem[];
+  SegGroupSmem& sm = *reinterpret_cast<SegGroupSmem*>(round_smem);
+  __shared__ int32_t s_item;
+  const int lane = threadIdx.x & 31;
+  // full sweep (first round, or no worklist), else skip clean work items
+  const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
+  const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
+  const uint8_t* sflag = A.dirty.srow_flag + (size_t)par * A.dirty.nsrow;
+  const int total = A.ngroups;
+  bool inf_flag = false;
+  for (;;) {
+    if (threadIdx.x == 0) s_item = atomicAdd(&A.st->work, 1);
+    __syncthreads();
+    const int item = s_item;
+    __syncthreads();
+    if (item >= total) break;
+    const SegGroup grp = A.groups[item];
+    if (!full) {
+      // dirty iff a row of one of its segments is marked
+      const bool d = threadIdx.x < grp.count && sflag[A.segs[grp.first + threadIdx.x].rslot];
+      if (!__syncthreads_or(d)) continue;
+    }
+    if (grp.count == 8 || grp.count < 8 && A.segs[grp.first].len > kLongSeg)
+      seg_group<kRowCheck, 8>(A, sm, grp, full ? nullptr : sflag, cfg);
+    else
+      seg_group<kRowCheck, 32>(A, sm, grp, full ? nullptr : sflag, cfg);
+  }
+  if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
+}
+
+// Pass 2 over the worklist: one warp per segment, coalesced re-read (mostly
+// L2 hits), entry filter, exact pipeline, atomic commit.
 __global__ void __launch_bounds__(256)
-    k_long_cand(const LongChunk* __restrict__ chunks, const int32_t* __restrict__ long_rows,
-                const Act* __restrict__ long_act, const int32_t* __restrict__ colx,
-                const double* __restrict__ vals, const double* __restrict__ lhs,
-                const double* __restrict__ rhs, const longlong2* __restrict__ key_in,
-                long long* __restrict__ key_out, DevState* __restrict__ st, const DevCfg cfg) {
-  __shared__ int32_t s_inf;
-  const LongChunk ch = chunks[blockIdx.x];
-  if (threadIdx.x == 0) s_inf = 0;
-  __syncthreads();
-  const Act act = long_act[ch.slot];
-  const int row = long_rows[ch.slot];
-  const double l = lhs[row], h = rhs[row];
-  for (int k = ch.k0 + threadIdx.x; k < ch.k1; k += blockDim.x) {
-    const int32_t c = __ldg(colx + k);
-    const double a = __ldg(vals + k);
-    const longlong2 kk = ld_key(key_in + (c & 0x7fffffff));
-    const double lo = key_dec(kk.x), up = key_dec(kk.y);
-    double min_res, max_res, cl, cu;
-    residual(act, a, lo, up, min_res, max_res);
-    candidates(a, l, h, min_res, max_res, c < 0, cfg, cl, cu);
-    const int kind = tighten(lo, up, cl, cu, cfg);
-    if (kind == 4) s_inf = 1;
-    else if (kind) commit_side(key_out, c & 0x7fffffff, kind, cl, cu);
+    k_seg_cand(const RoundArgs A, const DevCfg cfg) {
+  const int nwl = *((volatile int32_t*)&A.st->wl_count);
+  bool inf_flag = false;
+  for (int w = blockIdx.x; w < nwl; w += gridDim.x) {
+    const SegDesc d = A.segs[A.worklist[w]];
+    const Act act = A.row_act[d.rslot];
+    const int row = A.srow[d.rslot];
+    const double l = A.lhs[row], h = A.rhs[row];
+    const RowFilter f = row_filter(act, l, h);
+    for (int i = threadIdx.x; i < d.len; i += blockDim.x) {
+      const int k = d.k0 + i;
+      const int32_t c = __ldg(A.colx + k);
+      const double a = __ldg(A.vals + k);
+      double lo, up, q;
+      ld_snap(A.snap + (c & 0x7fffffff), lo, up, q);
+      double pmin, pmax;
+      contrib(a, lo, up, pmin, pmax);
+      if (entry_may(f, fabs(a) * q, isnan(pmin), isnan(pmax)) &&
+          entry_pipeline(act, a, lo, up, l, h, c, A.key_out, cfg))
+        inf_flag = true;
+    }
   }
-  __syncthreads();
-  if (threadIdx.x == 0 && s_inf) st->infeasible = 1;
+  if (__any_sync(0xffffffffu, inf_flag) && (threadIdx.x & 31) == 0) A.st->infeasible = 1;
 }
 
-// ---- commit + round decision --------------------------------------------------
+// ---- commit + round decision ------------------------------------------------------
 template <int kThreads>
-__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, int* flag_or,
-                                                        int& f) {
+__device__ __forceinline__ unsigned long long block_sum(unsigned long long v, int& f) {
   __shared__ unsigned long long s_sum[kThreads / 32];
   __shared__ int s_f[kThreads / 32];
   for (int o = 16; o > 0; o >>= 1) {
@@ -272,27 +819,53 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, in
     v = t;
     f = ff;
   }
-  (void)flag_or;
   return v;
 }
 
+// Per variable (par_engine.cpp:191-197): count sides with out != in, flag
+// lo_out > up_out + abs, and write the next round's snapshot record.  The
+// last CTA takes the round decision of run_parallel (par_engine.cpp:248-266).
 __global__ void __launch_bounds__(kCommitThreads)
-    k_commit(longlong2* __restrict__ key_in, const longlong2* __restrict__ key_out, int n,
+    k_commit(Snap* __restrict__ snap, const longlong2* __restrict__ key_out, int n,
              DevState* __restrict__ st, long long* __restrict__ per_round, const DevCfg cfg,
-             cudaGraphConditionalHandle cond, int use_graph) {
+             const Dirty D, cudaGraphConditionalHandle cond, int use_graph) {
   unsigned long long changes = 0;
   int inf = 0;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
-    const longlong2 ki = key_in[j];
+  const int R = *((volatile int32_t*)&st->round);  // rounds before this one
+  const int nb = R & 1;                             // buffer of the next round's lists
+  const int cb = nb ^ 1;                            // buffer this round consumed
+  const int gstride = gridDim.x * blockDim.x;
+  const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int j = gtid; j < n; j += gstride) {
     const longlong2 ko = key_out[j];
-    const int c = (ki.x != ko.x) + (ki.y != ko.y);
+    const double lo = key_dec(ko.x), up = key_dec(ko.y);
+    const double2 in = *reinterpret_cast<const double2*>(&snap[j].lo);
+    // a change is a strict improvement, so comparing values is exact
+    const int c = (lo != in.x) + (up != in.y);
     if (c) {
       changes += c;
-      key_in[j] = ko;
+      const bool integral = snap[j].flags & 1;
+      Snap s = {lo, up, column_q(lo, up, integral, cfg), snap[j].flags};
+      snap[j] = s;
+      if (D.enabled) {
+        // mark the work item of every row containing column j for the next round
+        for (int e = D.col_ptr[j]; e < D.col_ptr[j + 1]; ++e) {
+          const int code = D.col_item[e];
+          if (code >= 0)
+            D.tile_flag[(size_t)nb * D.num_tiles + code] = 1;
+          else
+            D.srow_flag[(size_t)nb * D.nsrow + (-1 - code)] = 1;
+        }
+      }
     }
-    if (key_dec(ko.x) > __dadd_rn(key_dec(ko.y), cfg.imp_abs)) inf = 1;
+    if (lo > __dadd_rn(up, cfg.imp_abs)) inf = 1;
   }
-  changes = block_sum<kCommitThreads>(changes, nullptr, inf);
+  if (D.enabled) {
+    // the consumed buffer is the round-after-next's mark set
+    for (int i = gtid; i < D.num_tiles; i += gstride) D.tile_flag[(size_t)cb * D.num_tiles + i] = 0;
+    for (int i = gtid; i < D.nsrow; i += gstride) D.srow_flag[(size_t)cb * D.nsrow + i] = 0;
+  }
+  changes = block_sum<kCommitThreads>(changes, inf);
   if (threadIdx.x == 0) {
     if (changes) atomicAdd(&st->round_changes, changes);
     if (inf) st->infeasible = 1;
@@ -303,42 +876,52 @@ __global__ void __launch_bounds__(kCommitThreads)
       __threadfence();
       const long long ch = (long long)atomicAdd(&st->round_changes, 0ull);
       const int infeasible = atomicAdd(&st->infeasible, 0);
-      const int r = st->round + 1;
+      const int r = R + 1;
       st->round = r;
       if (r - 1 < cfg.round_limit) per_round[r - 1] = ch;
       st->total_changes += ch;
       int status = -1;
-      if (infeasible) status = 2;             // PG_INFEASIBLE
-      else if (ch == 0) status = 0;           // PG_CONVERGED
+      if (infeasible) status = 2;                 // PG_INFEASIBLE
+      else if (ch == 0) status = 0;               // PG_CONVERGED
       else if (r >= cfg.round_limit) status = 1;  // PG_ROUNDLIMIT
       st->status = status;
       st->done = status >= 0;
       st->round_changes = 0;
       st->infeasible = 0;
       st->ticket = 0;
+      st->wl_count = 0;
+      st->work = 0;
+      st->full = 0;
       __threadfence();
       if (use_graph) cudaGraphSetConditional(cond, status >= 0 ? 0u : 1u);
     }
   }
 }
 
-// Start of a solve: keys from the (normalised) start bounds, state reset,
-// bounds_crossed pre-check (engine_common.hpp:51-58).
+// Start of a solve: snapshot records and merge keys from the (normalised)
+// start bounds, state reset, bounds_crossed pre-check (engine_common.hpp:51-58).
 __global__ void __launch_bounds__(kCommitThreads)
     k_reset(const double* __restrict__ lo0, const double* __restrict__ up0,
-            longlong2* __restrict__ key_in, longlong2* __restrict__ key_out, int n,
-            DevState* __restrict__ st, const DevCfg cfg, int check_crossed,
-            cudaGraphConditionalHandle cond, int use_graph) {
-  int crossed = 0;
+            const uint8_t* __restrict__ integral, Snap* __restrict__ snap,
+            longlong2* __restrict__ key_out, int n, DevState* __restrict__ st, const DevCfg cfg,
+            const Dirty D, int check_crossed, cudaGraphConditionalHandle cond, int use_graph) {
+  int crossed = 0, frac = 0;
+  {
+    const int gstride = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    for (int i = gtid; i < 2 * D.num_tiles; i += gstride) D.tile_flag[i] = 0;
+    for (int i = gtid; i < 2 * D.nsrow; i += gstride) D.srow_flag[i] = 0;
+  }
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const double l = lo0[j], u = up0[j];
-    const longlong2 k = make_longlong2(key_enc(l), key_enc(u));
-    key_in[j] = k;
-    key_out[j] = k;
+    const bool in = integral[j] != 0;
+    snap[j] = Snap{l, u, column_q(l, u, in, cfg), in ? 1LL : 0LL};
+    key_out[j] = make_longlong2(key_enc(l), key_enc(u));
     if (l > __dadd_rn(u, cfg.imp_abs)) crossed = 1;
+    if (in && (l != floor(l) || u != ceil(u))) frac = 1;  // floor(+-inf) = +-inf
   }
+  if (frac) atomicOr(&st->frac_tmp, 1);
   unsigned long long dummy = 0;
-  block_sum<kCommitThreads>(dummy, nullptr, crossed);
+  block_sum<kCommitThreads>(dummy, crossed);
   if (threadIdx.x == 0) {
     if (crossed) atomicOr(&st->crossed, 1);
     __threadfence();
@@ -354,6 +937,11 @@ __global__ void __launch_bounds__(kCommitThreads)
       st->done = cr;
       st->ticket = 0;
       st->crossed = 0;
+      st->wl_count = 0;
+      st->work = 0;
+      st->full = 1;
+      st->frac_any = atomicAdd(&st->frac_tmp, 0);
+      st->frac_tmp = 0;
       st->ticket_reset = 0;
       __threadfence();
       if (use_graph) cudaGraphSetConditional(cond, cr ? 0u : 1u);
@@ -379,13 +967,65 @@ __global__ void k_normalize(double* __restrict__ v, int n, double thr) {
   }
 }
 
-// integrality packed into bit 31 of the column index: no per-entry byte gather
-__global__ void k_pack_cols(int32_t* __restrict__ colx, const uint8_t* __restrict__ integral,
-                            long long nnz) {
-  for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < nnz;
-       k += (long long)gridDim.x * blockDim.x) {
-    const int32_t c = colx[k];
-    colx[k] = integral[c] ? (int32_t)(c | 0x80000000u) : c;
+// Session init: rows into length-sorted order (perm[new] = old), lhs/rhs
+// normalised (model.hpp:147-151), integrality packed into bit 31 of the
+// column index (no per-entry byte gather).  One warp per row.
+__global__ void k_permute_rows(const int32_t* __restrict__ rp, const int32_t* __restrict__ cols,
+                               const double* __restrict__ vals, const double* __restrict__ lhs,
+                               const double* __restrict__ rhs, const int32_t* __restrict__ perm,
+                               const int32_t* __restrict__ new_rp,
+                               const uint8_t* __restrict__ integral, int32_t* __restrict__ colx,
+                               double* __restrict__ new_vals, double* __restrict__ new_lhs,
+                               double* __restrict__ new_rhs, int m, double thr) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    const int old = perm[i];
+    const int b = rp[old], len = rp[old + 1] - b, nb = new_rp[i];
+    for (int k = lane; k < len; k += 32) {
+      const int32_t c = cols[b + k];
+      colx[nb + k] = integral[c] ? (int32_t)(c | 0x80000000u) : c;
+      new_vals[nb + k] = vals[b + k];
+    }
+    if (lane == 0) {
+      const double l = lhs[old], h = rhs[old];
+      new_lhs[i] = l >= thr ? CUDART_INF : (l <= -thr ? -CUDART_INF : l);
+      new_rhs[i] = h >= thr ? CUDART_INF : (h <= -thr ? -CUDART_INF : h);
+    }
+  }
+}
+
+// ---- worklist index (session init) -----------------------------------------------
+// Work-item code of every sorted row: its warp tile, or -1 - segment-row slot.
+__global__ void k_row_codes(const TileDesc* __restrict__ tiles, int num_tiles, int first_seg_row,
+                            int m, int32_t* __restrict__ code) {
+  const int gstride = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
+  for (int t = gtid; t < num_tiles; t += gstride) {
+    const TileDesc d = tiles[t];
+    for (int r = 0; r < d.nr; ++r) code[d.r0 + r] = t;
+  }
+  for (int i = first_seg_row + gtid; i < m; i += gstride) code[i] = -1 - (i - first_seg_row);
+}
+
+// column counts (one warp per row)
+__global__ void k_csc_count(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ colx,
+                            int m, int32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m;
+       i += (gridDim.x * blockDim.x) >> 5)
+    for (int k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32)
+      atomicAdd(&cnt[colx[k] & 0x7fffffff], 1);
+}
+
+__global__ void k_csc_fill(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ colx,
+                           const int32_t* __restrict__ code, int m, int32_t* __restrict__ cursor,
+                           int32_t* __restrict__ col_item) {
+  const int lane = threadIdx.x & 31;
+  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m;
+       i += (gridDim.x * blockDim.x) >> 5) {
+    const int c = code[i];
+    for (int k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32)
+      col_item[atomicAdd(&cursor[colx[k] & 0x7fffffff], 1)] = c;
   }
 }
 

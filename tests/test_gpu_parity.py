@@ -276,3 +276,16 @@ def test_config2_full_size_bit_exact():
     inst = G.config_instance("c2")
     gpu = propagate_gpu(inst, PAR)
     assert_bit_exact(gpu, O.propagate_parallel(inst, PAR), "c2")
+
+
+@pytest.mark.parametrize("worklist", [False, True])
+@pytest.mark.parametrize("row_check", [False, True])
+def test_worklist_modes_identical(worklist, row_check):
+    """The device-side worklist is exact: same trajectory with it on and off."""
+    for seed in (3, 8, 13):
+        inst = G.gen_random(3000, 2500, seed, mean_row_nnz=9.0, integral_fraction=0.5)
+        cfg = EngineConfig(row_check=row_check, worklist=worklist)
+        assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg), inst.name)
+    inst = G.gen_powerlaw(20000, 20000, 77, cap=3000)
+    cfg = EngineConfig(row_check=row_check, worklist=worklist, nnz_budget=256)
+    assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg), inst.name)

@@ -1,0 +1,40 @@
+"""Profiling driver: one session of a config, a few isolated round-kernel
+launches (for ncu -k regex:k_tiles) and one full solve."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2009_07785_b200 import generators as G  # noqa: E402
+from paper_2009_07785_b200.engine import Session  # noqa: E402
+from paper_2009_07785_b200.model import EngineConfig, LoopMode  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c2")
+ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--solve", action="store_true")
+ap.add_argument("--host-loop", action="store_true")
+ap.add_argument("--debug-flags", type=int, default=0)
+a = ap.parse_args()
+inst = G.config_instance(a.config)
+cfg = EngineConfig(loop_mode=LoopMode.Host if a.host_loop else LoopMode.Graph)
+import ctypes as C  # noqa: E402
+from paper_2009_07785_b200 import abi  # noqa: E402
+if a.debug_flags:
+    lib = abi.load_library()
+    c = cfg.to_c()
+    c.flags |= a.debug_flags
+    p = inst.to_c()
+    h = C.c_void_p()
+    abi.check(lib.pg_session_create(C.byref(p), C.byref(c), C.byref(h)), "create")
+    ns, b = C.c_double(), C.c_double()
+    abi.check(lib.pg_session_time_round_kernel(h, a.reps, C.byref(ns), C.byref(b)), "time")
+    print(f"k_round {ns.value/1e3:.1f} us (debug flags {a.debug_flags:#x})")
+    sys.exit(0)
+with Session(inst, cfg) as s:
+    print(s.info())
+    ns, b = s.time_round_kernel(a.reps)
+    print(f"k_tiles {ns/1e3:.1f} us  {b/ns:.1f} GB/s")
+    if a.solve:
+        r = s.run()
+        print(r.status, r.rounds_executed, r.elapsed_ns / 1e6, "ms")
