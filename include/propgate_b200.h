@@ -90,7 +90,7 @@ typedef struct pg_config {
   int32_t scalar_mode;       /* PG_WIDE64 */
   int32_t device;            /* CUDA device ordinal, default 0 */
   int32_t loop_mode;         /* PG_LOOP_GRAPH */
-  uint32_t flags;            /* PG_FLAG_ROWCHECK | PG_FLAG_WORKLIST by default */
+  uint32_t flags;            /* PG_FLAG_ROWCHECK by default */
 } pg_config;
 
 /* propgate::PropagationResult (model.hpp:119-127).  `lower`/`upper` are

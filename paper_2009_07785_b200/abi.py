@@ -100,7 +100,7 @@ def default_config() -> PgConfig:
     c.scalar_mode = PG_WIDE64
     c.device = 0
     c.loop_mode = PG_LOOP_GRAPH
-    c.flags = PG_FLAG_ROWCHECK | PG_FLAG_WORKLIST
+    c.flags = PG_FLAG_ROWCHECK
     return c
 
 

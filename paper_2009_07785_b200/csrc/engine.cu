@@ -133,7 +133,8 @@ struct pg_session {
   // worklist index and dirty sets
   int32_t* d_col_ptr = nullptr;
   int32_t* d_col_item = nullptr;
-  uint8_t* d_flags = nullptr;  // tile | segment-row marks, two buffers each
+  uint8_t* d_flags = nullptr;  // row marks, two buffers
+  int32_t* d_chg = nullptr;    // changed-column lists, two buffers
   Dirty dirty{};
 
   // host mirrors
@@ -161,7 +162,7 @@ struct pg_session {
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
                     d_lo_res, d_up_res, d_tiles, d_groups, d_segs, d_srow, d_sfirst, d_chunk_seg, d_partial,
                     d_row_act, d_worklist, d_st, d_per_round, d_col_ptr, d_col_item,
-                    d_flags};
+                    d_flags, d_chg};
     for (void* p : ptrs)
       if (p) cudaFree(p);
     if (h_st) cudaFreeHost(h_st);
@@ -236,6 +237,7 @@ struct pg_session {
       k_seg_cand<<<std::min(nseg, num_sms * 8), 256, 0, stream>>>(A, dcfg);
     k_commit<<<grid_for(n, kCommitThreads), kCommitThreads, 0, stream>>>(
         d_snap, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0);
+    if (dirty.enabled) k_mark<<<num_sms * 8, 256, 0, stream>>>(dirty, d_st);
     PG_CUDA(cudaGetLastError());
   }
 
@@ -360,18 +362,15 @@ void build_tables(pg_session* s, const int32_t* rp, Tables& T) {
   const int64_t short_max = std::min<int64_t>(chunk, kShortMax);
   const int32_t m = s->m;
   int32_t i = 0;
+  // warp tiles: consecutive rows of one length L (rows are length-sorted)
   while (i < m && (int64_t)rp[i + 1] - rp[i] <= short_max) {
     const int32_t start = i;
-    int64_t acc = 0;
-    while (i < m && i - start < 32) {
-      const int64_t l = (int64_t)rp[i + 1] - rp[i];
-      if (l > short_max || acc + l > kWNnz) break;
-      acc += l;
-      ++i;
-    }
-    T.tiles.push_back({start, i - start, rp[start], (int32_t)acc});
+    const int64_t L = (int64_t)rp[i + 1] - rp[i];
+    const int32_t cap = L ? (int32_t)std::min<int64_t>(32, kWNnz / L) : 32;
+    while (i < m && i - start < cap && (int64_t)rp[i + 1] - rp[i] == L) ++i;
+    T.tiles.push_back({start, i - start, rp[start], (int32_t)(L * (i - start))});
     s->tile_rows += i - start;
-    s->tile_nnz += acc;
+    s->tile_nnz += L * (i - start);
   }
   for (; i < m; ++i) {
     const int32_t slot = (int32_t)T.srow.size();
@@ -547,21 +546,20 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     // worklist index: column -> work items (device counting sort by column)
     {
       Dirty& D = s->dirty;
-      D.num_tiles = s->num_tiles;
-      D.nsrow = s->nsrow;
+      D.m = m;
+      D.ms = (m + 15) & ~15;
+      D.n = n;
+      D.first_seg_row = (int32_t)s->tile_rows;
       D.enabled = (cfg->flags & PG_FLAG_WORKLIST) != 0;
-      const size_t nflags = 2 * ((size_t)s->num_tiles + s->nsrow);
-      s->d_flags = dalloc<uint8_t>(nflags);
-      D.tile_flag = s->d_flags;
-      D.srow_flag = D.tile_flag + 2 * (size_t)s->num_tiles;
+      s->d_flags = dalloc<uint8_t>(2 * (size_t)D.ms + 16);
+      D.row_flag = s->d_flags;
       if (D.enabled) {
+        s->d_chg = dalloc<int32_t>(2 * (size_t)n);
+        D.chg_list = s->d_chg;
         s->d_col_ptr = dalloc<int32_t>((size_t)n + 1);
         s->d_col_item = dalloc<int32_t>(nnz);
-        int32_t* code = dalloc<int32_t>(m);
         int32_t* cnt = dalloc<int32_t>((size_t)n + 1);
         PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)n + 1), st));
-        k_row_codes<<<s->grid_for(std::max<int64_t>(s->num_tiles, m), 256), 256, 0, st>>>(
-            s->d_tiles, s->num_tiles, (int)s->tile_rows, m, code);
         if (m) k_csc_count<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
             s->d_row_ptr, s->d_colx, m, cnt);
         size_t tmp_bytes = 0;
@@ -571,14 +569,13 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         PG_CUDA(cudaMemcpyAsync(cnt, s->d_col_ptr, sizeof(int32_t) * ((size_t)n + 1),
                                 cudaMemcpyDeviceToDevice, st));
         if (m) k_csc_fill<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
-            s->d_row_ptr, s->d_colx, code, m, cnt, s->d_col_item);
+            s->d_row_ptr, s->d_colx, m, cnt, s->d_col_item);
         PG_CUDA(cudaGetLastError());
         PG_CUDA(cudaStreamSynchronize(st));
         cudaFree(tmp);
-        cudaFree(code);
         cudaFree(cnt);
         D.col_ptr = s->d_col_ptr;
-        D.col_item = s->d_col_item;
+        D.col_row = s->d_col_item;
       }
     }
     s->upload_bounds(p->lower, p->upper);
@@ -627,7 +624,7 @@ void pg_config_default(pg_config* c) {
   c->scalar_mode = PG_WIDE64;
   c->device = 0;
   c->loop_mode = PG_LOOP_GRAPH;
-  c->flags = PG_FLAG_ROWCHECK | PG_FLAG_WORKLIST;
+  c->flags = PG_FLAG_ROWCHECK;
 }
 
 int pg_config_validate(const pg_config* cfg) {

@@ -52,6 +52,7 @@ struct DevState {
   int32_t full;                      // 1: every work item is dirty (first round)
   int32_t frac_any;                  // an integral column has a fractional start bound
   int32_t frac_tmp;                  // k_reset's accumulator of frac_any
+  int32_t nchg[2];                   // changed-column list lengths, by round parity
 };
 
 // Device-side worklist (PG_FLAG_WORKLIST): a round only
@@ -59,15 +60,17 @@ struct DevState {
 // round.  Exact under snapshot semantics: a row none of whose bounds changed
 // yields the same candidates, already accepted or rejected against the same
 // bounds (the reference's marking, seq_engine.cpp:29,37-38,77, by analogy).
-// The commit marks, with plain idempotent stores, the warp tile or the
-// segment row of every row containing a changed column; k_round skips
-// clean tiles and segment groups none of whose rows is marked.
+// Rows are marked: k_commit lists the changed columns (warp-aggregated
+// appends), k_mark walks each changed column's rows (column index built at
+// session init) and sets the row's flag for the next round.  k_tiles
+// compacts the marked rows of each warp tile; a segment group is processed
+// when a row of one of its segments is marked.
 struct Dirty {
-  const int32_t* col_ptr;   // [n+1] column -> its work-item codes
-  const int32_t* col_item;  // code >= 0: warp tile; code < 0: segment row -1-code
-  uint8_t* tile_flag;       // [2][num_tiles], by round parity
-  uint8_t* srow_flag;       // [2][nsrow]
-  int32_t num_tiles, nsrow;
+  const int32_t* col_ptr;   // [n+1] column -> rows (sorted row space) containing it
+  const int32_t* col_row;
+  uint8_t* row_flag;        // [2][ms], by round parity (ms = m rounded up to 16)
+  int32_t* chg_list;        // [2][n] changed columns of a round
+  int32_t m, ms, n, first_seg_row;
   int32_t enabled;
 };
 
@@ -448,7 +451,8 @@ __device__ __forceinline__ int popc_range(const unsigned (&m)[kWItems], int b, i
 
 // ---- short rows: warp tiles with per-warp asynchronous staging -------------------
 // Each warp owns a contiguous run of warp tiles (<= 32 consecutive rows of
-// <= kShortMax entries, <= 128 entries) and pipelines them three deep:
+// the SAME length L <= kShortMax, <= 128 entries) and pipelines them three
+// deep:
 //   tile i+2: TMA bulk copies of its vals/col streams -> shared memory
 //   tile i+1: cp.async gathers of the 16 B {lb, ub} snapshot of every entry
 //   tile i:   compute (one lane per row, sums in entry order)
@@ -461,7 +465,6 @@ struct __align__(16) TileStage {
   double vals[kWNnz + 2];   // +2 / +4: the bulk copies start 16 B aligned
   int32_t cols[kWNnz + 4];
   double2 rec[kWNnz];       // {lb, ub} of every entry's column
-  int32_t rp[36];           // row_ptr slice of the tile's rows
   double lhs[34];
   double rhs[34];
   TileDesc d;
@@ -470,13 +473,12 @@ struct __align__(16) TileStage {
 struct TileWarpSmem {
   TileStage stage[kTStages];
   uint64_t bar[kTStages];
-  double pmin[kWNnz];       // finite min contributions (0 for infinite ones)
+  double pmin[kWNnz];       // finite min contributions, [position][row]
   double pmax[kWNnz];
   double x[kWNnz];          // filter terms
   double minf[32], maxf[32], lhs[32], rhs[32], tr[32], tl[32];
   int32_t mini[32], maxi[32];
-  int32_t rp[33];
-  uint8_t row[kWNnz];
+  uint32_t cmin[32], cmax[32];  // per row: positions with an infinite contribution
   uint8_t qe[kWNnz];        // queue: entry index
   uint8_t mode[32];
 };
@@ -524,14 +526,12 @@ __device__ __forceinline__ void tile_issue_tma(const RoundArgs& A, TileStage& S,
   const int kv = d.k0 & ~1, kc = d.k0 & ~3, k1 = d.k0 + d.nz;
   const uint32_t bv = (uint32_t)(((k1 - kv) * 8 + 15) & ~15);
   const uint32_t bc = (uint32_t)(((k1 - kc) * 4 + 15) & ~15);
-  const int rr = d.r0 & ~3, rd = d.r0 & ~1;
-  const uint32_t br = (uint32_t)(((d.r0 + d.nr + 1 - rr) * 4 + 15) & ~15);
+  const int rd = d.r0 & ~1;
   const uint32_t bs = (uint32_t)(((d.r0 + d.nr - rd) * 8 + 15) & ~15);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  mbar_expect_tx(bar, bv + bc + br + 2 * bs);
+  mbar_expect_tx(bar, bc + bv + 2 * bs);
   bulk_g2s(S.vals, A.vals + kv, bv, bar);
   bulk_g2s(S.cols, A.colx + kc, bc, bar);
-  bulk_g2s(S.rp, A.row_ptr + rr, br, bar);
   bulk_g2s(S.lhs, A.lhs + rd, bs, bar);
   bulk_g2s(S.rhs, A.rhs + rd, bs, bar);
 }
@@ -563,45 +563,54 @@ __device__ void tile_compute(const RoundArgs& A, TileWarpSmem& W, const TileStag
   const int lane = threadIdx.x & 31;
   const TileDesc d = S.d;
   const int nr = d.nr, nz = d.nz;
-  const int ov = d.k0 & 1, oc = d.k0 & 3, orp = d.r0 & 3, ors = d.r0 & 1;
-  W.rp[lane] = S.rp[orp + min(lane, nr)] - d.k0;
-  if (lane == 0) W.rp[nr] = nz;
+  const int L = nr ? nz / nr : 0;  // every row of a warp tile has L entries
+  const float invL = L ? 1.0f / (float)L : 0.0f;
+  const int ov = d.k0 & 1, oc = d.k0 & 3, ors = d.r0 & 1;
+  W.cmin[lane] = 0u;
+  W.cmax[lane] = 0u;
+  __syncwarp();
 
-  // phase 1: contributions and filter terms from the staged entries
-  unsigned mmin[kWItems], mmax[kWItems];
+  // phase 1: contributions and filter terms of the staged entries, written
+  // transposed ([position][row]) so that phase 2 reads are conflict-free
+  double xq[kWItems];
+  int rq[kWItems];
+  unsigned infq = 0;  // bit 2q: min contribution infinite, bit 2q+1: max
 #pragma unroll
   for (int q = 0; q < kWItems; ++q) {
     const int e = lane + 32 * q;
-    bool imin = false, imax = false;
+    rq[q] = 0;
+    xq[q] = 0.0;
     if (e < nz) {
+      const int r = __float2int_rz(((float)e + 0.5f) * invL);
+      const int i = e - r * L;
+      rq[q] = r;
       const double a = S.vals[ov + e];
-      const int32_t cx = S.cols[oc + e];
-      const double2 r = S.rec[e];
-      const double bmin = a > 0 ? r.x : r.y;
-      const double bmax = a > 0 ? r.y : r.x;
-      imin = isinf(bmin);
-      imax = isinf(bmax);
-      W.pmin[e] = imin ? 0.0 : __dmul_rn(a, bmin);
-      W.pmax[e] = imax ? 0.0 : __dmul_rn(a, bmax);
-      W.x[e] = fabs(a) * column_q_fast(r.x, r.y, cx < 0, frac_any, cfg);
+      const double2 b = S.rec[e];
+      const double bmin = a > 0 ? b.x : b.y;
+      const double bmax = a > 0 ? b.y : b.x;
+      const bool imin = isinf(bmin), imax = isinf(bmax);
+      W.pmin[i * nr + r] = imin ? 0.0 : __dmul_rn(a, bmin);
+      W.pmax[i * nr + r] = imax ? 0.0 : __dmul_rn(a, bmax);
+      const double x = fabs(a) * column_q_fast(b.x, b.y, S.cols[oc + e] < 0, frac_any, cfg);
+      W.x[i * nr + r] = x;
+      xq[q] = x;
+      if (imin) atomicOr(&W.cmin[r], 1u << i);
+      if (imax) atomicOr(&W.cmax[r], 1u << i);
+      infq |= (imin ? 1u : 0u) << (2 * q) | (imax ? 2u : 0u) << (2 * q);
     }
-    mmin[q] = __ballot_sync(0xffffffffu, imin);
-    mmax[q] = __ballot_sync(0xffffffffu, imax);
   }
   __syncwarp();
 
-  // phase 2: one lane per row, sums in entry order (propcore.hpp:50-63)
+  // phase 2: one lane per row, L sums in entry order (propcore.hpp:50-63)
   bool may = false;
   if (lane < nr) {
-    const int b = W.rp[lane], e = W.rp[lane + 1];
     double smin = 0.0, smax = 0.0, xmax = -CUDART_INF;
-    for (int k = b; k < e; ++k) {
-      smin = __dadd_rn(smin, W.pmin[k]);
-      smax = __dadd_rn(smax, W.pmax[k]);
-      xmax = fmax(xmax, W.x[k]);
-      W.row[k] = (uint8_t)lane;
+    for (int i = 0; i < L; ++i) {
+      smin = __dadd_rn(smin, W.pmin[i * nr + lane]);
+      smax = __dadd_rn(smax, W.pmax[i * nr + lane]);
+      xmax = fmax(xmax, W.x[i * nr + lane]);
     }
-    const Act act = {smin, smax, popc_range(mmin, b, e), popc_range(mmax, b, e)};
+    const Act act = {smin, smax, __popc(W.cmin[lane]), __popc(W.cmax[lane])};
     const double l = S.lhs[ors + lane], h = S.rhs[ors + lane];
     if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
     const RowFilter f = row_filter(act, l, h);
@@ -626,12 +635,10 @@ __device__ void tile_compute(const RoundArgs& A, TileWarpSmem& W, const TileStag
   for (int q = 0; q < kWItems; ++q) {
     const int e = lane + 32 * q;
     bool pass = false;
-    if (e < nz) {
-      const int r = W.row[e];
-      if ((may_rows >> r) & 1u) {
-        const RowFilter f = {W.tr[r], W.tl[r], W.mode[r]};
-        pass = entry_may(f, W.x[e], (mmin[q] >> lane) & 1u, (mmax[q] >> lane) & 1u);
-      }
+    if (e < nz && ((may_rows >> rq[q]) & 1u)) {
+      const int r = rq[q];
+      const RowFilter f = {W.tr[r], W.tl[r], W.mode[r]};
+      pass = entry_may(f, xq[q], (infq >> (2 * q)) & 1u, (infq >> (2 * q + 1)) & 1u);
     }
     const unsigned m = __ballot_sync(0xffffffffu, pass);
     if (pass) W.qe[qn + __popc(m & ((1u << lane) - 1u))] = (uint8_t)e;
@@ -640,10 +647,10 @@ __device__ void tile_compute(const RoundArgs& A, TileWarpSmem& W, const TileStag
   __syncwarp();
   for (int i = lane; i < qn; i += 32) {
     const int e = W.qe[i];
-    const int r = W.row[e];
-    const double2 rc = S.rec[e];
+    const int r = __float2int_rz(((float)e + 0.5f) * invL);
+    const double2 b = S.rec[e];
     const Act act = {W.minf[r], W.maxf[r], W.mini[r], W.maxi[r]};
-    if (entry_pipeline(act, S.vals[ov + e], rc.x, rc.y, W.lhs[r], W.rhs[r], S.cols[oc + e],
+    if (entry_pipeline(act, S.vals[ov + e], b.x, b.y, W.lhs[r], W.rhs[r], S.cols[oc + e],
                        A.key_out, cfg))
       inf_flag = true;
   }
@@ -663,18 +670,51 @@ __global__ void __launch_bounds__(kTWarps * 32) k_tiles(const RoundArgs A, const
   if (tb >= te) return;
   const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
   const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
-  const uint8_t* tflag = A.dirty.tile_flag + (size_t)par * A.dirty.num_tiles;
+  const uint8_t* rflag = A.dirty.row_flag + (size_t)par * A.dirty.ms;
   const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
-  // next tile at or after t that must be processed (-1 = none)
-  auto next_tile = [&](int t) -> int {
-    if (full) return t < te ? t : -1;
-    for (; t < te; t += 32) {
-      const bool d = t + lane < te && tflag[t + lane];
-      const unsigned m = __ballot_sync(0xffffffffu, d);
-      if (m) return t + __ffs(m) - 1;
+  auto next_tile = [&](int t) -> int { return t < te ? t : -1; };
+  if (!full) {
+    // sparse round: per tile, the marked rows only, as a compacted virtual
+    // tile staged with plain loads (uniform row length keeps the layout)
+    bool inf_sparse = false;
+    for (int t0 = tb; t0 < te; t0 += 32) {
+      TileDesc wd = {0, 0, 0, 0};
+      if (t0 + lane < te) wd = A.tiles[t0 + lane];
+      for (int u = 0; u < 32 && t0 + u < te; ++u) {
+        TileDesc d;
+        d.r0 = __shfl_sync(0xffffffffu, wd.r0, u);
+        d.nr = __shfl_sync(0xffffffffu, wd.nr, u);
+        d.k0 = __shfl_sync(0xffffffffu, wd.k0, u);
+        d.nz = __shfl_sync(0xffffffffu, wd.nz, u);
+        const unsigned m = __ballot_sync(0xffffffffu, lane < d.nr && rflag[d.r0 + lane]);
+        if (!m) continue;
+        const int L = d.nz / d.nr, nv = __popc(m);
+        TileStage& S = W.stage[0];
+        // lane p of a marked row takes slot rank(p) of the virtual tile
+        if ((m >> lane) & 1u) {
+          const int rank = __popc(m & ((1u << lane) - 1u));
+          W.qe[rank] = (uint8_t)lane;
+          S.lhs[rank] = A.lhs[d.r0 + lane];
+          S.rhs[rank] = A.rhs[d.r0 + lane];
+        }
+        __syncwarp();
+        const float invL = 1.0f / (float)L;
+        for (int e = lane; e < nv * L; e += 32) {
+          const int r = __float2int_rz(((float)e + 0.5f) * invL);
+          const int k = d.k0 + W.qe[r] * L + (e - r * L);
+          const int32_t c = __ldg(A.colx + k);
+          S.vals[e] = __ldg(A.vals + k);
+          S.cols[e] = c;
+          S.rec[e] = __ldg(reinterpret_cast<const double2*>(&A.snap[c & 0x7fffffff].lo));
+        }
+        if (lane == 0) S.d = TileDesc{0, nv, 0, nv * L};
+        __syncwarp();
+        tile_compute<kRowCheck>(A, W, S, frac_any, inf_sparse, cfg);
+      }
     }
-    return -1;
-  };
+    if (__any_sync(0xffffffffu, inf_sparse) && lane == 0) A.st->infeasible = 1;
+    return;
+  }
   if (lane == 0)
     for (int i = 0; i < kTStages; ++i) mbar_init(&W.bar[i], 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -743,7 +783,7 @@ __global__ void __launch_bounds__(kRoundThreads, PG_ROUND_MINB) k_round(const Ro
   // full sweep (first round, or no worklist), else skip clean work items
   const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
   const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
-  const uint8_t* sflag = A.dirty.srow_flag + (size_t)par * A.dirty.nsrow;
+  const uint8_t* sflag = A.dirty.row_flag + (size_t)par * A.dirty.ms + A.dirty.first_seg_row;
   const int total = A.ngroups;
   bool inf_flag = false;
   for (;;) {
@@ -768,30 +808,55 @@ __global__ void __launch_bounds__(kRoundThreads, PG_ROUND_MINB) k_round(const Ro
 
 // Pass 2 over the worklist: one warp per segment, coalesced re-read (mostly
 // L2 hits), entry filter, exact pipeline, atomic commit.
+// Pass 2 over the worklist: the segments of rows that may tighten.  Each
+// warp takes one segment (a short segment is one or two coalesced steps; a
+// long one is split over the CTA's warps in 32-entry strides).
+__device__ __forceinline__ bool seg_cand_entries(const RoundArgs& A, const SegDesc& d,
+                                                 const Act& act, const RowFilter& f, double l,
+                                                 double h, int first, int stride,
+                                                 const DevCfg& cfg) {
+  bool inf_flag = false;
+  for (int i = first; i < d.len; i += stride) {
+    const int k = d.k0 + i;
+    const int32_t c = __ldg(A.colx + k);
+    const double a = __ldg(A.vals + k);
+    double lo, up, q;
+    ld_snap(A.snap + (c & 0x7fffffff), lo, up, q);
+    double pmin, pmax;
+    contrib(a, lo, up, pmin, pmax);
+    if (entry_may(f, fabs(a) * q, isnan(pmin), isnan(pmax)) &&
+        entry_pipeline(act, a, lo, up, l, h, c, A.key_out, cfg))
+      inf_flag = true;
+  }
+  return inf_flag;
+}
+
 __global__ void __launch_bounds__(256)
     k_seg_cand(const RoundArgs A, const DevCfg cfg) {
   const int nwl = *((volatile int32_t*)&A.st->wl_count);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   bool inf_flag = false;
+  // long segments: one CTA each (worklist order is arbitrary, test per entry)
   for (int w = blockIdx.x; w < nwl; w += gridDim.x) {
     const SegDesc d = A.segs[A.worklist[w]];
+    if (d.len <= kLongSeg) continue;
     const Act act = A.row_act[d.rslot];
     const int row = A.srow[d.rslot];
     const double l = A.lhs[row], h = A.rhs[row];
-    const RowFilter f = row_filter(act, l, h);
-    for (int i = threadIdx.x; i < d.len; i += blockDim.x) {
-      const int k = d.k0 + i;
-      const int32_t c = __ldg(A.colx + k);
-      const double a = __ldg(A.vals + k);
-      double lo, up, q;
-      ld_snap(A.snap + (c & 0x7fffffff), lo, up, q);
-      double pmin, pmax;
-      contrib(a, lo, up, pmin, pmax);
-      if (entry_may(f, fabs(a) * q, isnan(pmin), isnan(pmax)) &&
-          entry_pipeline(act, a, lo, up, l, h, c, A.key_out, cfg))
-        inf_flag = true;
-    }
+    inf_flag |= seg_cand_entries(A, d, act, row_filter(act, l, h), l, h, threadIdx.x,
+                                 blockDim.x, cfg);
   }
-  if (__any_sync(0xffffffffu, inf_flag) && (threadIdx.x & 31) == 0) A.st->infeasible = 1;
+  // short segments: one warp each
+  for (int w = blockIdx.x * (blockDim.x >> 5) + warp; w < nwl;
+       w += gridDim.x * (blockDim.x >> 5)) {
+    const SegDesc d = A.segs[A.worklist[w]];
+    if (d.len > kLongSeg) continue;
+    const Act act = A.row_act[d.rslot];
+    const int row = A.srow[d.rslot];
+    const double l = A.lhs[row], h = A.rhs[row];
+    inf_flag |= seg_cand_entries(A, d, act, row_filter(act, l, h), l, h, lane, 32, cfg);
+  }
+  if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
 }
 
 // ---- commit + round decision ------------------------------------------------------
@@ -847,23 +912,25 @@ __global__ void __launch_bounds__(kCommitThreads)
       const bool integral = snap[j].flags & 1;
       Snap s = {lo, up, column_q(lo, up, integral, cfg), snap[j].flags};
       snap[j] = s;
-      if (D.enabled) {
-        // mark the work item of every row containing column j for the next round
-        for (int e = D.col_ptr[j]; e < D.col_ptr[j + 1]; ++e) {
-          const int code = D.col_item[e];
-          if (code >= 0)
-            D.tile_flag[(size_t)nb * D.num_tiles + code] = 1;
-          else
-            D.srow_flag[(size_t)nb * D.nsrow + (-1 - code)] = 1;
-        }
+    }
+    if (D.enabled) {
+      // changed columns of this round -> list (one atomic per warp)
+      const unsigned act = __activemask();
+      const unsigned chm = __ballot_sync(act, c != 0);
+      if (chm) {
+        const int leader = __ffs(act) - 1;
+        int base = 0;
+        if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&st->nchg[cb], __popc(chm));
+        base = __shfl_sync(act, base, leader);
+        if (c) D.chg_list[(size_t)cb * D.n + base + __popc(chm & ((1u << (threadIdx.x & 31)) - 1u))] = j;
       }
     }
     if (lo > __dadd_rn(up, cfg.imp_abs)) inf = 1;
   }
   if (D.enabled) {
-    // the consumed buffer is the round-after-next's mark set
-    for (int i = gtid; i < D.num_tiles; i += gstride) D.tile_flag[(size_t)cb * D.num_tiles + i] = 0;
-    for (int i = gtid; i < D.nsrow; i += gstride) D.srow_flag[(size_t)cb * D.nsrow + i] = 0;
+    // the consumed marks become the round-after-next's mark set
+    uint32_t* f = reinterpret_cast<uint32_t*>(D.row_flag + (size_t)cb * D.ms);
+    for (int i = gtid; i < D.ms / 4; i += gstride) f[i] = 0u;
   }
   changes = block_sum<kCommitThreads>(changes, inf);
   if (threadIdx.x == 0) {
@@ -892,6 +959,7 @@ __global__ void __launch_bounds__(kCommitThreads)
       st->wl_count = 0;
       st->work = 0;
       st->full = 0;
+      st->nchg[nb] = 0;  // the list k_mark consumed after the previous commit
       __threadfence();
       if (use_graph) cudaGraphSetConditional(cond, status >= 0 ? 0u : 1u);
     }
@@ -908,8 +976,8 @@ __global__ void __launch_bounds__(kCommitThreads)
   int crossed = 0, frac = 0;
   {
     const int gstride = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
-    for (int i = gtid; i < 2 * D.num_tiles; i += gstride) D.tile_flag[i] = 0;
-    for (int i = gtid; i < 2 * D.nsrow; i += gstride) D.srow_flag[i] = 0;
+    uint32_t* f = reinterpret_cast<uint32_t*>(D.row_flag);
+    for (int i = gtid; i < D.ms / 2; i += gstride) f[i] = 0u;
   }
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const double l = lo0[j], u = up0[j];
@@ -940,6 +1008,7 @@ __global__ void __launch_bounds__(kCommitThreads)
       st->wl_count = 0;
       st->work = 0;
       st->full = 1;
+      st->nchg[0] = st->nchg[1] = 0;
       st->frac_any = atomicAdd(&st->frac_tmp, 0);
       st->frac_tmp = 0;
       st->ticket_reset = 0;
@@ -995,17 +1064,26 @@ __global__ void k_permute_rows(const int32_t* __restrict__ rp, const int32_t* __
   }
 }
 
-// ---- worklist index (session init) -----------------------------------------------
-// Work-item code of every sorted row: its warp tile, or -1 - segment-row slot.
-__global__ void k_row_codes(const TileDesc* __restrict__ tiles, int num_tiles, int first_seg_row,
-                            int m, int32_t* __restrict__ code) {
-  const int gstride = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  for (int t = gtid; t < num_tiles; t += gstride) {
-    const TileDesc d = tiles[t];
-    for (int r = 0; r < d.nr; ++r) code[d.r0 + r] = t;
+// After the commit of round r: mark, for round r + 1, every row containing a
+// column changed in round r (one warp per changed column).
+__global__ void __launch_bounds__(256) k_mark(const Dirty D, DevState* __restrict__ st) {
+  const int r = *((volatile int32_t*)&st->round);
+  if (!D.enabled || *((volatile int32_t*)&st->done)) return;
+  const int cb = r & 1, nb = (r + 1) & 1;
+  const int nchg = *((volatile int32_t*)&st->nchg[cb]);
+  uint8_t* flag = D.row_flag + (size_t)nb * D.ms;
+  const int lane = threadIdx.x & 31;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchg;
+       w += (gridDim.x * blockDim.x) >> 5) {
+    const int j = D.chg_list[(size_t)cb * D.n + w];
+    for (int e = D.col_ptr[j] + lane; e < D.col_ptr[j + 1]; e += 32) {
+      const int row = D.col_row[e];
+      if (!flag[row]) flag[row] = 1;  // read first: most rows are marked repeatedly
+    }
   }
-  for (int i = first_seg_row + gtid; i < m; i += gstride) code[i] = -1 - (i - first_seg_row);
 }
+
+// ---- worklist index (session init) -----------------------------------------------
 
 // column counts (one warp per row)
 __global__ void k_csc_count(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ colx,
@@ -1018,15 +1096,12 @@ __global__ void k_csc_count(const int32_t* __restrict__ row_ptr, const int32_t* 
 }
 
 __global__ void k_csc_fill(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ colx,
-                           const int32_t* __restrict__ code, int m, int32_t* __restrict__ cursor,
-                           int32_t* __restrict__ col_item) {
+                           int m, int32_t* __restrict__ cursor, int32_t* __restrict__ col_row) {
   const int lane = threadIdx.x & 31;
   for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m;
-       i += (gridDim.x * blockDim.x) >> 5) {
-    const int c = code[i];
+       i += (gridDim.x * blockDim.x) >> 5)
     for (int k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32)
-      col_item[atomicAdd(&cursor[colx[k] & 0x7fffffff], 1)] = c;
-  }
+      col_row[atomicAdd(&cursor[colx[k] & 0x7fffffff], 1)] = i;
 }
 
 }  // namespace pgb

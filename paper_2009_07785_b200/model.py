@@ -153,7 +153,7 @@ class EngineConfig:
     device: int = 0
     loop_mode: LoopMode = LoopMode.Graph
     row_check: bool = True
-    worklist: bool = True
+    worklist: bool = False
 
     def to_c(self) -> abi.PgConfig:
         c = abi.PgConfig()

@@ -57,15 +57,16 @@ __global__ void k(const double* __restrict__ vals, const int* __restrict__ cols,
   if (acc == 12345.678) out[0] = acc;
 }
 
-template <int MODE>
-float run(const double* v, const int* c, const Rec* r, long long nnz, double* out, int grid) {
+template <int MODE, int ITEMS = 8>
+float run(const double* v, const int* c, const Rec* r, long long nnz, double* out, int grid,
+          int threads = 256) {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  for (int i = 0; i < 3; ++i) k<MODE, 8><<<grid, 256>>>(v, c, r, nnz, out);
+  for (int i = 0; i < 3; ++i) k<MODE, ITEMS><<<grid, threads>>>(v, c, r, nnz, out);
   cudaEventRecord(a);
   const int reps = 10;
-  for (int i = 0; i < reps; ++i) k<MODE, 8><<<grid, 256>>>(v, c, r, nnz, out);
+  for (int i = 0; i < reps; ++i) k<MODE, ITEMS><<<grid, threads>>>(v, c, r, nnz, out);
   cudaEventRecord(b);
   cudaEventSynchronize(b);
   float ms;
@@ -104,6 +105,17 @@ int main(int argc, char** argv) {
     const float t3 = run<3>(v, c, r, nnz, out, grid);
     printf("grid %d: stream %.1f us (%.0f GB/s) | +16B gather %.1f us | +32B gather %.1f us | +8B gather %.1f us\n",
            grid, t0 * 1e3, 12.0 * nnz / (t0 * 1e-3) / 1e9, t1 * 1e3, t2 * 1e3, t3 * 1e3);
+  }
+  // memory-level-parallelism sweep for the 16 B gather: warps/SM x items
+  printf("MLP sweep (16 B gather, 12M entries): warps/SM items -> us, in-flight/SM\n");
+  for (int wps : {4, 8, 12, 16, 24, 32}) {
+    const int grid = sms * wps / 4;  // 128-thread CTAs
+    const float t1 = run<1, 1>(v, c, r, nnz, out, grid, 128);
+    const float t2 = run<1, 2>(v, c, r, nnz, out, grid, 128);
+    const float t4 = run<1, 4>(v, c, r, nnz, out, grid, 128);
+    const float t8 = run<1, 8>(v, c, r, nnz, out, grid, 128);
+    printf("  %2d warps/SM: items1 %.1f | items2 %.1f | items4 %.1f | items8 %.1f us\n", wps,
+           t1 * 1e3, t2 * 1e3, t4 * 1e3, t8 * 1e3);
   }
   return 0;
 }
