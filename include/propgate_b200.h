@@ -176,6 +176,17 @@ int pg_session_propagate_batch(pg_session* s, int32_t K, const double* lower,
 int pg_session_time_round_kernel(pg_session* s, int32_t reps, double* mean_ns,
                                  double* bytes);
 
+/* ---- row-sharded multi-GPU (config 5): one process per GPU --------------
+ * New capability (the reference is single-process).  Each rank creates a
+ * session over its contiguous row shard (all columns), rank 0 draws an NCCL
+ * unique id, every rank attaches with it; each round then merges the shards'
+ * bound keys and infeasibility with one NCCL max all-reduce over NVLink,
+ * captured inside the device-resident loop.  Results are bit-identical to a
+ * single GPU (exact max/min merges, rows never split). */
+int pg_nccl_unique_id(uint8_t* out128);
+int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank,
+                           int32_t world);
+
 /* Session statistics: number of row tiles, long rows, chunks. */
 int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info);
 

@@ -77,6 +77,9 @@ def oracle_lib():
         lib.orc_classify.restype = C.c_int32
         lib.orc_tighten.argtypes = [C.c_double] * 4 + [_G, _dp]
         lib.orc_tighten.restype = C.c_int32
+        lib.orc_propcore_rows.argtypes = [C.c_int32, _ip, _dp, _dp, _dp, _dp, _G, _dp, _ip, _dp, _dp,
+                                          _dp, _ip]
+        lib.orc_propcore_rows.restype = None
         _orc = lib
     return _orc
 

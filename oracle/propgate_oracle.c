@@ -196,3 +196,41 @@ int32_t orc_tighten(double old_lo, double old_up, double cand_lo, double cand_up
   if (kind == 4 || !(kind & 2)) out2[1] = 0;
   return kind;
 }
+
+/* Batch form of the propcore entry points over many independent rows (row t
+ * uses columns 0..len-1 of its own slice), for the golden-vector tests:
+ * act[4t..], klass[t]; per entry k: res[2k..], cand[4k..] (integral 0 then
+ * 1, {lo, up}), tight[2k..] and tkind[k] of tighten(lo, up, cand(integral 0)). */
+void orc_propcore_rows(int32_t nrows, const int32_t* row_len, const double* coefs,
+                       const double* lower, const double* upper, const double* sides,
+                       const pg_config* cfg, double* act, int32_t* klass, double* res,
+                       double* cand, double* tight, int32_t* tkind) {
+  int64_t off = 0;
+  int32_t cols[64];
+  for (int i = 0; i < 64; ++i) cols[i] = i;
+  for (int32_t t = 0; t < nrows; ++t) {
+    const int32_t L = row_len[t];
+    const act_f64 a = row_act_f64(cols, coefs + off, L, lower + off, upper + off);
+    act[4 * t + 0] = a.min_finite;
+    act[4 * t + 1] = a.max_finite;
+    act[4 * t + 2] = a.min_inf;
+    act[4 * t + 3] = a.max_inf;
+    const double lhs = sides[2 * t], rhs = sides[2 * t + 1];
+    klass[t] = classify_f64(&a, lhs, rhs, cfg);
+    for (int32_t k = 0; k < L; ++k) {
+      const int64_t e = off + k;
+      double mn, mx;
+      residual_f64(&a, coefs[e], lower[e], upper[e], &mn, &mx);
+      res[2 * e] = mn;
+      res[2 * e + 1] = mx;
+      for (int integ = 0; integ < 2; ++integ)
+        candidates_f64(coefs[e], lhs, rhs, mn, mx, integ, cfg, &cand[4 * e + 2 * integ],
+                       &cand[4 * e + 2 * integ + 1]);
+      double o2[2];
+      tkind[e] = orc_tighten(lower[e], upper[e], cand[4 * e], cand[4 * e + 1], cfg, o2);
+      tight[2 * e] = o2[0];
+      tight[2 * e + 1] = o2[1];
+    }
+    off += L;
+  }
+}

@@ -19,6 +19,8 @@
 // host synchronisation per round.
 #include <cuda_runtime.h>
 
+#include <dlfcn.h>
+
 #include <algorithm>
 #include <cstdio>
 #include <cstring>
@@ -94,6 +96,43 @@ void check_problem(const pg_problem* p) {
     throw Error{PG_EINVAL, "row_ptr must start at 0 and end at nnz"};
 }
 
+// NCCL, loaded on first use (the single-GPU engine has no NCCL dependency).
+// Values from nccl.h: ncclInt64 = 4, ncclMax = 2; ncclUniqueId = 128 bytes.
+constexpr int kNcclInt64 = 4;
+constexpr int kNcclMax = 2;
+struct NcclUid {
+  char internal[128];
+};
+struct Nccl {
+  void* h = nullptr;
+  int (*get_unique_id)(NcclUid*) = nullptr;
+  int (*comm_init_rank)(void**, int, NcclUid, int) = nullptr;
+  int (*comm_destroy)(void*) = nullptr;
+  int (*all_reduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  const char* (*error_string)(int) = nullptr;
+  bool load() {
+    if (h) return true;
+    for (const char* name : {"libnccl.so.2", "libnccl.so"}) {
+      h = dlopen(name, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    get_unique_id = (int (*)(NcclUid*))dlsym(h, "ncclGetUniqueId");
+    comm_init_rank = (int (*)(void**, int, NcclUid, int))dlsym(h, "ncclCommInitRank");
+    comm_destroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+    all_reduce_fn = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
+        h, "ncclAllReduce");
+    error_string = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    return get_unique_id && comm_init_rank && comm_destroy && all_reduce_fn;
+  }
+  int all_reduce(const void* s, void* r, size_t count, int dt, int op, void* comm,
+                 cudaStream_t st) const {
+    return all_reduce_fn(s, r, count, dt, op, comm, st);
+  }
+  const char* error(int rc) const { return error_string ? error_string(rc) : "nccl error"; }
+};
+Nccl g_nccl;
+
 }  // namespace
 
 struct pg_session {
@@ -149,6 +188,7 @@ struct pg_session {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   cudaStream_t stream2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  void* comm = nullptr;  // NCCL communicator of the row-sharded mode
 
   ~pg_session() {
     if (dev >= 0) cudaSetDevice(dev);
@@ -159,6 +199,7 @@ struct pg_session {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream2) cudaStreamDestroy(stream2);
+    if (comm) g_nccl.comm_destroy(comm);
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
                     d_lo_res, d_up_res, d_tiles, d_groups, d_segs, d_srow, d_sfirst, d_chunk_seg, d_partial,
                     d_row_act, d_worklist, d_st, d_per_round, d_col_ptr, d_col_item,
@@ -235,6 +276,16 @@ struct pg_session {
     if (k1_end) PG_CUDA(cudaEventRecord(k1_end, stream));
     if (nseg > 0)
       k_seg_cand<<<std::min(nseg, num_sms * 8), 256, 0, stream>>>(A, dcfg);
+    if (comm) {
+      // row shards: merge every rank's bound keys (lb keys and negated ub keys)
+      // and infeasibility with one max all-reduce; each rank then commits the
+      // same merged bounds, so counts and decisions need no further exchange
+      k_flag_to_slot<<<1, 32, 0, stream>>>(d_st, d_key_out + n);
+      PG_CUDA(cudaGetLastError());
+      const int rc = g_nccl.all_reduce(d_key_out, d_key_out, 2 * ((size_t)n + 1), kNcclInt64,
+                                       kNcclMax, comm, stream);
+      if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllReduce: ") + g_nccl.error(rc)};
+    }
     k_commit<<<grid_for(n, kCommitThreads), kCommitThreads, 0, stream>>>(
         d_snap, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0);
     if (dirty.enabled) k_mark<<<num_sms * 8, 256, 0, stream>>>(dirty, d_st);
@@ -482,7 +533,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->d_rhs = dalloc<double>((size_t)m + 2);
     s->d_snap = dalloc<Snap>(n);
     s->d_integral = dalloc<uint8_t>(n);
-    s->d_key_out = dalloc<longlong2>(n);
+    s->d_key_out = dalloc<longlong2>((size_t)n + 1);  // + infeasibility slot
     s->d_lo0 = dalloc<double>(n);
     s->d_up0 = dalloc<double>(n);
     s->d_lo_res = dalloc<double>(n);
@@ -822,6 +873,54 @@ int pg_session_time_round_kernel(pg_session* s, int32_t reps, double* mean_ns, d
     // vals + col per entry, row_ptr, lhs/rhs, one {lb, ub} read per column
     *bytes = 12.0 * (double)s->nnz + 4.0 * (double)(s->m + 1) + 16.0 * (double)s->m +
              16.0 * (double)s->n;
+    return PG_OK;
+  });
+}
+
+int pg_nccl_unique_id(uint8_t* out128) {
+  if (!out128) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  if (!g_nccl.load()) {
+    g_err = "libnccl.so.2 could not be loaded";
+    return PG_ENCCL;
+  }
+  NcclUid uid;
+  const int rc = g_nccl.get_unique_id(&uid);
+  if (rc != 0) {
+    g_err = std::string("ncclGetUniqueId: ") + g_nccl.error(rc);
+    return PG_ENCCL;
+  }
+  std::memcpy(out128, uid.internal, 128);
+  return PG_OK;
+}
+
+int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank, int32_t world) {
+  if (!s || !uid128 || world < 1 || rank < 0 || rank >= world) {
+    g_err = "invalid communicator arguments";
+    return PG_EINVAL;
+  }
+  return guarded([&] {
+    PG_CUDA(cudaSetDevice(s->dev));
+    if (!g_nccl.load()) throw Error{PG_ENCCL, "libnccl.so.2 could not be loaded"};
+    NcclUid uid;
+    std::memcpy(uid.internal, uid128, 128);
+    void* comm = nullptr;
+    const int rc = g_nccl.comm_init_rank(&comm, world, uid, rank);
+    if (rc != 0) throw Error{PG_ENCCL, std::string("ncclCommInitRank: ") + g_nccl.error(rc)};
+    if (s->comm) g_nccl.comm_destroy(s->comm);
+    s->comm = comm;
+    // the device-resident loop now carries the all-reduce: rebuild the graph
+    if (s->exec) {
+      cudaGraphExecDestroy(s->exec);
+      s->exec = nullptr;
+    }
+    if (s->graph) {
+      cudaGraphDestroy(s->graph);
+      s->graph = nullptr;
+    }
+    if (s->cfg.loop_mode == PG_LOOP_GRAPH) s->build_graph();
     return PG_OK;
   });
 }

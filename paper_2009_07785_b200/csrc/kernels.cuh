@@ -174,9 +174,11 @@ __device__ __forceinline__ void commit_side(long long* key_out, int j, int kind,
     if (*((volatile long long*)p) < k) atomicMax(p, k);
   }
   if (kind & 2) {
-    const long long k = key_enc(canon0(cu));
+    // upper bounds are kept as NEGATED keys so that one max-reduction merges
+    // both sides (one NCCL all-reduce on the row-sharded path)
+    const long long k = -key_enc(canon0(cu));
     long long* p = key_out + 2 * (size_t)j + 1;
-    if (*((volatile long long*)p) > k) atomicMin(p, k);
+    if (*((volatile long long*)p) < k) atomicMax(p, k);
   }
 }
 
@@ -903,7 +905,7 @@ __global__ void __launch_bounds__(kCommitThreads)
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   for (int j = gtid; j < n; j += gstride) {
     const longlong2 ko = key_out[j];
-    const double lo = key_dec(ko.x), up = key_dec(ko.y);
+    const double lo = key_dec(ko.x), up = key_dec(-ko.y);
     const double2 in = *reinterpret_cast<const double2*>(&snap[j].lo);
     // a change is a strict improvement, so comparing values is exact
     const int c = (lo != in.x) + (up != in.y);
@@ -942,7 +944,10 @@ __global__ void __launch_bounds__(kCommitThreads)
       // last CTA: the round decision of run_parallel (par_engine.cpp:248-266)
       __threadfence();
       const long long ch = (long long)atomicAdd(&st->round_changes, 0ull);
-      const int infeasible = atomicAdd(&st->infeasible, 0);
+      // key_out[n].x: the all-reduced infeasibility of every rank (row shards)
+      volatile long long* slot = (volatile long long*)&key_out[n].x;
+      const int infeasible = atomicAdd(&st->infeasible, 0) | (*slot != 0);
+      *slot = 0;
       const int r = R + 1;
       st->round = r;
       if (r - 1 < cfg.round_limit) per_round[r - 1] = ch;
@@ -976,6 +981,7 @@ __global__ void __launch_bounds__(kCommitThreads)
   int crossed = 0, frac = 0;
   {
     const int gstride = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (gtid == 0) key_out[n] = make_longlong2(0, 0);  // infeasibility slot
     uint32_t* f = reinterpret_cast<uint32_t*>(D.row_flag);
     for (int i = gtid; i < D.ms / 2; i += gstride) f[i] = 0u;
   }
@@ -983,7 +989,7 @@ __global__ void __launch_bounds__(kCommitThreads)
     const double l = lo0[j], u = up0[j];
     const bool in = integral[j] != 0;
     snap[j] = Snap{l, u, column_q(l, u, in, cfg), in ? 1LL : 0LL};
-    key_out[j] = make_longlong2(key_enc(l), key_enc(u));
+    key_out[j] = make_longlong2(key_enc(l), -key_enc(u));
     if (l > __dadd_rn(u, cfg.imp_abs)) crossed = 1;
     if (in && (l != floor(l) || u != ceil(u))) frac = 1;  // floor(+-inf) = +-inf
   }
@@ -1018,13 +1024,19 @@ __global__ void __launch_bounds__(kCommitThreads)
   }
 }
 
+// Row-sharded rounds: this rank's infeasibility into the slot that rides the
+// bound all-reduce (max over {lb key, -ub key, flag}).
+__global__ void k_flag_to_slot(const DevState* __restrict__ st, longlong2* __restrict__ slot) {
+  if (threadIdx.x == 0) slot->x = *((volatile const int32_t*)&st->infeasible) ? 1 : 0;
+}
+
 // keys -> doubles (result download)
 __global__ void k_decode(const longlong2* __restrict__ key, double* __restrict__ lo,
                          double* __restrict__ up, int n) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) {
     const longlong2 k = key[j];
     lo[j] = key_dec(k.x);
-    up[j] = key_dec(k.y);
+    up[j] = key_dec(-k.y);
   }
 }
 

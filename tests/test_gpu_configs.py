@@ -1,0 +1,104 @@
+"""GPU parity on the benchmark configurations, bit-exact
+against the restated cpu_par, plus the multi-GPU code paths on one GPU.
+
+Full sizes are covered where the oracle finishes in seconds; for the larger
+ones a reduced instance of the same recipe and size-independent properties."""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2009_07785_b200 import generators as G
+from paper_2009_07785_b200.engine import Session, propagate_gpu
+from paper_2009_07785_b200.model import EngineConfig, LoopMode, PropagationStatus
+from paper_2009_07785_b200.multi import RowShardedSession, propagate_nodes_sharded
+
+pytestmark = pytest.mark.gpu
+PAR = EngineConfig(row_check=False)
+
+
+def assert_bit_exact(gpu, ref, what=""):
+    assert gpu.status == ref.status, (what, gpu.status, ref.status)
+    assert gpu.rounds_executed == ref.rounds_executed, what
+    assert gpu.per_round_changes == ref.per_round_changes, what
+    assert np.array_equal(O.canon(gpu.bounds.lower), O.canon(ref.bounds.lower)), what
+    assert np.array_equal(O.canon(gpu.bounds.upper), O.canon(ref.bounds.upper)), what
+
+
+def test_c3_long_rows_reduced():
+    """C3 recipe at 1/10 scale: 10k rows, every 100th with 10k-15k entries
+    (chunked long-row path, several chunks per row, groups of 8)."""
+    inst = G.gen_longrows(10000, 20000, 3001, long_every=100, long_min=10000, long_max=15000)
+    for wl in (False, True):
+        cfg = EngineConfig(row_check=False, worklist=wl)
+        assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg), f"c3 wl={wl}")
+
+
+def test_c5_set_partitioning_reduced():
+    inst = G.gen_setpart(100000, 500000, 50, f_fixed=0.2, seed=5001)
+    assert_bit_exact(propagate_gpu(inst, PAR), O.propagate_parallel(inst, PAR), "c5")
+    bad = G.gen_setpart(100000, 500000, 50, f_fixed=0.2, seed=5001, infeasible=True)
+    r = propagate_gpu(bad, EngineConfig())
+    assert r.status == PropagationStatus.Infeasible
+    assert r.status == O.propagate_sequential(bad, PAR).status
+
+
+def test_c4_nodes_match_oracle():
+    inst = G.gen_random(20000, 20000, 4, mean_row_nnz=8.0, integral_fraction=0.5)
+    root = O.propagate_parallel(inst, PAR)
+    lo, up = G.gen_nodes(inst, root.bounds.lower, root.bounds.upper, K=16)
+    k0, k1, blo, bup, st, rd = propagate_nodes_sharded(inst, PAR, lo, up, rank=0, world=1)
+    assert (k0, k1) == (0, 16)
+    for k in range(16):
+        ref = O.propagate_parallel(inst, PAR, lo[k], up[k])
+        assert st[k] == int(ref.status) and rd[k] == ref.rounds_executed
+        assert np.array_equal(O.canon(blo[k]), O.canon(ref.bounds.lower))
+        assert np.array_equal(O.canon(bup[k]), O.canon(ref.bounds.upper))
+
+
+@pytest.mark.parametrize("loop", [LoopMode.Graph, LoopMode.Host])
+def test_row_sharded_nccl_world1(loop):
+    """The row-sharded path (NCCL max all-reduce of the bound keys inside the
+    device loop) with one rank: identical to the plain engine and the oracle."""
+    try:
+        from paper_2009_07785_b200.multi import nccl_unique_id
+        nccl_unique_id()
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    for inst in (G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003),
+                 G.gen_random(4000, 4000, 9, mean_row_nnz=10.0, integral_fraction=0.5)):
+        cfg = EngineConfig(row_check=False, loop_mode=loop)
+        rs = RowShardedSession(inst, cfg, rank=0, world=1)
+        try:
+            assert_bit_exact(rs.propagate(), O.propagate_parallel(inst, PAR), inst.name)
+        finally:
+            rs.close()
+    bad = G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003, infeasible=True)
+    rs = RowShardedSession(bad, EngineConfig(), rank=0, world=1)
+    assert rs.propagate().status == PropagationStatus.Infeasible
+    rs.close()
+
+
+@pytest.mark.slow
+def test_c2_full_seeds_properties():
+    """C2 full size, two more seeds: bit-exact to the restated cpu_par, and
+    re-propagating the fixpoint is a 1-round no-op (idempotence)."""
+    for seed in (20090779, 20090780):
+        inst = G.config_instance("c2", seed)
+        with Session(inst, PAR) as s:
+            r = s.propagate()
+            assert_bit_exact(r, O.propagate_parallel(inst, PAR), inst.name)
+            again = s.propagate(r.bounds.lower, r.bounds.upper)
+            assert again.status == PropagationStatus.Converged and again.rounds_executed == 1
+
+
+@pytest.mark.slow
+def test_c1_seeds_vs_seq_verdicts():
+    for seed in range(1, 6):
+        inst = G.config_instance("c1", seed)
+        gpu = propagate_gpu(inst)
+        seq = O.propagate_sequential(inst, PAR)
+        assert (gpu.status == PropagationStatus.Infeasible) == (seq.status == PropagationStatus.Infeasible)
+        if gpu.status == seq.status == PropagationStatus.Converged:
+            integ = inst.integral.astype(bool)
+            assert np.array_equal(gpu.bounds.lower[integ], seq.bounds.lower[integ])
+            assert O.bounds_equal(seq.bounds.lower, gpu.bounds.lower).all()
