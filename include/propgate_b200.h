@@ -176,6 +176,24 @@ int pg_session_propagate_batch(pg_session* s, int32_t K, const double* lower,
 int pg_session_time_round_kernel(pg_session* s, int32_t reps, double* mean_ns,
                                  double* bytes);
 
+/* ---- branch-and-bound nodes (config 4) -----------------------------------
+ * pg_session_set_root propagates the session's start bounds and, when the
+ * result is Converged, keeps that fixpoint on the device as the root.
+ * pg_session_propagate_nodes then solves K child nodes, each the root with a
+ * few bounds overridden (node k: entries node_ptr[k]..node_ptr[k+1]-1 of
+ * vars/lo/up), back to back in one stream with no host round trip per node.
+ * With PG_FLAG_WORKLIST, a node's round 1 visits only the rows containing an
+ * overridden column (exact: every other row's candidates were rejected
+ * against the same bounds in the root's confirming round).  Per-node results
+ * are those of pg_propagate on the node's full bounds; lower_out/upper_out
+ * ([K * num_cols], node-major) may be NULL.  elapsed_ns: device time of all
+ * K solves. */
+int pg_session_set_root(pg_session* s, pg_result* res);
+int pg_session_propagate_nodes(pg_session* s, int32_t K, const int32_t* node_ptr,
+                               const int32_t* vars, const double* lo, const double* up,
+                               int32_t* status, int32_t* rounds, double* lower_out,
+                               double* upper_out, int64_t* elapsed_ns);
+
 /* ---- row-sharded multi-GPU (config 5): one process per GPU --------------
  * New capability (the reference is single-process).  Each rank creates a
  * session over its contiguous row shard (all columns), rank 0 draws an NCCL

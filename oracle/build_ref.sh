@@ -36,4 +36,11 @@ for p in "${pids[@]}"; do wait "$p"; done
 LIBOBJS="$OBJ/model.o $OBJ/generators.o $OBJ/seq_engine.o $OBJ/par_engine.o $OBJ/mps.o $OBJ/harness.o"
 $CXX -shared -pthread -o "$OUT/libpropgate_ref.so" $LIBOBJS "$OBJ/ref_shim.o"
 $CXX -pthread -o "$OUT/acceptance" $LIBOBJS "$OBJ/acceptance.o"
+# drop-in check: reference types/engines + the GPU engine via include/propgate_b200.hpp
+REPO="$(cd "$HERE/.." && pwd)"
+if [ -f "$REPO/paper_2009_07785_b200/libpropgate_b200.so" ]; then
+  $CXX $FLAGS -I"$REPO/include" -c "$REPO/tests/cpp/gpu_dropin.cpp" -o "$OBJ/gpu_dropin.o"
+  $CXX -pthread -o "$OUT/gpu_dropin" $LIBOBJS "$OBJ/gpu_dropin.o" \
+      -L"$REPO/paper_2009_07785_b200" -lpropgate_b200 -Wl,-rpath,'$ORIGIN/../../paper_2009_07785_b200'
+fi
 echo "build_ref: ok -> $OUT"

@@ -118,6 +118,9 @@ PROTOTYPES = {
     "pg_session_propagate_batch": (C.c_int, [C.c_void_p, C.c_int32, _dp, _dp, _dp, _dp, _ip, _ip]),
     "pg_session_time_round_kernel": (C.c_int, [C.c_void_p, C.c_int32, _dp, _dp]),
     "pg_session_info": (C.c_int, [C.c_void_p, _lp, C.c_int32]),
+    "pg_session_set_root": (C.c_int, [C.c_void_p, C.POINTER(PgResult)]),
+    "pg_session_propagate_nodes": (C.c_int, [C.c_void_p, C.c_int32, _ip, _ip, _dp, _dp, _ip, _ip,
+                                             _dp, _dp, _lp]),
     "pg_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "pg_session_attach_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32]),
     "pg_last_error": (C.c_char_p, []),

@@ -189,6 +189,11 @@ struct pg_session {
   cudaStream_t stream2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* comm = nullptr;  // NCCL communicator of the row-sharded mode
+  // branch-and-bound: the root fixpoint and the next solve's start control
+  NodeCtl* d_ctl = nullptr;
+  double* d_root_lo = nullptr;
+  double* d_root_up = nullptr;
+  bool has_root = false;
 
   ~pg_session() {
     if (dev >= 0) cudaSetDevice(dev);
@@ -200,6 +205,8 @@ struct pg_session {
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream2) cudaStreamDestroy(stream2);
     if (comm) g_nccl.comm_destroy(comm);
+    for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up})
+      if (p) cudaFree(p);
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
                     d_lo_res, d_up_res, d_tiles, d_groups, d_segs, d_srow, d_sfirst, d_chunk_seg, d_partial,
                     d_row_act, d_worklist, d_st, d_per_round, d_col_ptr, d_col_item,
@@ -294,16 +301,17 @@ struct pg_session {
 
   void enqueue_reset(bool use_graph, bool check_crossed) {
     k_reset<<<grid_for(n, kCommitThreads), kCommitThreads, 0, stream>>>(
-        d_lo0, d_up0, d_integral, d_snap, d_key_out, n, d_st, dcfg, dirty, check_crossed ? 1 : 0,
-        cond, use_graph ? 1 : 0);
+        d_lo0, d_up0, d_integral, d_snap, d_key_out, n, d_st, dcfg, dirty, d_ctl,
+        check_crossed ? 1 : 0, cond, use_graph ? 1 : 0);
+    if (dirty.enabled) k_mark_vars<<<num_sms * 2, 256, 0, stream>>>(dirty, d_ctl);
     PG_CUDA(cudaGetLastError());
   }
 
   void build_graph() {
     PG_CUDA(cudaGraphCreate(&graph, 0));
     PG_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
-    // node 1: reset (captured)
-    cudaGraphNode_t reset_node;
+    // node 1: reset (+ warm-start marks), captured
+    cudaGraphNode_t reset_node = nullptr;
     {
       cudaGraph_t g2 = nullptr;
       PG_CUDA(cudaStreamBeginCaptureToGraph(stream, graph, nullptr, nullptr, 0,
@@ -314,7 +322,11 @@ struct pg_session {
       PG_CUDA(cudaGraphGetNodes(graph, nullptr, &count));
       std::vector<cudaGraphNode_t> nodes(count);
       PG_CUDA(cudaGraphGetNodes(graph, nodes.data(), &count));
-      reset_node = nodes.back();
+      for (cudaGraphNode_t nd : nodes) {  // the sink of the captured chain
+        size_t deps = 0;
+        PG_CUDA(cudaGraphNodeGetDependentNodes(nd, nullptr, &deps));
+        if (deps == 0) reset_node = nd;
+      }
     }
     // node 2: WHILE(cond) { round }
     cudaGraphNodeParams cp = {};
@@ -549,6 +561,8 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->d_worklist = dalloc<int32_t>(T.segs.size());
     s->d_row_done = dalloc<int32_t>(T.srow.size());
     s->d_st = dalloc<DevState>(1);
+    s->d_ctl = dalloc<NodeCtl>(1);
+    PG_CUDA(cudaMemset(s->d_ctl, 0, sizeof(NodeCtl)));  // cold starts
     s->d_per_round = dalloc<long long>(cfg->round_limit);
     PG_CUDA(cudaMallocHost(&s->h_st, sizeof(DevState)));
 
@@ -838,6 +852,117 @@ int pg_session_propagate_batch(pg_session* s, int32_t K, const double* lower, co
       status[k] = r.status;
       rounds[k] = r.rounds_executed;
     }
+    return PG_OK;
+  });
+}
+
+int pg_session_set_root(pg_session* s, pg_result* res) {
+  if (!s || !res) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  return guarded([&] {
+    PG_CUDA(cudaSetDevice(s->dev));
+    const int64_t ns = s->run_solve(true);
+    s->fill_result(res, ns);
+    s->has_root = res->status == PG_CONVERGED;
+    if (s->has_root) {
+      if (!s->d_root_lo) {
+        s->d_root_lo = dalloc<double>(s->n);
+        s->d_root_up = dalloc<double>(s->n);
+      }
+      k_decode<<<s->grid_for(s->n, 256), 256, 0, s->stream>>>(s->d_key_out, s->d_root_lo,
+                                                              s->d_root_up, s->n);
+      PG_CUDA(cudaGetLastError());
+      PG_CUDA(cudaStreamSynchronize(s->stream));
+    }
+    return PG_OK;
+  });
+}
+
+int pg_session_propagate_nodes(pg_session* s, int32_t K, const int32_t* node_ptr,
+                               const int32_t* vars, const double* lo, const double* up,
+                               int32_t* status, int32_t* rounds, double* lower_out,
+                               double* upper_out, int64_t* elapsed_ns) {
+  if (!s || K < 0 || (K && (!node_ptr || !status || !rounds))) {
+    g_err = "invalid node arguments";
+    return PG_EINVAL;
+  }
+  if (!s->has_root) {
+    g_err = "pg_session_set_root must succeed (Converged) before propagating nodes";
+    return PG_EINVAL;
+  }
+  return guarded([&] {
+    PG_CUDA(cudaSetDevice(s->dev));
+    const int32_t total = node_ptr[K];
+    for (int32_t k = 0; k < K; ++k)
+      if (node_ptr[k + 1] < node_ptr[k]) throw Error{PG_EINVAL, "node_ptr must be nondecreasing"};
+    for (int32_t i = 0; i < total; ++i)
+      if (vars[i] < 0 || vars[i] >= s->n) throw Error{PG_EINVAL, "node override column out of range"};
+    int32_t* d_vars = dalloc<int32_t>(total);
+    double* d_lo = dalloc<double>(total);
+    double* d_up = dalloc<double>(total);
+    NodeCtl* d_ctls = dalloc<NodeCtl>(K);
+    int2* d_out = dalloc<int2>(K);
+    cudaStream_t st = s->stream;
+    if (total) {
+      PG_CUDA(cudaMemcpyAsync(d_vars, vars, sizeof(int32_t) * total, cudaMemcpyHostToDevice, st));
+      PG_CUDA(cudaMemcpyAsync(d_lo, lo, sizeof(double) * total, cudaMemcpyHostToDevice, st));
+      PG_CUDA(cudaMemcpyAsync(d_up, up, sizeof(double) * total, cudaMemcpyHostToDevice, st));
+    }
+    std::vector<NodeCtl> ctls(K);
+    for (int32_t k = 0; k < K; ++k)
+      ctls[k] = NodeCtl{1, node_ptr[k + 1] - node_ptr[k], d_vars + node_ptr[k], d_lo + node_ptr[k],
+                        d_up + node_ptr[k]};
+    if (K) PG_CUDA(cudaMemcpyAsync(d_ctls, ctls.data(), sizeof(NodeCtl) * K, cudaMemcpyHostToDevice, st));
+    const size_t n = (size_t)s->n;
+    PG_CUDA(cudaEventRecord(s->ev0, st));
+    for (int32_t k = 0; k < K; ++k) {
+      // stream-ordered: root -> start bounds, overrides, warm control, solve
+      PG_CUDA(cudaMemcpyAsync(s->d_lo0, s->d_root_lo, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      PG_CUDA(cudaMemcpyAsync(s->d_up0, s->d_root_up, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      PG_CUDA(cudaMemcpyAsync(s->d_ctl, d_ctls + k, sizeof(NodeCtl), cudaMemcpyDeviceToDevice, st));
+      k_apply_node<<<4, 256, 0, st>>>(s->d_lo0, s->d_up0, s->d_ctl, s->cfg.infinity_threshold);
+      PG_CUDA(cudaGetLastError());
+      if (s->cfg.loop_mode == PG_LOOP_GRAPH) {
+        PG_CUDA(cudaGraphLaunch(s->exec, st));
+      } else {
+        s->enqueue_reset(false, true);
+        PG_CUDA(cudaMemcpyAsync(s->h_st, s->d_st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+        PG_CUDA(cudaStreamSynchronize(st));
+        while (!s->h_st->done) {
+          s->enqueue_round(false);
+          PG_CUDA(cudaMemcpyAsync(s->h_st, s->d_st, sizeof(DevState), cudaMemcpyDeviceToHost, st));
+          PG_CUDA(cudaStreamSynchronize(st));
+        }
+      }
+      // (status, round) of the node, stream-ordered, no host sync
+      PG_CUDA(cudaMemcpyAsync(&d_out[k].x, &s->d_st->status, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      PG_CUDA(cudaMemcpyAsync(&d_out[k].y, &s->d_st->round, sizeof(int32_t), cudaMemcpyDeviceToDevice, st));
+      if (lower_out || upper_out) {
+        k_decode<<<s->grid_for(s->n, 256), 256, 0, st>>>(s->d_key_out, s->d_lo_res, s->d_up_res, s->n);
+        if (lower_out)
+          PG_CUDA(cudaMemcpyAsync(lower_out + k * n, s->d_lo_res, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+        if (upper_out)
+          PG_CUDA(cudaMemcpyAsync(upper_out + k * n, s->d_up_res, sizeof(double) * n, cudaMemcpyDeviceToHost, st));
+      }
+    }
+    PG_CUDA(cudaEventRecord(s->ev1, st));
+    PG_CUDA(cudaMemsetAsync(s->d_ctl, 0, sizeof(NodeCtl), st));  // later solves start cold
+    // the session's start bounds are the root fixpoint again
+    PG_CUDA(cudaMemcpyAsync(s->d_lo0, s->d_root_lo, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    PG_CUDA(cudaMemcpyAsync(s->d_up0, s->d_root_up, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+    std::vector<int2> out(K);
+    if (K) PG_CUDA(cudaMemcpyAsync(out.data(), d_out, sizeof(int2) * K, cudaMemcpyDeviceToHost, st));
+    PG_CUDA(cudaStreamSynchronize(st));
+    float ms = 0.f;
+    PG_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+    if (elapsed_ns) *elapsed_ns = (int64_t)((double)ms * 1e6);
+    for (int32_t k = 0; k < K; ++k) {
+      status[k] = out[k].x < 0 ? PG_ROUNDLIMIT : out[k].x;
+      rounds[k] = out[k].y;
+    }
+    for (void* p : {(void*)d_vars, (void*)d_lo, (void*)d_up, (void*)d_ctls, (void*)d_out}) cudaFree(p);
     return PG_OK;
   });
 }

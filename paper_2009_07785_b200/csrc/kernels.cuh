@@ -74,6 +74,17 @@ struct Dirty {
   int32_t enabled;
 };
 
+// Start of the next solve (device memory, set by stream-ordered copies):
+// warm = 1 for a branch-and-bound node started from the session's root
+// fixpoint, with `nvars` overridden columns vars[i] -> [lo[i], up[i]].
+struct NodeCtl {
+  int32_t warm;
+  int32_t nvars;
+  const int32_t* vars;
+  const double* lo;
+  const double* up;
+};
+
 // Per-column snapshot record, gathered with one 256-bit load per entry.
 //   lo, up  the round's input bounds (bounds_in of par_engine.cpp:162)
 //   q       filter coefficient (see entry_x), +inf = always examine
@@ -977,7 +988,8 @@ __global__ void __launch_bounds__(kCommitThreads)
     k_reset(const double* __restrict__ lo0, const double* __restrict__ up0,
             const uint8_t* __restrict__ integral, Snap* __restrict__ snap,
             longlong2* __restrict__ key_out, int n, DevState* __restrict__ st, const DevCfg cfg,
-            const Dirty D, int check_crossed, cudaGraphConditionalHandle cond, int use_graph) {
+            const Dirty D, const NodeCtl* __restrict__ ctl, int check_crossed,
+            cudaGraphConditionalHandle cond, int use_graph) {
   int crossed = 0, frac = 0;
   {
     const int gstride = gridDim.x * blockDim.x, gtid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1013,7 +1025,9 @@ __global__ void __launch_bounds__(kCommitThreads)
       st->crossed = 0;
       st->wl_count = 0;
       st->work = 0;
-      st->full = 1;
+      // warm start from a root fixpoint: round 1 visits only the rows that
+      // k_mark_vars marks (see NodeCtl)
+      st->full = (D.enabled && ctl->warm) ? 0 : 1;
       st->nchg[0] = st->nchg[1] = 0;
       st->frac_any = atomicAdd(&st->frac_tmp, 0);
       st->frac_tmp = 0;
@@ -1073,6 +1087,35 @@ __global__ void k_permute_rows(const int32_t* __restrict__ rp, const int32_t* __
       new_lhs[i] = l >= thr ? CUDART_INF : (l <= -thr ? -CUDART_INF : l);
       new_rhs[i] = h >= thr ? CUDART_INF : (h <= -thr ? -CUDART_INF : h);
     }
+  }
+}
+
+// Warm start of a branch-and-bound node (config C4): the start bounds are a
+// converged root fixpoint with a few bounds overridden.  Every row of the
+// root had all of its candidates rejected against the root bounds in the
+// root's confirming round, so in the node's round 1 only rows containing an
+// overridden column can produce anything; marking exactly those keeps the
+// trajectory identical to a full sweep.
+__global__ void __launch_bounds__(256)
+    k_mark_vars(const Dirty D, const NodeCtl* __restrict__ ctl) {
+  if (!D.enabled || !ctl->warm) return;
+  uint8_t* flag = D.row_flag + (size_t)1 * D.ms;  // round 1 reads buffer (0 + 1) & 1
+  const int lane = threadIdx.x & 31;
+  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ctl->nvars;
+       w += (gridDim.x * blockDim.x) >> 5) {
+    const int j = ctl->vars[w];
+    for (int e = D.col_ptr[j] + lane; e < D.col_ptr[j + 1]; e += 32) flag[D.col_row[e]] = 1;
+  }
+}
+
+// start bounds of a node: the root fixpoint (copied before) + its overrides
+__global__ void k_apply_node(double* __restrict__ lo0, double* __restrict__ up0,
+                             const NodeCtl* __restrict__ ctl, double thr) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ctl->nvars; i += gridDim.x * blockDim.x) {
+    const int j = ctl->vars[i];
+    const double l = ctl->lo[i], u = ctl->up[i];
+    lo0[j] = l >= thr ? CUDART_INF : (l <= -thr ? -CUDART_INF : l);
+    up0[j] = u >= thr ? CUDART_INF : (u <= -thr ? -CUDART_INF : u);
   }
 }
 

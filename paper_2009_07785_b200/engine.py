@@ -168,3 +168,49 @@ class Session:
         v = np.zeros(len(self.INFO_FIELDS), dtype=np.int64)
         abi.check(_lib().pg_session_info(self._h, abi.ptr(v, C.c_int64), v.shape[0]), "info")
         return dict(zip(self.INFO_FIELDS, (int(x) for x in v)))
+
+    # ---- branch-and-bound nodes (config C4) ------------------------------------
+    def set_root(self) -> PropagationResult:
+        """Propagate the start bounds; a Converged result becomes the
+        device-resident root for propagate_nodes."""
+        n = self.instance.num_cols()
+        r, lo, up, prc = new_c_result(n, self.cfg.round_limit)
+        abi.check(_lib().pg_session_set_root(self._h, C.byref(r)), "pg_session_set_root")
+        return result_from_c(r, lo, up, prc)
+
+    def propagate_nodes(self, node_ptr, vars_, lo, up, want_bounds=False):
+        """K child nodes of the root, node k overriding vars_[node_ptr[k]:node_ptr[k+1]]
+        with [lo, up].  Returns (status[K], rounds[K], lower[K,n]|None,
+        upper[K,n]|None, device_ns)."""
+        node_ptr = np.ascontiguousarray(node_ptr, dtype=np.int32)
+        vars_ = np.ascontiguousarray(vars_, dtype=np.int32)
+        lo = np.ascontiguousarray(lo, dtype=np.float64)
+        up = np.ascontiguousarray(up, dtype=np.float64)
+        K = node_ptr.shape[0] - 1
+        n = self.instance.num_cols()
+        st = np.zeros(K, dtype=np.int32)
+        rd = np.zeros(K, dtype=np.int32)
+        lo_out = np.empty((K, n)) if want_bounds else None
+        up_out = np.empty((K, n)) if want_bounds else None
+        ns = C.c_int64()
+        abi.check(_lib().pg_session_propagate_nodes(
+            self._h, K, abi.ptr(node_ptr, C.c_int32), abi.ptr(vars_, C.c_int32),
+            abi.ptr(lo, C.c_double), abi.ptr(up, C.c_double), abi.ptr(st, C.c_int32),
+            abi.ptr(rd, C.c_int32), abi.ptr(lo_out, C.c_double), abi.ptr(up_out, C.c_double),
+            C.byref(ns)), "pg_session_propagate_nodes")
+        return st, rd, lo_out, up_out, ns.value
+
+
+def node_overrides(root_lower, root_upper, lower, upper):
+    """Sparse form of node bound vectors ([K, n]) relative to the root:
+    (node_ptr, vars, lo, up)."""
+    ptr, vs, ls, us = [0], [], [], []
+    for k in range(lower.shape[0]):
+        d = np.flatnonzero((lower[k] != root_lower) | (upper[k] != root_upper))
+        vs.append(d)
+        ls.append(lower[k][d])
+        us.append(upper[k][d])
+        ptr.append(ptr[-1] + len(d))
+    cat = (lambda xs, dt: np.concatenate(xs).astype(dt) if xs else np.zeros(0, dt))
+    return (np.array(ptr, dtype=np.int32), cat(vs, np.int32), cat(ls, np.float64),
+            cat(us, np.float64))

@@ -102,3 +102,31 @@ def test_c1_seeds_vs_seq_verdicts():
             integ = inst.integral.astype(bool)
             assert np.array_equal(gpu.bounds.lower[integ], seq.bounds.lower[integ])
             assert O.bounds_equal(seq.bounds.lower, gpu.bounds.lower).all()
+
+
+@pytest.mark.parametrize("worklist", [False, True])
+def test_c4_warm_started_nodes(worklist):
+    """Nodes relative to a device-resident root fixpoint (sparse overrides);
+    with the worklist, round 1 visits only rows of the branched columns --
+    results identical to full propagations of the node bounds."""
+    from paper_2009_07785_b200.engine import node_overrides
+    inst = G.gen_random(30000, 30000, 4, mean_row_nnz=8.0, integral_fraction=0.5)
+    cfg = EngineConfig(row_check=False, worklist=worklist)
+    with Session(inst, cfg) as s:
+        root = s.set_root()
+        assert root.status == PropagationStatus.Converged
+        ref_root = O.propagate_parallel(inst, PAR)
+        assert np.array_equal(O.canon(root.bounds.lower), O.canon(ref_root.bounds.lower))
+        lo, up = G.gen_nodes(inst, root.bounds.lower, root.bounds.upper, K=24)
+        ptr, vs, ls, us = node_overrides(root.bounds.lower, root.bounds.upper, lo, up)
+        st, rd, blo, bup, ns = s.propagate_nodes(ptr, vs, ls, us, want_bounds=True)
+        assert ns > 0
+        for k in range(24):
+            ref = O.propagate_parallel(inst, PAR, lo[k], up[k])
+            assert st[k] == int(ref.status) and rd[k] == ref.rounds_executed, k
+            assert np.array_equal(O.canon(blo[k]), O.canon(ref.bounds.lower)), k
+            assert np.array_equal(O.canon(bup[k]), O.canon(ref.bounds.upper)), k
+        # afterwards the session's start bounds are the root fixpoint: a cold
+        # solve confirms it in one round
+        again = s.propagate()
+        assert again.status == PropagationStatus.Converged and again.rounds_executed == 1
