@@ -194,44 +194,45 @@ def cpu_baseline(inst, budget_s=25.0):
             "status": res.status.name, "rounds": res.rounds_executed}, res
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
-    ap.add_argument("--seed", type=int, default=None)
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--e2e-steps", type=int, default=3)
-    args = ap.parse_args()
-    args.warmup = max(args.warmup, 3)
-
-    world, rank, local = dist_init()
-    inst = make_instance(args.config, args.seed)
-    if args.impl == "reference":
-        run_reference(args, inst, rank, world)
-        return
-
+def _gpu_setup(local, world):
     import torch
     import torch.distributed as dist
-
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return torch, dist
 
+
+def _max_over_ranks(torch, dist, world, local, v):
+    if world > 1:
+        t = torch.tensor([v], dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        v = float(t.item())
+    return v
+
+
+def _common_line(args, world, ms, scaling, workload, extra_cfg):
+    return {"metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": False, "scaling": scaling, "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": workload, **extra_cfg}}
+
+
+def bench_single(args, inst, world, rank, local):
+    """C1/C2/C3: one instance per GPU (N > 1: independent replicas)."""
+    torch, dist = _gpu_setup(local, world)
     from paper_2009_07785_b200.engine import Session, propagate_gpu
     from paper_2009_07785_b200.model import EngineConfig
 
-    cfg = EngineConfig(device=local)
+    cfg = EngineConfig(device=local, worklist=args.worklist)
     m, n, nnz = inst.num_rows(), inst.num_cols(), inst.matrix.nnz()
     sess = Session(inst, cfg)
     info = sess.info()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
-
     for _ in range(args.warmup):
         r = sess.run()
-    launches_per_round = 1 + (1 if info["segments"] else 0) + 1
+    launches_per_round = 2 + (1 if info["segments"] else 0) + (1 if info["num_tiles"] else 0) + (
+        1 if args.worklist else 0)
 
     def barrier():
         torch.cuda.synchronize()
@@ -251,51 +252,43 @@ def main():
             rounds.append(r.rounds_executed)
         barrier()
         wall_ms = (time.perf_counter() - t0) * 1e3
-    total_ms = float(np.sum(step_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms = total_ms / args.steps
+    ms = _max_over_ranks(torch, dist, world, local, float(np.sum(step_ms))) / args.steps
     R = rounds[-1]
     gpu_launches = sum(1 + rr * launches_per_round for rr in rounds)
 
-    # dominant kernel alone (roofline)
+    # dominant kernels alone (roofline), first-round snapshot
     k_ns, k_bytes = sess.time_round_kernel(reps=20)
     peak, peak_kind = hbm_peak()
     achieved = k_bytes / (k_ns * 1e-9) / 1e9
 
-    # e2e through the C-ABI with pinned host buffers
+    # e2e through the C-ABI (pg_propagate) with pinned host buffers
     pinned = pinned_copy(inst)
     e2e = []
-    for i in range(args.e2e_steps + 1):
+    for _ in range(args.e2e_steps + 1):
         torch.cuda.synchronize()
         t1 = time.perf_counter()
         re = propagate_gpu(pinned, cfg)
         e2e.append((time.perf_counter() - t1) * 1e3)
-    e2e_ms = float(np.median(e2e[1:]))
+    e2e_ms = _max_over_ranks(torch, dist, world, local, float(np.median(e2e[1:])))
     assert re.status == r.status and re.rounds_executed == R
 
-    line = {
-        "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic",
-        "config": {"workload": args.config, "instance": inst.name, "m": m, "n": n, "nnz": nnz,
-                   "parallelism": "replicas" if world > 1 else "single-gpu",
-                   "l2": "flushed between steps (256 MB write); instance > L2",
-                   "warp_tiles": info["num_tiles"], "segment_rows": info["seg_rows"],
-                   "segments": info["segments"]},
+    line = _common_line(args, world, ms, "weak", args.config, {
+        "instance": inst.name, "m": m, "n": n, "nnz": nnz,
+        "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
+        "worklist": args.worklist, "l2": "flushed between steps (256 MB write); instance > L2",
+        "warp_tiles": info["num_tiles"], "segment_rows": info["seg_rows"],
+        "segments": info["segments"]})
+    line.update({
         "rounds": R, "status": r.status.name,
         "rounds_per_s": round(R / (ms / 1e3), 1),
         "ms_per_round": round(ms / max(R, 1), 5),
         "gbs_per_round": round(b_round(m, n, nnz) * R / (ms / 1e3) / 1e9, 1),
         "round_roofline_frac": round(b_round(m, n, nnz) * R / (ms / 1e3) / 1e9 / peak, 4),
-        "round_roofline_frac_8tbs": round(b_round(m, n, nnz) * R / (ms / 1e3) / 8e12 * 1e9 / 1e9, 4),
+        "round_roofline_frac_8tbs": round(b_round(m, n, nnz) * R / (ms / 1e3) / 8e12, 4),
         "wall_ms_per_step": round(wall_ms / args.steps, 3),
-        "roofline": {"kernel": "k_round", "bound": "hbm", "achieved": round(achieved, 1),
-                     "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
-                     "frac": round(achieved / peak, 4), "traffic": None,
+        "roofline": {"kernel": "k_round+k_tiles (dense round)", "bound": "hbm",
+                     "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
                      "bytes_per_launch": k_bytes, "launch_us": round(k_ns / 1e3, 3),
                      "share_of_round": round(k_ns / 1e6 / (ms / max(R, 1)), 3)},
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
@@ -303,16 +296,151 @@ def main():
                 "d2h_bytes_per_step": int(16 * n + 8 * R)},
         "gpu_launches": int(gpu_launches),
         "clocks": clk.summary(),
-    }
+    })
     if rank == 0 and not args.no_cpu_baseline:
-        cb, cres = cpu_baseline(inst)
+        cb, _ = cpu_baseline(inst)
         line["cpu_baseline"] = cb
         line["speedup_vs_cpu_seq"] = round(cb["value"] / ms, 2)
         line["e2e_speedup_vs_cpu_seq"] = round(cb["value"] / e2e_ms, 2)
+    sess.close()
+    return line
+
+
+def c4_nodes(inst, root_lo, root_up, k0, k1):
+    from paper_2009_07785_b200 import generators as G
+    from paper_2009_07785_b200.engine import node_overrides
+    lo, up = G.gen_nodes(inst, root_lo, root_up, K=k1 - k0, seed_base=4_000_000 + k0)
+    return lo, up, node_overrides(root_lo, root_up, lo, up)
+
+
+def bench_nodes(args, inst, world, rank, local):
+    """C4: K branch-and-bound child nodes of the root fixpoint, node-sharded
+    (contiguous slices, matrix replicated, no per-round communication)."""
+    torch, dist = _gpu_setup(local, world)
+    from paper_2009_07785_b200.engine import Session
+    from paper_2009_07785_b200.model import EngineConfig
+    from paper_2009_07785_b200.multi import node_shards
+
+    cfg = EngineConfig(device=local, worklist=True)
+    k0, k1 = node_shards(args.nodes, world)[rank]
+    sess = Session(inst, cfg)
+    root = sess.set_root()
+    _, _, (ptr, vs, ls, us) = c4_nodes(inst, root.bounds.lower, root.bounds.upper, k0, k1)
+    for _ in range(args.warmup):
+        sess.propagate_nodes(ptr[: min(65, len(ptr))], vs, ls, us)
+    times = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for _ in range(args.steps):
+            st, rd, _, _, ns = sess.propagate_nodes(ptr, vs, ls, us)
+            times.append(ns / 1e6)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = _max_over_ranks(torch, dist, world, local, float(np.mean(times)))
+    K = args.nodes
+    line = _common_line(args, world, ms, "strong", "c4", {
+        "instance": inst.name, "m": inst.num_rows(), "n": inst.num_cols(),
+        "nnz": inst.matrix.nnz(), "nodes": K, "parallelism": f"node-sharded x{world}",
+        "root_rounds": root.rounds_executed, "warm_start": "root fixpoint + device worklist"})
+    line.update({"nodes_per_s": round(K / (ms / 1e3), 1), "ms_per_node": round(ms / (k1 - k0), 4),
+                 "rounds_mean": round(float(np.mean(rd)), 3),
+                 "status_counts": {str(s): int((st == s).sum()) for s in np.unique(st)},
+                 "clocks": clk.summary(), "gpu_launches": None,
+                 "e2e": {"value": round(ms, 4), "unit": "ms",
+                         "h2d_bytes_per_step": int(4 * len(ptr) + 20 * len(vs)),
+                         "d2h_bytes_per_step": int(8 * (k1 - k0))}})
+    if rank == 0 and not args.no_cpu_baseline:
+        from oracle import oracle as O
+        sample = 16
+        lo, up, _ = c4_nodes(inst, root.bounds.lower, root.bounds.upper, 0, sample)
+        fn = O.ref_propagate_sequential if O.ref_available() else O.propagate_sequential
+        t = [fn(inst, EngineConfig(), lo[k], up[k]).elapsed_ns / 1e6 for k in range(sample)]
+        per = float(np.mean(t))
+        line["cpu_baseline"] = {"value": round(per * K, 1), "unit": "ms", "cores": 1,
+                                "kind": "reference" if O.ref_available() else "port",
+                                "sample": f"cpu_seq on nodes 0..{sample - 1}, mean {per:.2f} ms/node "
+                                          f"x {K} nodes (extrapolated)"}
+        line["speedup_vs_cpu_seq"] = round(per * K / ms, 2)
+    sess.close()
+    return line
+
+
+def bench_rowshard(args, inst, world, rank, local):
+    """C5: one 50M-entry set-partitioning instance, row-sharded over the
+    GPUs; one NCCL max all-reduce merges the bound keys every round."""
+    torch, dist = _gpu_setup(local, world)
+    from paper_2009_07785_b200.model import EngineConfig
+    from paper_2009_07785_b200.multi import RowShardedSession
+
+    cfg = EngineConfig(device=local, worklist=args.worklist)
+    rs = RowShardedSession(inst, cfg, rank, world)
+    for _ in range(args.warmup):
+        r = rs.run()
+    times = []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        for _ in range(args.steps):
+            r = rs.run()
+            times.append(r.elapsed_ns / 1e6)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+    ms = _max_over_ranks(torch, dist, world, local, float(np.mean(times)))
+    m, n, nnz = inst.num_rows(), inst.num_cols(), inst.matrix.nnz()
+    R = r.rounds_executed
+    line = _common_line(args, world, ms, "strong", "c5", {
+        "instance": inst.name, "m": m, "n": n, "nnz": nnz,
+        "parallelism": f"row-sharded x{world} (NCCL max all-reduce of bound keys)",
+        "worklist": args.worklist})
+    line.update({"rounds": R, "status": r.status.name, "rounds_per_s": round(R / (ms / 1e3), 1),
+                 "gbs_per_round": round(b_round(m, n, nnz) * R / (ms / 1e3) / 1e9, 1),
+                 "clocks": clk.summary(), "gpu_launches": None,
+                 "e2e": {"value": round(ms, 4), "unit": "ms", "h2d_bytes_per_step": 0,
+                         "d2h_bytes_per_step": 8 * R}})
+    if rank == 0 and not args.no_cpu_baseline:
+        cb, _ = cpu_baseline(inst, budget_s=40.0)
+        line["cpu_baseline"] = cb
+        line["speedup_vs_cpu_seq"] = round(cb["value"] / ms, 2)
+    rs.close()
+    return line
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
+    ap.add_argument("--seed", type=int, default=None)
+    ap.add_argument("--nodes", type=int, default=8192, help="C4: number of B&B nodes")
+    ap.add_argument("--worklist", type=int, default=0, help="device-side worklist (exact)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    args.worklist = bool(args.worklist)
+
+    world, rank, local = dist_init()
+    inst = make_instance(args.config, args.seed)
+    if args.impl == "reference":
+        run_reference(args, inst, rank, world)
+        return
+    if args.config == "c4":
+        line = bench_nodes(args, inst, world, rank, local)
+    elif args.config == "c5":
+        line = bench_rowshard(args, inst, world, rank, local)
+    else:
+        line = bench_single(args, inst, world, rank, local)
     if rank == 0:
         print(json.dumps(line), flush=True)
-    sess.close()
     if world > 1:
+        import torch.distributed as dist
         dist.barrier()
         dist.destroy_process_group()
 

@@ -22,6 +22,10 @@
 #include <dlfcn.h>
 
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
+#include <mutex>
+#include <thread>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -53,12 +57,42 @@ struct Error {
                   std::string(#call) + ": " + cudaGetErrorString(e_)};                   \
   } while (0)
 
+// Device memory comes from the device's stream-ordered pool with an infinite
+// release threshold: repeated sessions (one-shot pg_propagate calls, B&B
+// sessions) reuse it instead of paying cudaMalloc / cudaFree each time.
+thread_local cudaStream_t t_alloc_stream = nullptr;
 template <typename T>
 T* dalloc(size_t count) {
   void* p = nullptr;
   if (count == 0) count = 1;
-  PG_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  PG_CUDA(cudaMallocAsync(&p, count * sizeof(T), t_alloc_stream));
   return static_cast<T*>(p);
+}
+inline void dfree(void* p) {
+  if (p) cudaFreeAsync(p, t_alloc_stream);
+}
+
+// per-device properties, queried once (cudaGetDeviceProperties costs ms)
+struct DevInfo {
+  bool ok = false;
+  int major = 0, minor = 0, sms = 0;
+  std::string name;
+};
+DevInfo device_info(int dev) {
+  static DevInfo cache[64];
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 0 || dev >= 64) return DevInfo{};
+  if (!cache[dev].ok) {
+    cudaDeviceProp prop;
+    PG_CUDA(cudaGetDeviceProperties(&prop, dev));
+    cache[dev] = DevInfo{true, prop.major, prop.minor, prop.multiProcessorCount, prop.name};
+    cudaMemPool_t pool;
+    PG_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t keep = UINT64_MAX;
+    PG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  return cache[dev];
 }
 
 int validate(const pg_config* c) {
@@ -95,6 +129,19 @@ void check_problem(const pg_problem* p) {
   if (p->row_ptr[0] != 0 || p->row_ptr[p->num_rows] != p->nnz)
     throw Error{PG_EINVAL, "row_ptr must start at 0 and end at nnz"};
 }
+
+// PG_TIMING=1: phase times of session setup on stderr (e2e diagnostics)
+struct PhaseTimer {
+  bool on = getenv("PG_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+  void lap(const char* what) {
+    if (!on) return;
+    const auto now = std::chrono::steady_clock::now();
+    fprintf(stderr, "[pg] %-24s %8.3f ms\n", what,
+            std::chrono::duration<double, std::milli>(now - t).count());
+    t = now;
+  }
+};
 
 // NCCL, loaded on first use (the single-GPU engine has no NCCL dependency).
 // Values from nccl.h: ncclInt64 = 4, ncclMax = 2; ncclUniqueId = 128 bytes.
@@ -197,6 +244,7 @@ struct pg_session {
 
   ~pg_session() {
     if (dev >= 0) cudaSetDevice(dev);
+    t_alloc_stream = stream;
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     if (ev0) cudaEventDestroy(ev0);
@@ -205,14 +253,12 @@ struct pg_session {
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream2) cudaStreamDestroy(stream2);
     if (comm) g_nccl.comm_destroy(comm);
-    for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up})
-      if (p) cudaFree(p);
+    for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up}) dfree(p);
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
                     d_lo_res, d_up_res, d_tiles, d_groups, d_segs, d_srow, d_sfirst, d_chunk_seg, d_partial,
                     d_row_act, d_worklist, d_st, d_per_round, d_col_ptr, d_col_item,
                     d_flags, d_chg};
-    for (void* p : ptrs)
-      if (p) cudaFree(p);
+    for (void* p : ptrs) dfree(p);  // stream-ordered: no device sync here
     if (h_st) cudaFreeHost(h_st);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -410,6 +456,24 @@ struct pg_session {
 
 namespace {
 
+int host_threads(int64_t work) {
+  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
+  return (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)hw, 16, work / 65536 + 1}));
+}
+
+template <typename F>
+void parallel_for(int nt, F&& f) {
+  if (nt <= 1) {
+    f(0);
+    return;
+  }
+  std::vector<std::thread> th;
+  th.reserve(nt - 1);
+  for (int t = 1; t < nt; ++t) th.emplace_back(f, t);
+  f(0);
+  for (auto& x : th) x.join();
+}
+
 struct Tables {
   std::vector<TileDesc> tiles;
   std::vector<SegGroup> groups;
@@ -446,8 +510,23 @@ void build_tables(pg_session* s, const int32_t* rp, Tables& T) {
     s->seg_nnz += (int64_t)rp[i + 1] - rp[i];
   }
   T.sfirst.push_back((int32_t)T.segs.size());
-  std::stable_sort(T.segs.begin(), T.segs.end(),
-                   [](const SegDesc& x, const SegDesc& y) { return x.len > y.len; });
+  if (chunk <= (1 << 20)) {
+    // stable counting sort by length, descending
+    std::vector<int64_t> cnt((size_t)chunk + 2, 0);
+    for (const SegDesc& d : T.segs) ++cnt[(size_t)(chunk - d.len)];
+    int64_t run = 0;
+    for (auto& c : cnt) {
+      const int64_t x = c;
+      c = run;
+      run += x;
+    }
+    std::vector<SegDesc> out(T.segs.size());
+    for (const SegDesc& d : T.segs) out[(size_t)cnt[(size_t)(chunk - d.len)]++] = d;
+    T.segs.swap(out);
+  } else {
+    std::stable_sort(T.segs.begin(), T.segs.end(),
+                     [](const SegDesc& x, const SegDesc& y) { return x.len > y.len; });
+  }
   // groups: 8 segments when long (shorter per-group critical path), else 32
   for (size_t q = 0; q < T.segs.size();) {
     const int32_t g = T.segs[q].len > kLongSeg ? 8 : 32;
@@ -463,13 +542,13 @@ void build_tables(pg_session* s, const int32_t* rp, Tables& T) {
 }
 
 pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
+  PhaseTimer tm;
   check_problem(p);
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
     throw Error{PG_ENODEV, "no CUDA device visible (the B200 engine has no CPU fallback)"};
   if (cfg->device < 0 || cfg->device >= ndev) throw Error{PG_EINVAL, "device ordinal out of range"};
-  cudaDeviceProp prop;
-  PG_CUDA(cudaGetDeviceProperties(&prop, cfg->device));
+  const DevInfo prop = device_info(cfg->device);
   if (prop.major != 10)
     throw Error{PG_ENODEV, std::string("device is ") + prop.name + " (sm_" +
                                std::to_string(prop.major * 10 + prop.minor) +
@@ -477,11 +556,12 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
   if (cfg->scalar_mode != PG_WIDE64)
     throw Error{PG_EINVAL, "scalar_mode Narrow32 is not implemented on the GPU engine yet"};
 
+  tm.lap("device query");
   auto* s = new pg_session;
   try {
     s->dev = cfg->device;
     PG_CUDA(cudaSetDevice(s->dev));
-    s->num_sms = prop.multiProcessorCount;
+    s->num_sms = prop.sms;
     PG_CUDA(cudaFuncSetAttribute(k_round<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(SegGroupSmem)));
     PG_CUDA(cudaFuncSetAttribute(k_round<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -503,36 +583,73 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->dcfg.round_limit = cfg->round_limit;
     s->dcfg.flags = cfg->flags;
     PG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    t_alloc_stream = s->stream;
     PG_CUDA(cudaEventCreate(&s->ev0));
     PG_CUDA(cudaStreamCreateWithFlags(&s->stream2, cudaStreamNonBlocking));
     PG_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
     PG_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
     PG_CUDA(cudaEventCreate(&s->ev1));
 
-    // Rows sorted by length (stable counting sort): consecutive rows of a
-    // tile then have near-uniform lengths.  Row order is not observable --
-    // candidates merge by exact max/min and each row is summed on its own.
+    tm.lap("streams/attributes");
+    // The caller's arrays go to the device first (asynchronous from pinned
+    // memory) so the host-side ordering below overlaps the transfer.
+    int32_t* t_rp = dalloc<int32_t>((size_t)p->num_rows + 1);
+    int32_t* t_cols = dalloc<int32_t>(p->nnz);
+    double* t_vals = dalloc<double>(p->nnz);
+    double* t_lhs = dalloc<double>(p->num_rows);
+    double* t_rhs = dalloc<double>(p->num_rows);
+    s->d_integral = dalloc<uint8_t>(p->num_cols);
+    {
+      cudaStream_t st = s->stream;
+      auto h2d = [&](void* dst, const void* src, size_t bytes) {
+        if (bytes) PG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+      };
+      h2d(t_rp, p->row_ptr, sizeof(int32_t) * ((size_t)p->num_rows + 1));
+      h2d(t_cols, p->col_idx, sizeof(int32_t) * p->nnz);
+      h2d(t_vals, p->values, sizeof(double) * p->nnz);
+      h2d(t_lhs, p->lhs, sizeof(double) * p->num_rows);
+      h2d(t_rhs, p->rhs, sizeof(double) * p->num_rows);
+      h2d(s->d_integral, p->integral, p->num_cols);
+    }
+    // Row order: short rows (<= short_max entries) grouped by exact length
+    // (stable counting sort, parallel), longer rows after them in input
+    // order (their segments are sorted by length in build_tables).  Row
+    // order is not observable -- candidates merge by exact max/min and each
+    // row is summed on its own.
     const int32_t m = s->m, n = s->n;
     const int64_t nnz = s->nnz;
+    const int32_t short_max = (int32_t)std::min<int64_t>(cfg->nnz_budget, kShortMax);
+    const int32_t nb = short_max + 2;  // buckets 0..short_max, then "segment rows"
     std::vector<int32_t> perm(m), srp(m + 1);
     {
-      constexpr int32_t kCap = 1 << 16;
-      std::vector<int64_t> cnt(kCap + 2, 0);
-      for (int32_t i = 0; i < m; ++i)
-        ++cnt[std::min<int64_t>((int64_t)p->row_ptr[i + 1] - p->row_ptr[i], kCap) + 1];
-      for (int32_t b = 1; b <= kCap + 1; ++b) cnt[b] += cnt[b - 1];
-      for (int32_t i = 0; i < m; ++i)
-        perm[cnt[std::min<int64_t>((int64_t)p->row_ptr[i + 1] - p->row_ptr[i], kCap)]++] = i;
-      // rows at or beyond the cap: order them by length too
-      const int64_t first_cap = cnt[kCap - 1];
-      std::stable_sort(perm.begin() + first_cap, perm.end(), [&](int32_t x, int32_t y) {
-        return p->row_ptr[x + 1] - p->row_ptr[x] < p->row_ptr[y + 1] - p->row_ptr[y];
+      const int nt = host_threads(m);
+      std::vector<std::vector<int64_t>> hist(nt, std::vector<int64_t>(nb, 0));
+      auto bucket = [&](int32_t i) {
+        const int64_t L = (int64_t)p->row_ptr[i + 1] - p->row_ptr[i];
+        return L <= short_max ? (int32_t)L : short_max + 1;
+      };
+      parallel_for(nt, [&](int t) {
+        const int32_t b = (int32_t)((int64_t)m * t / nt), e = (int32_t)((int64_t)m * (t + 1) / nt);
+        for (int32_t i = b; i < e; ++i) ++hist[t][bucket(i)];
+      });
+      int64_t run = 0;
+      for (int32_t k = 0; k < nb; ++k)
+        for (int t = 0; t < nt; ++t) {
+          const int64_t c = hist[t][k];
+          hist[t][k] = run;
+          run += c;
+        }
+      parallel_for(nt, [&](int t) {
+        const int32_t b = (int32_t)((int64_t)m * t / nt), e = (int32_t)((int64_t)m * (t + 1) / nt);
+        for (int32_t i = b; i < e; ++i) perm[hist[t][bucket(i)]++] = i;
       });
       srp[0] = 0;
       for (int32_t i = 0; i < m; ++i) srp[i + 1] = srp[i] + (p->row_ptr[perm[i] + 1] - p->row_ptr[perm[i]]);
     }
+    tm.lap("row sort (host)");
     Tables T;
     build_tables(s, srp.data(), T);
+    tm.lap("tables (host)");
     s->num_tiles = (int32_t)T.tiles.size();
     s->nseg = (int32_t)T.segs.size();
     s->nsrow = (int32_t)T.srow.size();
@@ -544,7 +661,6 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->d_lhs = dalloc<double>((size_t)m + 2);
     s->d_rhs = dalloc<double>((size_t)m + 2);
     s->d_snap = dalloc<Snap>(n);
-    s->d_integral = dalloc<uint8_t>(n);
     s->d_key_out = dalloc<longlong2>((size_t)n + 1);  // + infeasibility slot
     s->d_lo0 = dalloc<double>(n);
     s->d_up0 = dalloc<double>(n);
@@ -566,12 +682,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->d_per_round = dalloc<long long>(cfg->round_limit);
     PG_CUDA(cudaMallocHost(&s->h_st, sizeof(DevState)));
 
-    // staging copies of the caller's arrays (original row order)
-    int32_t* t_rp = dalloc<int32_t>(m + 1);
-    int32_t* t_cols = dalloc<int32_t>(nnz);
-    double* t_vals = dalloc<double>(nnz);
-    double* t_lhs = dalloc<double>(m);
-    double* t_rhs = dalloc<double>(m);
+    tm.lap("allocations");
     int32_t* t_perm = dalloc<int32_t>(m);
     uint8_t* d_integral = s->d_integral;
 
@@ -580,19 +691,9 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     PG_CUDA(cudaMemsetAsync(s->d_row_done, 0, sizeof(int32_t) * std::max<size_t>(1, T.srow.size()), st));
     PG_CUDA(cudaMemsetAsync(s->d_colx, 0, sizeof(int32_t) * (nnz + 4), st));
     PG_CUDA(cudaMemsetAsync(s->d_vals, 0, sizeof(double) * (nnz + 2), st));
-    PG_CUDA(cudaMemcpyAsync(t_rp, p->row_ptr, sizeof(int32_t) * (m + 1), cudaMemcpyHostToDevice, st));
     PG_CUDA(cudaMemcpyAsync(s->d_row_ptr, srp.data(), sizeof(int32_t) * (m + 1),
                             cudaMemcpyHostToDevice, st));
     if (m) PG_CUDA(cudaMemcpyAsync(t_perm, perm.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
-    if (nnz) {
-      PG_CUDA(cudaMemcpyAsync(t_cols, p->col_idx, sizeof(int32_t) * nnz, cudaMemcpyHostToDevice, st));
-      PG_CUDA(cudaMemcpyAsync(t_vals, p->values, sizeof(double) * nnz, cudaMemcpyHostToDevice, st));
-    }
-    if (m) {
-      PG_CUDA(cudaMemcpyAsync(t_lhs, p->lhs, sizeof(double) * m, cudaMemcpyHostToDevice, st));
-      PG_CUDA(cudaMemcpyAsync(t_rhs, p->rhs, sizeof(double) * m, cudaMemcpyHostToDevice, st));
-    }
-    if (n) PG_CUDA(cudaMemcpyAsync(d_integral, p->integral, n, cudaMemcpyHostToDevice, st));
     if (m) {
       k_permute_rows<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
           t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, d_integral, s->d_colx,
@@ -608,6 +709,8 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     up(s->d_srow, T.srow.data(), sizeof(int32_t) * T.srow.size());
     up(s->d_sfirst, T.sfirst.data(), sizeof(int32_t) * T.sfirst.size());
     up(s->d_chunk_seg, T.chunk_seg.data(), sizeof(int32_t) * T.chunk_seg.size());
+    PG_CUDA(cudaStreamSynchronize(st));
+    tm.lap("H2D + permute");
     // worklist index: column -> work items (device counting sort by column)
     {
       Dirty& D = s->dirty;
@@ -637,8 +740,8 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
             s->d_row_ptr, s->d_colx, m, cnt, s->d_col_item);
         PG_CUDA(cudaGetLastError());
         PG_CUDA(cudaStreamSynchronize(st));
-        cudaFree(tmp);
-        cudaFree(cnt);
+        dfree(tmp);
+        dfree(cnt);
         D.col_ptr = s->d_col_ptr;
         D.col_row = s->d_col_item;
       }
@@ -648,8 +751,10 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     PG_CUDA(cudaStreamSynchronize(st));
     for (void* q : {(void*)t_rp, (void*)t_cols, (void*)t_vals, (void*)t_lhs, (void*)t_rhs,
                     (void*)t_perm})
-      cudaFree(q);
+      dfree(q);
+    tm.lap("worklist/bounds/free");
     if (cfg->loop_mode == PG_LOOP_GRAPH) s->build_graph();
+    tm.lap("graph instantiate");
     return s;
   } catch (...) {
     delete s;
@@ -754,8 +859,11 @@ int pg_propagate(const pg_problem* p, const pg_config* cfg, pg_result* res) {
   pg_session* s = nullptr;
   int rc = pg_session_create(p, cfg, &s);
   if (rc) return rc;
+  PhaseTimer tm;
   rc = pg_session_run(s, res);
+  tm.lap("solve + download");
   pg_session_destroy(s);
+  tm.lap("destroy");
   return rc;
 }
 
@@ -867,6 +975,7 @@ int pg_session_set_root(pg_session* s, pg_result* res) {
     s->fill_result(res, ns);
     s->has_root = res->status == PG_CONVERGED;
     if (s->has_root) {
+      t_alloc_stream = s->stream;
       if (!s->d_root_lo) {
         s->d_root_lo = dalloc<double>(s->n);
         s->d_root_up = dalloc<double>(s->n);
@@ -894,6 +1003,7 @@ int pg_session_propagate_nodes(pg_session* s, int32_t K, const int32_t* node_ptr
   }
   return guarded([&] {
     PG_CUDA(cudaSetDevice(s->dev));
+    t_alloc_stream = s->stream;
     const int32_t total = node_ptr[K];
     for (int32_t k = 0; k < K; ++k)
       if (node_ptr[k + 1] < node_ptr[k]) throw Error{PG_EINVAL, "node_ptr must be nondecreasing"};
@@ -962,7 +1072,8 @@ int pg_session_propagate_nodes(pg_session* s, int32_t K, const int32_t* node_ptr
       status[k] = out[k].x < 0 ? PG_ROUNDLIMIT : out[k].x;
       rounds[k] = out[k].y;
     }
-    for (void* p : {(void*)d_vars, (void*)d_lo, (void*)d_up, (void*)d_ctls, (void*)d_out}) cudaFree(p);
+    t_alloc_stream = st;
+    for (void* p : {(void*)d_vars, (void*)d_lo, (void*)d_up, (void*)d_ctls, (void*)d_out}) dfree(p);
     return PG_OK;
   });
 }
