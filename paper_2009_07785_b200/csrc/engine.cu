@@ -36,7 +36,10 @@
 #include "../../include/propgate_b200.h"
 #include <cub/device/device_scan.cuh>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "kernels.cuh"
+#include "setup.cuh"
 
 using namespace pgb;
 
@@ -456,91 +459,6 @@ struct pg_session {
 
 namespace {
 
-int host_threads(int64_t work) {
-  const int hw = (int)std::max(1u, std::thread::hardware_concurrency());
-  return (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)hw, 16, work / 65536 + 1}));
-}
-
-template <typename F>
-void parallel_for(int nt, F&& f) {
-  if (nt <= 1) {
-    f(0);
-    return;
-  }
-  std::vector<std::thread> th;
-  th.reserve(nt - 1);
-  for (int t = 1; t < nt; ++t) th.emplace_back(f, t);
-  f(0);
-  for (auto& x : th) x.join();
-}
-
-struct Tables {
-  std::vector<TileDesc> tiles;
-  std::vector<SegGroup> groups;
-  std::vector<SegDesc> segs;
-  std::vector<int32_t> srow, sfirst, chunk_seg, seg_group;
-};
-
-// Tables over the length-sorted rows: warp tiles of short rows, segments of
-// long rows (chunks of nnz_budget, as wide_row_activities), the latter
-// sorted by length so that a warp's 32 segments have near-equal work.
-void build_tables(pg_session* s, const int32_t* rp, Tables& T) {
-  const int64_t chunk = s->cfg.nnz_budget;
-  const int64_t short_max = std::min<int64_t>(chunk, kShortMax);
-  const int32_t m = s->m;
-  int32_t i = 0;
-  // warp tiles: consecutive rows of one length L (rows are length-sorted)
-  while (i < m && (int64_t)rp[i + 1] - rp[i] <= short_max) {
-    const int32_t start = i;
-    const int64_t L = (int64_t)rp[i + 1] - rp[i];
-    const int32_t cap = L ? (int32_t)std::min<int64_t>(32, kWNnz / L) : 32;
-    while (i < m && i - start < cap && (int64_t)rp[i + 1] - rp[i] == L) ++i;
-    T.tiles.push_back({start, i - start, rp[start], (int32_t)(L * (i - start))});
-    s->tile_rows += i - start;
-    s->tile_nnz += L * (i - start);
-  }
-  for (; i < m; ++i) {
-    const int32_t slot = (int32_t)T.srow.size();
-    T.srow.push_back(i);
-    T.sfirst.push_back((int32_t)T.segs.size());
-    for (int64_t k = rp[i]; k < rp[i + 1]; k += chunk) {
-      const int32_t len = (int32_t)std::min<int64_t>(chunk, rp[i + 1] - k);
-      T.segs.push_back({(int32_t)k, len, (int32_t)T.segs.size(), slot});
-    }
-    s->seg_nnz += (int64_t)rp[i + 1] - rp[i];
-  }
-  T.sfirst.push_back((int32_t)T.segs.size());
-  if (chunk <= (1 << 20)) {
-    // stable counting sort by length, descending
-    std::vector<int64_t> cnt((size_t)chunk + 2, 0);
-    for (const SegDesc& d : T.segs) ++cnt[(size_t)(chunk - d.len)];
-    int64_t run = 0;
-    for (auto& c : cnt) {
-      const int64_t x = c;
-      c = run;
-      run += x;
-    }
-    std::vector<SegDesc> out(T.segs.size());
-    for (const SegDesc& d : T.segs) out[(size_t)cnt[(size_t)(chunk - d.len)]++] = d;
-    T.segs.swap(out);
-  } else {
-    std::stable_sort(T.segs.begin(), T.segs.end(),
-                     [](const SegDesc& x, const SegDesc& y) { return x.len > y.len; });
-  }
-  // groups: 8 segments when long (shorter per-group critical path), else 32
-  for (size_t q = 0; q < T.segs.size();) {
-    const int32_t g = T.segs[q].len > kLongSeg ? 8 : 32;
-    const int32_t cnt = (int32_t)std::min<size_t>(g, T.segs.size() - q);
-    T.groups.push_back({(int32_t)q, cnt});
-    q += cnt;
-  }
-  T.chunk_seg.assign(T.segs.size(), 0);
-  for (size_t q = 0; q < T.segs.size(); ++q) T.chunk_seg[T.segs[q].out] = (int32_t)q;
-  T.seg_group.assign(T.segs.size(), 0);
-  for (size_t g = 0; g < T.groups.size(); ++g)
-    for (int32_t q = 0; q < T.groups[g].count; ++q) T.seg_group[T.groups[g].first + q] = (int32_t)g;
-}
-
 pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
   PhaseTimer tm;
   check_problem(p);
@@ -591,71 +509,148 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     PG_CUDA(cudaEventCreate(&s->ev1));
 
     tm.lap("streams/attributes");
-    // The caller's arrays go to the device first (asynchronous from pinned
-    // memory) so the host-side ordering below overlaps the transfer.
-    int32_t* t_rp = dalloc<int32_t>((size_t)p->num_rows + 1);
-    int32_t* t_cols = dalloc<int32_t>(p->nnz);
-    double* t_vals = dalloc<double>(p->nnz);
-    double* t_lhs = dalloc<double>(p->num_rows);
-    double* t_rhs = dalloc<double>(p->num_rows);
-    s->d_integral = dalloc<uint8_t>(p->num_cols);
-    {
-      cudaStream_t st = s->stream;
-      auto h2d = [&](void* dst, const void* src, size_t bytes) {
-        if (bytes) PG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
-      };
-      h2d(t_rp, p->row_ptr, sizeof(int32_t) * ((size_t)p->num_rows + 1));
-      h2d(t_cols, p->col_idx, sizeof(int32_t) * p->nnz);
-      h2d(t_vals, p->values, sizeof(double) * p->nnz);
-      h2d(t_lhs, p->lhs, sizeof(double) * p->num_rows);
-      h2d(t_rhs, p->rhs, sizeof(double) * p->num_rows);
-      h2d(s->d_integral, p->integral, p->num_cols);
-    }
-    // Row order: short rows (<= short_max entries) grouped by exact length
-    // (stable counting sort, parallel), longer rows after them in input
-    // order (their segments are sorted by length in build_tables).  Row
-    // order is not observable -- candidates merge by exact max/min and each
-    // row is summed on its own.
     const int32_t m = s->m, n = s->n;
     const int64_t nnz = s->nnz;
     const int32_t short_max = (int32_t)std::min<int64_t>(cfg->nnz_budget, kShortMax);
-    const int32_t nb = short_max + 2;  // buckets 0..short_max, then "segment rows"
-    std::vector<int32_t> perm(m), srp(m + 1);
-    {
-      const int nt = host_threads(m);
-      std::vector<std::vector<int64_t>> hist(nt, std::vector<int64_t>(nb, 0));
-      auto bucket = [&](int32_t i) {
-        const int64_t L = (int64_t)p->row_ptr[i + 1] - p->row_ptr[i];
-        return L <= short_max ? (int32_t)L : short_max + 1;
-      };
-      parallel_for(nt, [&](int t) {
-        const int32_t b = (int32_t)((int64_t)m * t / nt), e = (int32_t)((int64_t)m * (t + 1) / nt);
-        for (int32_t i = b; i < e; ++i) ++hist[t][bucket(i)];
-      });
-      int64_t run = 0;
-      for (int32_t k = 0; k < nb; ++k)
-        for (int t = 0; t < nt; ++t) {
-          const int64_t c = hist[t][k];
-          hist[t][k] = run;
-          run += c;
-        }
-      parallel_for(nt, [&](int t) {
-        const int32_t b = (int32_t)((int64_t)m * t / nt), e = (int32_t)((int64_t)m * (t + 1) / nt);
-        for (int32_t i = b; i < e; ++i) perm[hist[t][bucket(i)]++] = i;
-      });
-      srp[0] = 0;
-      for (int32_t i = 0; i < m; ++i) srp[i + 1] = srp[i] + (p->row_ptr[perm[i] + 1] - p->row_ptr[perm[i]]);
-    }
-    tm.lap("row sort (host)");
-    Tables T;
-    build_tables(s, srp.data(), T);
-    tm.lap("tables (host)");
-    s->num_tiles = (int32_t)T.tiles.size();
-    s->nseg = (int32_t)T.segs.size();
-    s->nsrow = (int32_t)T.srow.size();
-    s->ngroups = (int32_t)T.groups.size();
+    const int32_t chunk = cfg->nnz_budget;
+    const int32_t nb = short_max + 2;  // length classes 0..short_max, then segment rows
+    cudaStream_t st = s->stream, s2 = s->stream2;
 
+    // buffers: the caller's arrays staged in input row order, the ordering work
+    int32_t* t_rp = dalloc<int32_t>((size_t)m + 1);
+    int32_t* t_cols = dalloc<int32_t>(nnz);
+    double* t_vals = dalloc<double>(nnz);
+    double* t_lhs = dalloc<double>(m);
+    double* t_rhs = dalloc<double>(m);
+    s->d_integral = dalloc<uint8_t>(n);
     s->d_row_ptr = dalloc<int32_t>((size_t)m + 1 + 4);  // +16 B: bulk-copy tail
+    uint8_t* key = dalloc<uint8_t>(m);
+    uint8_t* key2 = dalloc<uint8_t>(m);
+    int32_t* idx = dalloc<int32_t>(m);
+    int32_t* t_perm = dalloc<int32_t>(m);
+    int32_t* slen = dalloc<int32_t>((size_t)m + 1);
+    int32_t* counts = dalloc<int32_t>(kMaxClasses + 4);
+    PG_CUDA(cudaEventRecord(s->ev_fork, st));
+    PG_CUDA(cudaStreamWaitEvent(s2, s->ev_fork, 0));
+    // stream 1: the bulk of the upload (asynchronous from pinned memory)
+    auto h2d = [&](void* dst, const void* src, size_t bytes, cudaStream_t q) {
+      if (bytes) PG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, q));
+    };
+    h2d(t_cols, p->col_idx, sizeof(int32_t) * nnz, st);
+    h2d(t_vals, p->values, sizeof(double) * nnz, st);
+    h2d(t_lhs, p->lhs, sizeof(double) * m, st);
+    h2d(t_rhs, p->rhs, sizeof(double) * m, st);
+    h2d(s->d_integral, p->integral, n, st);
+
+    // stream 2, concurrently: row order.  Short rows (<= short_max entries)
+    // grouped by exact length (stable radix sort), then the rows split into
+    // segments in input order.  Row order is not observable -- candidates
+    // merge by exact max/min and each row is summed on its own.
+    h2d(t_rp, p->row_ptr, sizeof(int32_t) * ((size_t)m + 1), s2);
+    void* tmp = nullptr;
+    size_t tmp_bytes = 0;
+    auto cub_tmp = [&](size_t need) {
+      if (need > tmp_bytes) {
+        t_alloc_stream = s2;
+        dfree(tmp);
+        tmp = dalloc<unsigned char>(need);
+        tmp_bytes = need;
+        t_alloc_stream = st;
+      }
+    };
+    std::vector<int32_t> cls(kMaxClasses + 4, 0);
+    if (m) {
+      k_row_keys<<<s->grid_for(m, 256), 256, 0, s2>>>(t_rp, m, short_max, key, idx);
+      size_t need = 0;
+      PG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, idx, t_perm, m, 0, 5, s2));
+      cub_tmp(need);
+      PG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, key, key2, idx, t_perm, m, 0, 5, s2));
+      k_sorted_len<<<s->grid_for((int64_t)m + 1, 256), 256, 0, s2>>>(t_rp, t_perm, m, slen);
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, slen, s->d_row_ptr, m + 1, s2));
+      cub_tmp(need);
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, slen, s->d_row_ptr, m + 1, s2));
+      PG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (kMaxClasses + 4), s2));
+      k_class_counts<<<s->grid_for(m, 256), 256, 0, s2>>>(key2, m, counts);
+      PG_CUDA(cudaMemcpyAsync(cls.data(), counts, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s2));
+      PG_CUDA(cudaStreamSynchronize(s2));
+    }
+    TileLayout lay{};
+    lay.nclass = short_max + 1;
+    {
+      int32_t row = 0, tiles = 0;
+      for (int32_t L = 0; L <= short_max; ++L) {
+        lay.class_start[L] = row;
+        lay.tile_off[L] = tiles;
+        const int32_t cap = L ? std::min(32, kWNnz / L) : 32;
+        tiles += (cls[L] + cap - 1) / cap;
+        row += cls[L];
+      }
+      lay.class_start[short_max + 1] = row;
+      lay.tile_off[short_max + 1] = tiles;
+      s->num_tiles = tiles;
+      s->tile_rows = row;
+      s->nsrow = m - row;
+    }
+    s->d_tiles = dalloc<TileDesc>(s->num_tiles);
+    s->d_srow = dalloc<int32_t>(s->nsrow);
+    s->d_sfirst = dalloc<int32_t>((size_t)s->nsrow + 1);
+    int32_t* scnt = dalloc<int32_t>((size_t)s->nsrow + 1);
+    PG_CUDA(cudaEventRecord(s->ev_join, st));
+    PG_CUDA(cudaStreamWaitEvent(s2, s->ev_join, 0));  // allocations above happen on stream 1
+    if (s->num_tiles)
+      k_make_tiles<<<s->grid_for(s->num_tiles, 256), 256, 0, s2>>>(lay, s->d_row_ptr, s->d_tiles);
+    int32_t h_nseg = 0, h_nlong = 0;
+    if (s->nsrow) {
+      k_seg_counts<<<s->grid_for((int64_t)s->nsrow + 1, 256), 256, 0, s2>>>(
+          s->d_row_ptr, (int)s->tile_rows, s->nsrow, chunk, scnt, s->d_srow);
+      size_t need = 0;
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, scnt, s->d_sfirst, s->nsrow + 1, s2));
+      cub_tmp(need);
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, scnt, s->d_sfirst, s->nsrow + 1, s2));
+      PG_CUDA(cudaMemcpyAsync(&h_nseg, s->d_sfirst + s->nsrow, sizeof(int32_t), cudaMemcpyDeviceToHost, s2));
+      PG_CUDA(cudaStreamSynchronize(s2));
+    }
+    s->nseg = h_nseg;
+    for (int32_t L = 0; L <= short_max; ++L) s->tile_nnz += (int64_t)L * cls[L];
+    s->seg_nnz = nnz - s->tile_nnz;
+    s->d_segs = dalloc<SegDesc>(s->nseg);
+    s->d_chunk_seg = dalloc<int32_t>(s->nseg);
+    SegDesc* segs_in = dalloc<SegDesc>(s->nseg);
+    uint32_t* skey = dalloc<uint32_t>(s->nseg);
+    uint32_t* skey2 = dalloc<uint32_t>(s->nseg);
+    int32_t* sidx = dalloc<int32_t>(s->nseg);
+    int32_t* sorder = dalloc<int32_t>(s->nseg);
+    int32_t* d_nlong = dalloc<int32_t>(1);
+    PG_CUDA(cudaMemsetAsync(d_nlong, 0, sizeof(int32_t), st));
+    PG_CUDA(cudaEventRecord(s->ev_join, st));
+    PG_CUDA(cudaStreamWaitEvent(s2, s->ev_join, 0));
+    if (s->nseg) {
+      k_emit_segs<<<s->grid_for((int64_t)s->nsrow * 32, 256, 16), 256, 0, s2>>>(
+          s->d_row_ptr, s->d_sfirst, (int)s->tile_rows, s->nsrow, chunk, segs_in, skey, sidx);
+      int bits = 1;
+      while (bits < 32 && (1u << bits) <= (uint32_t)chunk) ++bits;
+      size_t need = 0;
+      PG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, skey, skey2, sidx, sorder, s->nseg, 0,
+                                              bits, s2));
+      cub_tmp(need);
+      PG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, skey, skey2, sidx, sorder, s->nseg, 0,
+                                              bits, s2));
+      k_order_segs<<<s->grid_for(s->nseg, 256), 256, 0, s2>>>(segs_in, sorder, s->nseg, s->d_segs,
+                                                              s->d_chunk_seg, d_nlong);
+      PG_CUDA(cudaMemcpyAsync(&h_nlong, d_nlong, sizeof(int32_t), cudaMemcpyDeviceToHost, s2));
+      PG_CUDA(cudaStreamSynchronize(s2));
+    }
+    const int32_t n8 = (h_nlong + 7) / 8;
+    s->ngroups = s->nseg ? n8 + std::max(0, (s->nseg - 8 * n8 + 31) / 32) : 0;
+    s->d_groups = dalloc<SegGroup>(s->ngroups);
+    PG_CUDA(cudaEventRecord(s->ev_join, st));
+    PG_CUDA(cudaStreamWaitEvent(s2, s->ev_join, 0));
+    if (s->ngroups)
+      k_make_groups<<<s->grid_for(s->ngroups, 256), 256, 0, s2>>>(s->nseg, n8, s->ngroups,
+                                                                  s->d_groups);
+    PG_CUDA(cudaGetLastError());
+    tm.lap("ordering + tables (dev)");
+
     s->d_colx = dalloc<int32_t>(nnz + 4);  // +16 B: bulk copies round up to 16 B
     s->d_vals = dalloc<double>(nnz + 2);
     s->d_lhs = dalloc<double>((size_t)m + 2);
@@ -666,49 +661,34 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->d_up0 = dalloc<double>(n);
     s->d_lo_res = dalloc<double>(n);
     s->d_up_res = dalloc<double>(n);
-    s->d_tiles = dalloc<TileDesc>(T.tiles.size());
-    s->d_groups = dalloc<SegGroup>(T.groups.size());
-    s->d_segs = dalloc<SegDesc>(T.segs.size());
-    s->d_srow = dalloc<int32_t>(T.srow.size());
-    s->d_sfirst = dalloc<int32_t>(T.sfirst.size());
-    s->d_chunk_seg = dalloc<int32_t>(T.chunk_seg.size());
-    s->d_partial = dalloc<SegPartial>(T.segs.size());
-    s->d_row_act = dalloc<Act>(T.srow.size());
-    s->d_worklist = dalloc<int32_t>(T.segs.size());
-    s->d_row_done = dalloc<int32_t>(T.srow.size());
+    s->d_partial = dalloc<SegPartial>(s->nseg);
+    s->d_row_act = dalloc<Act>(s->nsrow);
+    s->d_worklist = dalloc<int32_t>(s->nseg);
+    s->d_row_done = dalloc<int32_t>(s->nsrow);
     s->d_st = dalloc<DevState>(1);
     s->d_ctl = dalloc<NodeCtl>(1);
-    PG_CUDA(cudaMemset(s->d_ctl, 0, sizeof(NodeCtl)));  // cold starts
     s->d_per_round = dalloc<long long>(cfg->round_limit);
     PG_CUDA(cudaMallocHost(&s->h_st, sizeof(DevState)));
-
-    tm.lap("allocations");
-    int32_t* t_perm = dalloc<int32_t>(m);
-    uint8_t* d_integral = s->d_integral;
-
-    cudaStream_t st = s->stream;
+    PG_CUDA(cudaMemsetAsync(s->d_ctl, 0, sizeof(NodeCtl), st));  // cold starts
     PG_CUDA(cudaMemsetAsync(s->d_st, 0, sizeof(DevState), st));
-    PG_CUDA(cudaMemsetAsync(s->d_row_done, 0, sizeof(int32_t) * std::max<size_t>(1, T.srow.size()), st));
+    PG_CUDA(cudaMemsetAsync(s->d_row_done, 0, sizeof(int32_t) * std::max<int32_t>(1, s->nsrow), st));
     PG_CUDA(cudaMemsetAsync(s->d_colx, 0, sizeof(int32_t) * (nnz + 4), st));
     PG_CUDA(cudaMemsetAsync(s->d_vals, 0, sizeof(double) * (nnz + 2), st));
-    PG_CUDA(cudaMemcpyAsync(s->d_row_ptr, srp.data(), sizeof(int32_t) * (m + 1),
-                            cudaMemcpyHostToDevice, st));
-    if (m) PG_CUDA(cudaMemcpyAsync(t_perm, perm.data(), sizeof(int32_t) * m, cudaMemcpyHostToDevice, st));
+    // the ordering (stream 2) must be complete before the permutation
+    PG_CUDA(cudaEventRecord(s->ev_join, s2));
+    PG_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
     if (m) {
       k_permute_rows<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
-          t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, d_integral, s->d_colx,
+          t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, s->d_integral, s->d_colx,
           s->d_vals, s->d_lhs, s->d_rhs, m, cfg->infinity_threshold);
       PG_CUDA(cudaGetLastError());
     }
-    auto up = [&](void* dst, const void* src, size_t bytes) {
-      if (bytes) PG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
-    };
-    up(s->d_tiles, T.tiles.data(), sizeof(TileDesc) * T.tiles.size());
-    up(s->d_groups, T.groups.data(), sizeof(SegGroup) * T.groups.size());
-    up(s->d_segs, T.segs.data(), sizeof(SegDesc) * T.segs.size());
-    up(s->d_srow, T.srow.data(), sizeof(int32_t) * T.srow.size());
-    up(s->d_sfirst, T.sfirst.data(), sizeof(int32_t) * T.sfirst.size());
-    up(s->d_chunk_seg, T.chunk_seg.data(), sizeof(int32_t) * T.chunk_seg.size());
+    uint8_t* d_integral = s->d_integral;
+    (void)d_integral;
+    for (void* q : {(void*)key, (void*)key2, (void*)idx, (void*)slen, (void*)counts, (void*)scnt,
+                    (void*)segs_in, (void*)skey, (void*)skey2, (void*)sidx, (void*)sorder,
+                    (void*)d_nlong, tmp})
+      dfree(q);
     PG_CUDA(cudaStreamSynchronize(st));
     tm.lap("H2D + permute");
     // worklist index: column -> work items (device counting sort by column)

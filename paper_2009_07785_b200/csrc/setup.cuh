@@ -1,0 +1,123 @@
+// setup.cuh -- device-side session setup (row order, tiles, segments).
+//
+// Untimed in the reference's protocol (its initialisation -- partition,
+// working copies, pool -- is excluded from `elapsed`), but part of the
+// end-to-end call: doing it on the device keeps pg_propagate close to its
+// upload + solve + download cost.
+#pragma once
+
+#include "kernels.cuh"
+
+namespace pgb {
+
+// length class of every row: exact length for short rows, one class for the
+// rows that are split into segments; plus the identity permutation
+__global__ void k_row_keys(const int32_t* __restrict__ rp, int m, int short_max,
+                           uint8_t* __restrict__ key, int32_t* __restrict__ idx) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int L = rp[i + 1] - rp[i];
+    key[i] = (uint8_t)(L <= short_max ? L : short_max + 1);
+    idx[i] = i;
+  }
+}
+
+// lengths in the new order (the exclusive scan gives the permuted row_ptr)
+__global__ void k_sorted_len(const int32_t* __restrict__ rp, const int32_t* __restrict__ perm,
+                             int m, int32_t* __restrict__ slen) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= m; i += gridDim.x * blockDim.x)
+    slen[i] = i < m ? rp[perm[i] + 1] - rp[perm[i]] : 0;
+}
+
+constexpr int kMaxClasses = kShortMax + 2;
+struct TileLayout {
+  int32_t nclass;                   // short_max + 1 length classes 0..short_max
+  int32_t class_start[kMaxClasses];  // first sorted row of class L
+  int32_t tile_off[kMaxClasses];     // first tile of class L (+ total at nclass)
+};
+
+__device__ __forceinline__ int tile_cap(int L) { return L ? min(32, kWNnz / L) : 32; }
+
+// rows per length class
+__global__ void k_class_counts(const uint8_t* __restrict__ key, int m, int32_t* __restrict__ counts) {
+  __shared__ int32_t h[kMaxClasses];
+  for (int c = threadIdx.x; c < kMaxClasses; c += blockDim.x) h[c] = 0;
+  __syncthreads();
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    atomicAdd(&h[key[i]], 1);
+  __syncthreads();
+  for (int c = threadIdx.x; c < kMaxClasses; c += blockDim.x)
+    if (h[c]) atomicAdd(&counts[c], h[c]);
+}
+
+// warp tiles: class L's rows in runs of tile_cap(L) consecutive rows
+__global__ void k_make_tiles(const TileLayout lay, const int32_t* __restrict__ srp,
+                             TileDesc* __restrict__ tiles) {
+  const int total = lay.tile_off[lay.nclass];
+  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+    int L = 0;
+    while (L + 1 < lay.nclass && lay.tile_off[L + 1] <= t) ++L;
+    const int cap = tile_cap(L);
+    const int r0 = lay.class_start[L] + (t - lay.tile_off[L]) * cap;
+    const int end = lay.class_start[L + 1];
+    const int nr = min(cap, end - r0);
+    tiles[t] = TileDesc{r0, nr, srp[r0], nr * L};
+  }
+}
+
+// chunks per segment row (rows [first, m) of the sorted order)
+__global__ void k_seg_counts(const int32_t* __restrict__ srp, int first, int nsrow, int chunk,
+                             int32_t* __restrict__ cnt, int32_t* __restrict__ srow) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s <= nsrow; s += gridDim.x * blockDim.x) {
+    if (s < nsrow) {
+      const int i = first + s;
+      const int L = srp[i + 1] - srp[i];
+      cnt[s] = (L + chunk - 1) / chunk;
+      srow[s] = i;
+    } else {
+      cnt[s] = 0;
+    }
+  }
+}
+
+// one descriptor per chunk, in chunk order (out = partial index), plus the
+// descending-length sort key
+__global__ void k_emit_segs(const int32_t* __restrict__ srp, const int32_t* __restrict__ sfirst,
+                            int first, int nsrow, int chunk, SegDesc* __restrict__ segs,
+                            uint32_t* __restrict__ key, int32_t* __restrict__ idx) {
+  const int lane = threadIdx.x & 31;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nsrow;
+       s += (gridDim.x * blockDim.x) >> 5) {
+    const int i = first + s, k0 = srp[i], k1 = srp[i + 1];
+    const int q0 = sfirst[s], nq = sfirst[s + 1] - q0;
+    for (int c = lane; c < nq; c += 32) {
+      const int a = k0 + c * chunk;
+      const int len = min(chunk, k1 - a);
+      segs[q0 + c] = SegDesc{a, len, q0 + c, s};
+      key[q0 + c] = (uint32_t)(chunk - len);
+      idx[q0 + c] = q0 + c;
+    }
+  }
+}
+
+// segments into descending-length order; chunk -> sorted position
+__global__ void k_order_segs(const SegDesc* __restrict__ in, const int32_t* __restrict__ order,
+                             int nseg, SegDesc* __restrict__ out, int32_t* __restrict__ chunk_seg,
+                             int32_t* __restrict__ nlong) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nseg; q += gridDim.x * blockDim.x) {
+    const SegDesc d = in[order[q]];
+    out[q] = d;
+    chunk_seg[d.out] = q;
+    if (d.len > kLongSeg && (q + 1 == nseg || in[order[q + 1]].len <= kLongSeg)) *nlong = q + 1;
+  }
+}
+
+// groups: 8 segments while they are long (short per-group critical path),
+// then 32
+__global__ void k_make_groups(int nseg, int n8, int ngroups, SegGroup* __restrict__ groups) {
+  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
+    const int first = g < n8 ? 8 * g : 8 * n8 + 32 * (g - n8);
+    groups[g] = SegGroup{first, min(g < n8 ? 8 : 32, nseg - first)};
+  }
+}
+
+}  // namespace pgb
