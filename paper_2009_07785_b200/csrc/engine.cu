@@ -193,6 +193,7 @@ struct pg_session {
   pg_config cfg{};
   DevCfg dcfg{};
   int num_sms = 148;
+  int tiles_per_sm = 1;  // resident k_tiles CTAs per SM (occupancy)
 
   // device arrays
   int32_t* d_row_ptr = nullptr;
@@ -319,11 +320,12 @@ struct pg_session {
         k_round<false><<<grid, kRoundThreads, sizeof(SegGroupSmem), sg>>>(A, dcfg);
     }
     if (num_tiles > 0 && !(cfg.flags & 0x200u)) {
-      const int grid = std::max(1, std::min((num_tiles + kTWarps - 1) / kTWarps, num_sms * 3));
+      // all resident CTAs, each a producer warp + consumer warps over a tile ring
+      const int grid = std::max(1, std::min((num_tiles + 7) / 8, num_sms * tiles_per_sm));
       if (rowcheck)
-        k_tiles<true><<<grid, kTWarps * 32, sizeof(TileWarpSmem) * kTWarps, stream>>>(A, dcfg);
+        k_tiles<true><<<grid, kWsWarps * 32, sizeof(TilesSmem), stream>>>(A, dcfg);
       else
-        k_tiles<false><<<grid, kTWarps * 32, sizeof(TileWarpSmem) * kTWarps, stream>>>(A, dcfg);
+        k_tiles<false><<<grid, kWsWarps * 32, sizeof(TilesSmem), stream>>>(A, dcfg);
     }
     if (ngroups > 0 && num_tiles > 0) {
       PG_CUDA(cudaEventRecord(ev_join, stream2));
@@ -485,9 +487,12 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     PG_CUDA(cudaFuncSetAttribute(k_round<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sizeof(SegGroupSmem)));
     PG_CUDA(cudaFuncSetAttribute(k_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(TileWarpSmem) * kTWarps)));
+                                 (int)sizeof(TilesSmem)));
     PG_CUDA(cudaFuncSetAttribute(k_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(sizeof(TileWarpSmem) * kTWarps)));
+                                 (int)sizeof(TilesSmem)));
+    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->tiles_per_sm, k_tiles<true>,
+                                                          kWsWarps * 32, sizeof(TilesSmem)));
+    s->tiles_per_sm = std::max(1, s->tiles_per_sm);
 
     s->m = p->num_rows;
     s->n = p->num_cols;

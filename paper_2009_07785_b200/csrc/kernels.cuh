@@ -471,8 +471,6 @@ __device__ __forceinline__ int popc_range(const unsigned (&m)[kWItems], int b, i
 //   tile i:   compute (one lane per row, sums in entry order)
 // Neither stage holds registers, so a warp keeps ~256 gathers in flight with
 // no CTA barrier.  Rows are stored sorted by length (session init).
-constexpr int kTWarps = 4;
-constexpr int kTStages = 3;
 
 struct __align__(16) TileStage {
   double vals[kWNnz + 2];   // +2 / +4: the bulk copies start 16 B aligned
@@ -483,9 +481,7 @@ struct __align__(16) TileStage {
   TileDesc d;
 };
 
-struct TileWarpSmem {
-  TileStage stage[kTStages];
-  uint64_t bar[kTStages];
+struct TileWork {
   double pmin[kWNnz];       // finite min contributions, [position][row]
   double pmax[kWNnz];
   double x[kWNnz];          // filter terms
@@ -564,14 +560,15 @@ __device__ __forceinline__ void tile_issue_gathers(const RoundArgs& A, TileStage
 // frac_any = some integral column may carry a fractional bound
 __device__ __forceinline__ double column_q_fast(double lo, double up, bool integral,
                                                 bool frac_any, const DevCfg& c) {
-  if (isinf(lo) || isinf(up)) return CUDART_INF;
-  if (frac_any && integral && (lo != floor(lo) || up != ceil(up))) return CUDART_INF;
+  // an infinite bound makes both terms +inf (lb <= ub): no test needed
   const double thr = integral ? c.int_eps : c.imp_abs + c.imp_rel;
-  return ((up - lo) - thr) + (fabs(lo) + fabs(up)) * kMargin;
+  const double q = ((up - lo) - thr) + (fabs(lo) + fabs(up)) * kMargin;
+  if (frac_any && integral && (lo != floor(lo) || up != ceil(up))) return CUDART_INF;
+  return q;
 }
 
 template <bool kRowCheck>
-__device__ void tile_compute(const RoundArgs& A, TileWarpSmem& W, const TileStage& S,
+__device__ void tile_compute(const RoundArgs& A, TileWork& W, const TileStage& S,
                              bool frac_any, bool& inf_flag, const DevCfg& cfg) {
   const int lane = threadIdx.x & 31;
   const TileDesc d = S.d;
@@ -670,121 +667,173 @@ __device__ void tile_compute(const RoundArgs& A, TileWarpSmem& W, const TileStag
   __syncwarp();
 }
 
+// Warp-specialised dense path: per CTA one producer warp and kWsConsumers
+// consumer warps share a ring of kWsStages tile stages.
+//   producer: TMA bulk copies of tile i (vals/col/lhs/rhs), then -- kWsLag
+//             tiles behind -- cp.async gathers of the {lb, ub} records of
+//             tile i - lag, completing on the stage's `full` mbarrier
+//             (cp.async.mbarrier.arrive.noinc from every producer lane);
+//   consumer c: tiles c, c + C, ... : wait `full`, compute, release `empty`.
+// Memory parallelism is set by the ring depth, not by the number of
+// resident compute warps.
+#ifndef PG_WS_CONSUMERS
+#define PG_WS_CONSUMERS 6
+#endif
+#ifndef PG_WS_STAGES
+#define PG_WS_STAGES 8
+#endif
+constexpr int kWsConsumers = PG_WS_CONSUMERS;
+constexpr int kWsWarps = kWsConsumers + 1;
+constexpr int kWsStages = PG_WS_STAGES;
+constexpr int kWsLag = 2;
+
+struct TileRing {
+  TileStage stage[kWsStages];
+  uint64_t tma_bar[kWsStages];
+  uint64_t full_bar[kWsStages];
+  uint64_t empty_bar[kWsStages];
+  TileWork work[kWsConsumers];
+};
+struct TileSparseSmem {
+  TileStage stage[kWsWarps];
+  TileWork work[kWsWarps];
+};
+union TilesSmem {
+  TileRing ring;
+  TileSparseSmem sparse;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+// sparse round: per tile, the marked rows only, as a compacted virtual tile
+// staged with plain loads (uniform row length keeps the layout)
 template <bool kRowCheck>
-__global__ void __launch_bounds__(kTWarps * 32) k_tiles(const RoundArgs A, const DevCfg cfg) {
-  extern __shared__ __align__(16) unsigned char tiles_smem[];
-  TileWarpSmem& W = reinterpret_cast<TileWarpSmem*>(tiles_smem)[threadIdx.x >> 5];
+__device__ void tiles_sparse(const RoundArgs& A, TileStage& S, TileWork& W, int tb, int te,
+                             const uint8_t* rflag, bool frac_any, bool& inf_flag,
+                             const DevCfg& cfg) {
   const int lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * kTWarps + (threadIdx.x >> 5);
-  const int nw = gridDim.x * kTWarps;
-  // contiguous run of tiles of this warp (static: no global counter)
-  const int per = (A.num_tiles + nw - 1) / nw;
-  const int tb = min(gw * per, A.num_tiles), te = min(tb + per, A.num_tiles);
+  for (int t0 = tb; t0 < te; t0 += 32) {
+    TileDesc wd = {0, 0, 0, 0};
+    if (t0 + lane < te) wd = A.tiles[t0 + lane];
+    for (int u = 0; u < 32 && t0 + u < te; ++u) {
+      TileDesc d;
+      d.r0 = __shfl_sync(0xffffffffu, wd.r0, u);
+      d.nr = __shfl_sync(0xffffffffu, wd.nr, u);
+      d.k0 = __shfl_sync(0xffffffffu, wd.k0, u);
+      d.nz = __shfl_sync(0xffffffffu, wd.nz, u);
+      const unsigned m = __ballot_sync(0xffffffffu, lane < d.nr && rflag[d.r0 + lane]);
+      if (!m) continue;
+      const int L = d.nz / d.nr, nv = __popc(m);
+      // lane p of a marked row takes slot rank(p) of the virtual tile
+      if ((m >> lane) & 1u) {
+        const int rank = __popc(m & ((1u << lane) - 1u));
+        W.qe[rank] = (uint8_t)lane;
+        S.lhs[rank] = A.lhs[d.r0 + lane];
+        S.rhs[rank] = A.rhs[d.r0 + lane];
+      }
+      __syncwarp();
+      const float invL = 1.0f / (float)L;
+      for (int e = lane; e < nv * L; e += 32) {
+        const int r = __float2int_rz(((float)e + 0.5f) * invL);
+        const int k = d.k0 + W.qe[r] * L + (e - r * L);
+        const int32_t c = __ldg(A.colx + k);
+        S.vals[e] = __ldg(A.vals + k);
+        S.cols[e] = c;
+        S.rec[e] = __ldg(reinterpret_cast<const double2*>(&A.snap[c & 0x7fffffff].lo));
+      }
+      if (lane == 0) S.d = TileDesc{0, nv, 0, nv * L};
+      __syncwarp();
+      tile_compute<kRowCheck>(A, W, S, frac_any, inf_flag, cfg);
+    }
+  }
+}
+
+template <bool kRowCheck>
+__global__ void __launch_bounds__(kWsWarps * 32) k_tiles(const RoundArgs A, const DevCfg cfg) {
+  extern __shared__ __align__(16) unsigned char tiles_smem[];
+  TilesSmem& sm = *reinterpret_cast<TilesSmem*>(tiles_smem);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // contiguous run of tiles of this CTA (static: no global counter)
+  const int per = (A.num_tiles + gridDim.x - 1) / gridDim.x;
+  const int tb = min((int)blockIdx.x * per, A.num_tiles), te = min(tb + per, A.num_tiles);
   if (tb >= te) return;
   const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
-  const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
-  const uint8_t* rflag = A.dirty.row_flag + (size_t)par * A.dirty.ms;
   const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
-  auto next_tile = [&](int t) -> int { return t < te ? t : -1; };
+  bool inf_flag = false;
   if (!full) {
-    // sparse round: per tile, the marked rows only, as a compacted virtual
-    // tile staged with plain loads (uniform row length keeps the layout)
-    bool inf_sparse = false;
-    for (int t0 = tb; t0 < te; t0 += 32) {
-      TileDesc wd = {0, 0, 0, 0};
-      if (t0 + lane < te) wd = A.tiles[t0 + lane];
-      for (int u = 0; u < 32 && t0 + u < te; ++u) {
-        TileDesc d;
-        d.r0 = __shfl_sync(0xffffffffu, wd.r0, u);
-        d.nr = __shfl_sync(0xffffffffu, wd.nr, u);
-        d.k0 = __shfl_sync(0xffffffffu, wd.k0, u);
-        d.nz = __shfl_sync(0xffffffffu, wd.nz, u);
-        const unsigned m = __ballot_sync(0xffffffffu, lane < d.nr && rflag[d.r0 + lane]);
-        if (!m) continue;
-        const int L = d.nz / d.nr, nv = __popc(m);
-        TileStage& S = W.stage[0];
-        // lane p of a marked row takes slot rank(p) of the virtual tile
-        if ((m >> lane) & 1u) {
-          const int rank = __popc(m & ((1u << lane) - 1u));
-          W.qe[rank] = (uint8_t)lane;
-          S.lhs[rank] = A.lhs[d.r0 + lane];
-          S.rhs[rank] = A.rhs[d.r0 + lane];
-        }
-        __syncwarp();
-        const float invL = 1.0f / (float)L;
-        for (int e = lane; e < nv * L; e += 32) {
-          const int r = __float2int_rz(((float)e + 0.5f) * invL);
-          const int k = d.k0 + W.qe[r] * L + (e - r * L);
-          const int32_t c = __ldg(A.colx + k);
-          S.vals[e] = __ldg(A.vals + k);
-          S.cols[e] = c;
-          S.rec[e] = __ldg(reinterpret_cast<const double2*>(&A.snap[c & 0x7fffffff].lo));
-        }
-        if (lane == 0) S.d = TileDesc{0, nv, 0, nv * L};
-        __syncwarp();
-        tile_compute<kRowCheck>(A, W, S, frac_any, inf_sparse, cfg);
-      }
-    }
-    if (__any_sync(0xffffffffu, inf_sparse) && lane == 0) A.st->infeasible = 1;
+    const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
+    const uint8_t* rflag = A.dirty.row_flag + (size_t)par * A.dirty.ms;
+    // every warp takes a slice of the CTA's tiles
+    const int wper = (te - tb + kWsWarps - 1) / kWsWarps;
+    const int wb = min(tb + warp * wper, te), we = min(wb + wper, te);
+    tiles_sparse<kRowCheck>(A, sm.sparse.stage[warp], sm.sparse.work[warp], wb, we, rflag,
+                            frac_any, inf_flag, cfg);
+    if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
     return;
   }
-  if (lane == 0)
-    for (int i = 0; i < kTStages; ++i) mbar_init(&W.bar[i], 1);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncwarp();
-
-  // descriptors of a 32-tile window, one per lane (one coalesced load per window)
-  int wbase = -1;
-  TileDesc wdesc = {0, 0, 0, 0};
-  auto desc_of = [&](int t) -> TileDesc {
-    if (wbase < 0 || t >= wbase + 32) {
-      wbase = t;
-      if (t + lane < te) wdesc = A.tiles[t + lane];
+  TileRing& R = sm.ring;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kWsStages; ++i) {
+      mbar_init(&R.tma_bar[i], 1);
+      mbar_init(&R.full_bar[i], 32);
+      mbar_init(&R.empty_bar[i], 1);
     }
-    const int src = t - wbase;
-    TileDesc d;
-    d.r0 = __shfl_sync(0xffffffffu, wdesc.r0, src);
-    d.nr = __shfl_sync(0xffffffffu, wdesc.nr, src);
-    d.k0 = __shfl_sync(0xffffffffu, wdesc.k0, src);
-    d.nz = __shfl_sync(0xffffffffu, wdesc.nz, src);
-    return d;
-  };
-  int tq[kTStages];  // tiles in the pipeline: [0] compute, [1] gathers, [2] TMA
-  tq[0] = next_tile(tb);
-  if (tq[0] < 0) return;
-  tq[1] = next_tile(tq[0] + 1);
-  {
-    const TileDesc d0 = desc_of(tq[0]);
-    const TileDesc d1 = tq[1] >= 0 ? desc_of(tq[1]) : d0;
-    if (lane == 0) {
-      tile_issue_tma(A, W.stage[0], &W.bar[0], d0);
-      if (tq[1] >= 0) tile_issue_tma(A, W.stage[1], &W.bar[1], d1);
-    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  mbar_wait(&W.bar[0], 0);
-  tile_issue_gathers(A, W.stage[0], lane);
-  bool inf_flag = false;
-  for (int i = 0; tq[0] >= 0; ++i) {
-    const int s0 = i % kTStages, s1 = (i + 1) % kTStages, s2 = (i + 2) % kTStages;
-    if (tq[1] >= 0) {
-      mbar_wait(&W.bar[s1], (uint32_t)(((i + 1) / kTStages) & 1));
-      tile_issue_gathers(A, W.stage[s1], lane);
-      tq[2] = next_tile(tq[1] + 1);
-      if (tq[2] >= 0) {
-        const TileDesc d2 = desc_of(tq[2]);
-        if (lane == 0) tile_issue_tma(A, W.stage[s2], &W.bar[s2], d2);
+  __syncthreads();
+  const int N = te - tb;
+  if (warp == kWsConsumers) {
+    // ---- producer -----------------------------------------------------------
+    int wbase = -1;
+    TileDesc wdesc = {0, 0, 0, 0};
+    for (int it = 0; it < N + kWsLag; ++it) {
+      if (it < N) {
+        const int t = tb + it;
+        if (wbase < 0 || t >= wbase + 32) {  // descriptors, a 32-tile window per load
+          wbase = t;
+          if (t + lane < te) wdesc = A.tiles[t + lane];
+        }
+        TileDesc d;
+        d.r0 = __shfl_sync(0xffffffffu, wdesc.r0, t - wbase);
+        d.nr = __shfl_sync(0xffffffffu, wdesc.nr, t - wbase);
+        d.k0 = __shfl_sync(0xffffffffu, wdesc.k0, t - wbase);
+        d.nz = __shfl_sync(0xffffffffu, wdesc.nz, t - wbase);
+        const int slot = it % kWsStages, use = it / kWsStages;
+        if (use > 0) mbar_wait(&R.empty_bar[slot], (uint32_t)((use - 1) & 1));
+        if (lane == 0) tile_issue_tma(A, R.stage[slot], &R.tma_bar[slot], d);
       }
-      cp_async_wait<1>();
-    } else {
-      tq[2] = -1;
-      cp_async_wait<0>();
+      const int g = it - kWsLag;
+      if (g >= 0 && g < N) {
+        const int slot = g % kWsStages, use = g / kWsStages;
+        mbar_wait(&R.tma_bar[slot], (uint32_t)(use & 1));
+        TileStage& S = R.stage[slot];
+        const int oc = S.d.k0 & 3;
+#pragma unroll
+        for (int q = 0; q < kWItems; ++q) {
+          const int e = lane + 32 * q;
+          if (e < S.d.nz) cp_async16(&S.rec[e], &A.snap[S.cols[oc + e] & 0x7fffffff].lo);
+        }
+        cp_async_arrive_noinc(&R.full_bar[slot]);
+      }
     }
-    __syncwarp();
-    tile_compute<kRowCheck>(A, W, W.stage[s0], frac_any, inf_flag, cfg);
-    tq[0] = tq[1];
-    tq[1] = tq[2];
+  } else {
+    // ---- consumers ----------------------------------------------------------
+    TileWork& W = R.work[warp];
+    for (int i = warp; i < N; i += kWsConsumers) {
+      const int slot = i % kWsStages, use = i / kWsStages;
+      mbar_wait(&R.full_bar[slot], (uint32_t)(use & 1));
+      tile_compute<kRowCheck>(A, W, R.stage[slot], frac_any, inf_flag, cfg);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&R.empty_bar[slot]);
+    }
+    if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
   }
-  if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
 }
 
 template <bool kRowCheck>

@@ -15,9 +15,10 @@ ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--solve", action="store_true")
 ap.add_argument("--host-loop", action="store_true")
 ap.add_argument("--debug-flags", type=int, default=0)
+ap.add_argument("--worklist", action="store_true")
 a = ap.parse_args()
 inst = G.config_instance(a.config)
-cfg = EngineConfig(loop_mode=LoopMode.Host if a.host_loop else LoopMode.Graph)
+cfg = EngineConfig(loop_mode=LoopMode.Host if a.host_loop else LoopMode.Graph, worklist=a.worklist)
 import ctypes as C  # noqa: E402
 from paper_2009_07785_b200 import abi  # noqa: E402
 if a.debug_flags:
