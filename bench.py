@@ -14,7 +14,7 @@ instance (~200 MB in HBM) is larger than L2 and L2 is flushed between steps.
             graph launch; inputs resident in HBM), max over ranks
   e2e       the same solve through the C-ABI entry point pg_propagate with
             pinned HOST buffers: H2D upload + on-device setup + solve + D2H
-  roofline  the dominant kernel (k_round) timed alone with CUDA events:
+  roofline  the round kernels (k_sell + k_cand) timed alone with CUDA events:
             algorithmic bytes / mean launch time vs MEASURED_PEAKS hbm_gbs
   cpu_baseline  the reference's own cpu_seq (compiled from its sources into
             oracle/_ref; 1 core), best of a bounded number of solves
@@ -231,8 +231,8 @@ def bench_single(args, inst, world, rank, local):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
     for _ in range(args.warmup):
         r = sess.run()
-    launches_per_round = 2 + (1 if info["segments"] else 0) + (1 if info["num_tiles"] else 0) + (
-        1 if args.worklist else 0)
+    # k_sell + k_cand + k_commit (+ k_mark with the worklist)
+    launches_per_round = (2 if info["slices"] else 0) + 1 + (1 if args.worklist else 0)
 
     def barrier():
         torch.cuda.synchronize()
@@ -276,8 +276,8 @@ def bench_single(args, inst, world, rank, local):
         "instance": inst.name, "m": m, "n": n, "nnz": nnz,
         "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
         "worklist": args.worklist, "l2": "flushed between steps (256 MB write); instance > L2",
-        "warp_tiles": info["num_tiles"], "segment_rows": info["seg_rows"],
-        "segments": info["segments"]})
+        "slices": info["slices"], "chains": info["chains"], "sell_elems": info["sell_elems"],
+        "split_segments": info["segments"]})
     line.update({
         "rounds": R, "status": r.status.name,
         "rounds_per_s": round(R / (ms / 1e3), 1),
@@ -286,7 +286,7 @@ def bench_single(args, inst, world, rank, local):
         "round_roofline_frac": round(b_round(m, n, nnz) * R / (ms / 1e3) / 1e9 / peak, 4),
         "round_roofline_frac_8tbs": round(b_round(m, n, nnz) * R / (ms / 1e3) / 8e12, 4),
         "wall_ms_per_step": round(wall_ms / args.steps, 3),
-        "roofline": {"kernel": "k_round+k_tiles (dense round)", "bound": "hbm",
+        "roofline": {"kernel": "k_sell+k_cand (dense first round)", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
                      "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
                      "bytes_per_launch": k_bytes, "launch_us": round(k_ns / 1e3, 3),

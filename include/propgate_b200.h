@@ -205,7 +205,10 @@ int pg_nccl_unique_id(uint8_t* out128);
 int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank,
                            int32_t world);
 
-/* Session statistics: number of row tiles, long rows, chunks. */
+/* Session statistics, in this order: m, n, nnz, slices (sliced-ELL, 32
+ * chains each), split-candidate rows (> 16 entries), segments (chains of
+ * those rows), short rows, short-row entries, segment entries, chains,
+ * sliced-ELL elements (entries + padding). */
 int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info);
 
 /* Thread-local message of the last failed call on this thread. */

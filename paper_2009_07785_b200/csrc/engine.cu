@@ -24,6 +24,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cstdlib>
+#include <limits>
 #include <mutex>
 #include <thread>
 #include <cstdio>
@@ -40,6 +41,8 @@
 
 #include "kernels.cuh"
 #include "setup.cuh"
+#include "sell.cuh"
+#include "cand.cuh"
 
 using namespace pgb;
 
@@ -193,7 +196,8 @@ struct pg_session {
   pg_config cfg{};
   DevCfg dcfg{};
   int num_sms = 148;
-  int tiles_per_sm = 1;  // resident k_tiles CTAs per SM (occupancy)
+  int sell_per_sm = 1;   // resident k_sell CTAs per SM
+  int cand_per_sm = 1;   // resident k_cand CTAs per SM
 
   // device arrays
   int32_t* d_row_ptr = nullptr;
@@ -209,15 +213,21 @@ struct pg_session {
   double* d_up0 = nullptr;
   double* d_lo_res = nullptr;
   double* d_up_res = nullptr;
-  TileDesc* d_tiles = nullptr;
-  SegGroup* d_groups = nullptr;
   SegDesc* d_segs = nullptr;
   int32_t* d_srow = nullptr;
   int32_t* d_sfirst = nullptr;
-  int32_t* d_chunk_seg = nullptr;
   SegPartial* d_partial = nullptr;
-  Act* d_row_act = nullptr;
-  int32_t* d_worklist = nullptr;
+  Act* d_ract = nullptr;           // phase-2 queues
+  int32_t* d_wl_short = nullptr;
+  CandItem* d_wl_long = nullptr;
+  // sliced-ELL copy of the matrix (sell.cuh)
+  UnitDesc* d_units = nullptr;
+  SliceDesc* d_slices = nullptr;
+  double* d_sv = nullptr;
+  int32_t* d_sc = nullptr;
+  uint32_t* d_sw = nullptr;
+  int32_t nunits = 0, nslices = 0, lg_min = 0;
+  int64_t sell_elems = 0;
   DevState* d_st = nullptr;
   long long* d_per_round = nullptr;
   // worklist index and dirty sets
@@ -229,15 +239,15 @@ struct pg_session {
 
   // host mirrors
   DevState* h_st = nullptr;  // pinned
-  int32_t num_tiles = 0, nseg = 0, nsrow = 0, ngroups = 0;
-  int64_t tile_rows = 0, tile_nnz = 0, seg_nnz = 0;
+  int32_t nseg = 0, nsrow = 0;
+  int64_t short_rows = 0, short_nnz = 0, seg_nnz = 0, wl_long_cap = 0;
 
   // graph
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
   cudaGraphConditionalHandle cond = 0;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
-  cudaStream_t stream2 = nullptr;
+  cudaStream_t stream2 = nullptr;  // session setup: ordering overlapped with the upload
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* comm = nullptr;  // NCCL communicator of the row-sharded mode
   // branch-and-bound: the root fixpoint and the next solve's start control
@@ -259,8 +269,8 @@ struct pg_session {
     if (comm) g_nccl.comm_destroy(comm);
     for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up}) dfree(p);
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
-                    d_lo_res, d_up_res, d_tiles, d_groups, d_segs, d_srow, d_sfirst, d_chunk_seg, d_partial,
-                    d_row_act, d_worklist, d_st, d_per_round, d_col_ptr, d_col_item,
+                    d_lo_res, d_up_res, d_segs, d_srow, d_sfirst, d_partial,
+                    d_ract, d_wl_short, d_wl_long, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
                     d_flags, d_chg};
     for (void* p : ptrs) dfree(p);  // stream-ordered: no device sync here
     if (h_st) cudaFreeHost(h_st);
@@ -275,24 +285,27 @@ struct pg_session {
   // ---- one round of kernels, enqueued on `stream` ------------------------------
   RoundArgs round_args() const {
     RoundArgs A;
-    A.tiles = d_tiles;
-    A.num_tiles = num_tiles;
+    A.slices = d_slices;
+    A.nslices = nslices;
+    A.nunits = nunits;
+    A.units = d_units;
+    A.sv = d_sv;
+    A.sc = d_sc;
+    A.sw = d_sw;
+    A.pad_col = n;
     A.segs = d_segs;
-    A.nseg = nseg;
-    A.groups = d_groups;
-    A.ngroups = ngroups;
     A.srow = d_srow;
     A.sfirst = d_sfirst;
-    A.chunk_seg = d_chunk_seg;
     A.row_done = d_row_done;
     A.partial = d_partial;
-    A.row_act = d_row_act;
-    A.worklist = d_worklist;
     A.row_ptr = d_row_ptr;
     A.colx = d_colx;
     A.vals = d_vals;
     A.lhs = d_lhs;
     A.rhs = d_rhs;
+    A.ract = d_ract;
+    A.wl_short = d_wl_short;
+    A.wl_long = d_wl_long;
     A.snap = d_snap;
     A.key_out = (long long*)d_key_out;
     A.st = d_st;
@@ -300,40 +313,28 @@ struct pg_session {
     return A;
   }
 
+  // One round: phase 1 (k_sell), phase 2 (k_cand), [row shards: all-reduce],
+  // commit + decision (k_commit), [worklist: k_mark].  k1_begin/k1_end
+  // bracket the two compute phases (bench.py's roofline timing).
   void enqueue_round(bool use_graph, cudaEvent_t k1_begin = nullptr, cudaEvent_t k1_end = nullptr) {
     const bool rowcheck = (cfg.flags & PG_FLAG_ROWCHECK) != 0;
-    RoundArgs A = round_args();
-    // timing-only switches (results are wrong with them): 0x100 no segment
-    // groups, 0x200 no warp tiles
+    const RoundArgs A = round_args();
     if (k1_begin) PG_CUDA(cudaEventRecord(k1_begin, stream));
-    // segment groups and warp tiles are independent: two branches of the round
-    if (ngroups > 0 && num_tiles > 0) {
-      PG_CUDA(cudaEventRecord(ev_fork, stream));
-      PG_CUDA(cudaStreamWaitEvent(stream2, ev_fork, 0));
-    }
-    if (ngroups > 0 && !(cfg.flags & 0x100u)) {
-      cudaStream_t sg = num_tiles > 0 ? stream2 : stream;
-      const int grid = std::max(1, std::min(ngroups, num_sms * 2));
+    if (nslices > 0) {
+      const int grid = std::max(1, std::min((nslices + 7) / 8, num_sms * sell_per_sm));
       if (rowcheck)
-        k_round<true><<<grid, kRoundThreads, sizeof(SegGroupSmem), sg>>>(A, dcfg);
+        k_sell<true, true><<<grid, kSellThreads, 0, stream>>>(A, dcfg);
       else
-        k_round<false><<<grid, kRoundThreads, sizeof(SegGroupSmem), sg>>>(A, dcfg);
-    }
-    if (num_tiles > 0 && !(cfg.flags & 0x200u)) {
-      // all resident CTAs, each a producer warp + consumer warps over a tile ring
-      const int grid = std::max(1, std::min((num_tiles + 7) / 8, num_sms * tiles_per_sm));
-      if (rowcheck)
-        k_tiles<true><<<grid, kWsWarps * 32, sizeof(TilesSmem), stream>>>(A, dcfg);
-      else
-        k_tiles<false><<<grid, kWsWarps * 32, sizeof(TilesSmem), stream>>>(A, dcfg);
-    }
-    if (ngroups > 0 && num_tiles > 0) {
-      PG_CUDA(cudaEventRecord(ev_join, stream2));
-      PG_CUDA(cudaStreamWaitEvent(stream, ev_join, 0));
+        k_sell<false, true><<<grid, kSellThreads, 0, stream>>>(A, dcfg);
+      if (dirty.enabled) {
+        if (rowcheck)
+          k_sell<true, false><<<grid, kSellThreads, 0, stream>>>(A, dcfg);
+        else
+          k_sell<false, false><<<grid, kSellThreads, 0, stream>>>(A, dcfg);
+      }
+      k_cand<<<num_sms * cand_per_sm, kCandThreads, 0, stream>>>(A, dcfg);
     }
     if (k1_end) PG_CUDA(cudaEventRecord(k1_end, stream));
-    if (nseg > 0)
-      k_seg_cand<<<std::min(nseg, num_sms * 8), 256, 0, stream>>>(A, dcfg);
     if (comm) {
       // row shards: merge every rank's bound keys (lb keys and negated ub keys)
       // and infeasibility with one max all-reduce; each rank then commits the
@@ -482,17 +483,11 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->dev = cfg->device;
     PG_CUDA(cudaSetDevice(s->dev));
     s->num_sms = prop.sms;
-    PG_CUDA(cudaFuncSetAttribute(k_round<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(SegGroupSmem)));
-    PG_CUDA(cudaFuncSetAttribute(k_round<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(SegGroupSmem)));
-    PG_CUDA(cudaFuncSetAttribute(k_tiles<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(TilesSmem)));
-    PG_CUDA(cudaFuncSetAttribute(k_tiles<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)sizeof(TilesSmem)));
-    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->tiles_per_sm, k_tiles<true>,
-                                                          kWsWarps * 32, sizeof(TilesSmem)));
-    s->tiles_per_sm = std::max(1, s->tiles_per_sm);
+    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->sell_per_sm, k_sell<true, true>,
+                                                          kSellThreads, 0));
+    s->sell_per_sm = std::max(1, s->sell_per_sm);
+    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->cand_per_sm, k_cand, kCandThreads, 0));
+    s->cand_per_sm = std::max(1, s->cand_per_sm);
 
     s->m = p->num_rows;
     s->n = p->num_cols;
@@ -582,32 +577,24 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     TileLayout lay{};
     lay.nclass = short_max + 1;
     {
-      int32_t row = 0, tiles = 0;
+      int32_t row = 0;
       for (int32_t L = 0; L <= short_max; ++L) {
         lay.class_start[L] = row;
-        lay.tile_off[L] = tiles;
-        const int32_t cap = L ? std::min(32, kWNnz / L) : 32;
-        tiles += (cls[L] + cap - 1) / cap;
         row += cls[L];
       }
       lay.class_start[short_max + 1] = row;
-      lay.tile_off[short_max + 1] = tiles;
-      s->num_tiles = tiles;
-      s->tile_rows = row;
+      s->short_rows = row;
       s->nsrow = m - row;
     }
-    s->d_tiles = dalloc<TileDesc>(s->num_tiles);
     s->d_srow = dalloc<int32_t>(s->nsrow);
     s->d_sfirst = dalloc<int32_t>((size_t)s->nsrow + 1);
     int32_t* scnt = dalloc<int32_t>((size_t)s->nsrow + 1);
     PG_CUDA(cudaEventRecord(s->ev_join, st));
     PG_CUDA(cudaStreamWaitEvent(s2, s->ev_join, 0));  // allocations above happen on stream 1
-    if (s->num_tiles)
-      k_make_tiles<<<s->grid_for(s->num_tiles, 256), 256, 0, s2>>>(lay, s->d_row_ptr, s->d_tiles);
-    int32_t h_nseg = 0, h_nlong = 0;
+    int32_t h_nseg = 0;
     if (s->nsrow) {
       k_seg_counts<<<s->grid_for((int64_t)s->nsrow + 1, 256), 256, 0, s2>>>(
-          s->d_row_ptr, (int)s->tile_rows, s->nsrow, chunk, scnt, s->d_srow);
+          s->d_row_ptr, (int)s->short_rows, s->nsrow, chunk, scnt, s->d_srow);
       size_t need = 0;
       PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, scnt, s->d_sfirst, s->nsrow + 1, s2));
       cub_tmp(need);
@@ -616,22 +603,19 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       PG_CUDA(cudaStreamSynchronize(s2));
     }
     s->nseg = h_nseg;
-    for (int32_t L = 0; L <= short_max; ++L) s->tile_nnz += (int64_t)L * cls[L];
-    s->seg_nnz = nnz - s->tile_nnz;
+    for (int32_t L = 0; L <= short_max; ++L) s->short_nnz += (int64_t)L * cls[L];
+    s->seg_nnz = nnz - s->short_nnz;
     s->d_segs = dalloc<SegDesc>(s->nseg);
-    s->d_chunk_seg = dalloc<int32_t>(s->nseg);
     SegDesc* segs_in = dalloc<SegDesc>(s->nseg);
     uint32_t* skey = dalloc<uint32_t>(s->nseg);
     uint32_t* skey2 = dalloc<uint32_t>(s->nseg);
     int32_t* sidx = dalloc<int32_t>(s->nseg);
     int32_t* sorder = dalloc<int32_t>(s->nseg);
-    int32_t* d_nlong = dalloc<int32_t>(1);
-    PG_CUDA(cudaMemsetAsync(d_nlong, 0, sizeof(int32_t), st));
     PG_CUDA(cudaEventRecord(s->ev_join, st));
     PG_CUDA(cudaStreamWaitEvent(s2, s->ev_join, 0));
     if (s->nseg) {
       k_emit_segs<<<s->grid_for((int64_t)s->nsrow * 32, 256, 16), 256, 0, s2>>>(
-          s->d_row_ptr, s->d_sfirst, (int)s->tile_rows, s->nsrow, chunk, segs_in, skey, sidx);
+          s->d_row_ptr, s->d_sfirst, (int)s->short_rows, s->nsrow, chunk, segs_in, skey, sidx);
       int bits = 1;
       while (bits < 32 && (1u << bits) <= (uint32_t)chunk) ++bits;
       size_t need = 0;
@@ -640,19 +624,8 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       cub_tmp(need);
       PG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, skey, skey2, sidx, sorder, s->nseg, 0,
                                               bits, s2));
-      k_order_segs<<<s->grid_for(s->nseg, 256), 256, 0, s2>>>(segs_in, sorder, s->nseg, s->d_segs,
-                                                              s->d_chunk_seg, d_nlong);
-      PG_CUDA(cudaMemcpyAsync(&h_nlong, d_nlong, sizeof(int32_t), cudaMemcpyDeviceToHost, s2));
-      PG_CUDA(cudaStreamSynchronize(s2));
+      k_order_segs<<<s->grid_for(s->nseg, 256), 256, 0, s2>>>(segs_in, sorder, s->nseg, s->d_segs);
     }
-    const int32_t n8 = (h_nlong + 7) / 8;
-    s->ngroups = s->nseg ? n8 + std::max(0, (s->nseg - 8 * n8 + 31) / 32) : 0;
-    s->d_groups = dalloc<SegGroup>(s->ngroups);
-    PG_CUDA(cudaEventRecord(s->ev_join, st));
-    PG_CUDA(cudaStreamWaitEvent(s2, s->ev_join, 0));
-    if (s->ngroups)
-      k_make_groups<<<s->grid_for(s->ngroups, 256), 256, 0, s2>>>(s->nseg, n8, s->ngroups,
-                                                                  s->d_groups);
     PG_CUDA(cudaGetLastError());
     tm.lap("ordering + tables (dev)");
 
@@ -660,15 +633,24 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->d_vals = dalloc<double>(nnz + 2);
     s->d_lhs = dalloc<double>((size_t)m + 2);
     s->d_rhs = dalloc<double>((size_t)m + 2);
-    s->d_snap = dalloc<Snap>(n);
+    s->d_snap = dalloc<Snap>((size_t)n + 1);  // + the padding column of the sliced-ELL copy
+    {
+      // bounds [0, 0] (a padding entry adds +0.0) and q = -inf (its filter
+      // term 0 * -inf is NaN, which fmax ignores)
+      static const Snap pad = {0.0, 0.0, -std::numeric_limits<double>::infinity(), 0};
+      PG_CUDA(cudaMemcpyAsync(s->d_snap + n, &pad, sizeof(Snap), cudaMemcpyHostToDevice, st));
+    }
     s->d_key_out = dalloc<longlong2>((size_t)n + 1);  // + infeasibility slot
     s->d_lo0 = dalloc<double>(n);
     s->d_up0 = dalloc<double>(n);
     s->d_lo_res = dalloc<double>(n);
     s->d_up_res = dalloc<double>(n);
     s->d_partial = dalloc<SegPartial>(s->nseg);
-    s->d_row_act = dalloc<Act>(s->nsrow);
-    s->d_worklist = dalloc<int32_t>(s->nseg);
+    // phase-2 queues: every row at most once; a long row in pieces
+    s->d_ract = dalloc<Act>(m);
+    s->d_wl_short = dalloc<int32_t>(m);
+    s->wl_long_cap = nnz / kCandShort + nnz / kCandPiece + 1;
+    s->d_wl_long = dalloc<CandItem>(s->wl_long_cap);
     s->d_row_done = dalloc<int32_t>(s->nsrow);
     s->d_st = dalloc<DevState>(1);
     s->d_ctl = dalloc<NodeCtl>(1);
@@ -688,11 +670,79 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
           s->d_vals, s->d_lhs, s->d_rhs, m, cfg->infinity_threshold);
       PG_CUDA(cudaGetLastError());
     }
-    uint8_t* d_integral = s->d_integral;
-    (void)d_integral;
+    // sliced-ELL copy (sell.cuh): units sorted by length, slices per
+    // lanes-per-unit region, transposed fill
+    s->nunits = s->nseg + (int32_t)s->short_rows;
+    if (s->nunits) {
+      const int32_t nu = s->nunits;
+      UnitDesc* u_in = dalloc<UnitDesc>(nu);
+      int32_t* k0_in = dalloc<int32_t>(nu);
+      int32_t* uk0 = dalloc<int32_t>(nu);
+      uint32_t* ukey = dalloc<uint32_t>(nu);
+      uint32_t* ukey2 = dalloc<uint32_t>(nu);
+      int32_t* uidx = dalloc<int32_t>(nu);
+      int32_t* uord = dalloc<int32_t>(nu);
+      int32_t* rcnt = dalloc<int32_t>(4);
+      s->d_units = dalloc<UnitDesc>(nu);
+      PG_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(int32_t) * 4, st));
+      k_make_units<<<s->grid_for(nu, 256), 256, 0, st>>>(s->d_segs, s->nseg, s->d_srow, s->d_sfirst,
+                                                           lay, s->d_row_ptr, nu, chunk, u_in, k0_in,
+                                                           ukey, uidx);
+      int bits = 1;
+      while (bits < 32 && (1u << bits) <= (uint32_t)chunk) ++bits;
+      size_t need = 0;
+      PG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, ukey, ukey2, uidx, uord, nu, 0, bits, st));
+      void* stmp = dalloc<unsigned char>(need);
+      PG_CUDA(cub::DeviceRadixSort::SortPairs(stmp, need, ukey, ukey2, uidx, uord, nu, 0, bits, st));
+      k_order_units<<<s->grid_for(nu, 256), 256, 0, st>>>(u_in, k0_in, uord, nu, s->d_units, uk0);
+      // lanes per unit at least 2^lg_min: a small instance spreads its chains
+      // so that about one slice per resident warp remains
+      const int64_t resident = (int64_t)s->num_sms * s->sell_per_sm * kSellWarps;
+      int lg_min = 0;
+      while (lg_min < 3 && ((int64_t)nu << lg_min) < resident * 32) ++lg_min;
+      s->lg_min = lg_min;
+      k_unit_regions<<<s->grid_for(nu, 256), 256, 0, st>>>(s->d_units, nu, lg_min, rcnt);
+      int32_t hc[4] = {0, 0, 0, 0};
+      PG_CUDA(cudaMemcpyAsync(hc, rcnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
+      PG_CUDA(cudaStreamSynchronize(st));
+      SellRegions R{};
+      R.ustart[0] = 0;
+      R.ustart[1] = hc[3];
+      R.ustart[2] = std::max(hc[2], R.ustart[1]);
+      R.ustart[3] = std::max(hc[1], R.ustart[2]);
+      R.ustart[4] = nu;
+      R.sstart[0] = 0;
+      for (int k = 0; k < 4; ++k) {
+        const int H = 32 >> (3 - k);
+        R.sstart[k + 1] = R.sstart[k] + (R.ustart[k + 1] - R.ustart[k] + H - 1) / H;
+      }
+      s->nslices = R.sstart[4];
+      s->d_slices = dalloc<SliceDesc>(s->nslices);
+      long long* elems = dalloc<long long>((size_t)s->nslices + 1);
+      long long* soff = dalloc<long long>((size_t)s->nslices + 1);
+      k_slice_desc<<<s->grid_for((int64_t)s->nslices + 1, 256), 256, 0, st>>>(s->d_units, R,
+                                                                              s->d_slices, elems);
+      need = 0;
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, elems, soff, s->nslices + 1, st));
+      void* stmp2 = dalloc<unsigned char>(need);
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(stmp2, need, elems, soff, s->nslices + 1, st));
+      long long total = 0;
+      PG_CUDA(cudaMemcpyAsync(&total, soff + s->nslices, sizeof(long long), cudaMemcpyDeviceToHost, st));
+      PG_CUDA(cudaStreamSynchronize(st));
+      s->sell_elems = total;
+      s->d_sv = dalloc<double>((size_t)total + 1);
+      s->d_sc = dalloc<int32_t>((size_t)total + 1);
+      s->d_sw = dalloc<uint32_t>((size_t)total + 1);
+      k_fill_sell<<<s->grid_for((int64_t)s->nslices * 32, 256, 16), 256, 0, st>>>(
+          s->d_units, uk0, s->nslices, soff, s->d_vals, s->d_colx, n, s->d_slices, s->d_sv, s->d_sc);
+      PG_CUDA(cudaGetLastError());
+      for (void* q : {(void*)u_in, (void*)k0_in, (void*)uk0, (void*)ukey, (void*)ukey2, (void*)uidx,
+                      (void*)uord, (void*)rcnt, (void*)elems, (void*)soff, stmp, stmp2})
+        dfree(q);
+    }
     for (void* q : {(void*)key, (void*)key2, (void*)idx, (void*)slen, (void*)counts, (void*)scnt,
                     (void*)segs_in, (void*)skey, (void*)skey2, (void*)sidx, (void*)sorder,
-                    (void*)d_nlong, tmp})
+                    tmp})
       dfree(q);
     PG_CUDA(cudaStreamSynchronize(st));
     tm.lap("H2D + permute");
@@ -702,7 +752,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       D.m = m;
       D.ms = (m + 15) & ~15;
       D.n = n;
-      D.first_seg_row = (int32_t)s->tile_rows;
+      D.first_seg_row = (int32_t)s->short_rows;
       D.enabled = (cfg->flags & PG_FLAG_WORKLIST) != 0;
       s->d_flags = dalloc<uint8_t>(2 * (size_t)D.ms + 16);
       D.row_flag = s->d_flags;
@@ -738,6 +788,21 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
                     (void*)t_perm})
       dfree(q);
     tm.lap("worklist/bounds/free");
+    // keep the snapshot records (the per-entry random gathers) resident in a
+    // persisting L2 carve-out while the matrix streams through
+    if (const char* e = getenv("PG_L2_PERSIST_MB")) {
+      const size_t want = (size_t)atoi(e) << 20;
+      if (want) {
+        PG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+        cudaStreamAttrValue av = {};
+        av.accessPolicyWindow.base_ptr = s->d_snap;
+        av.accessPolicyWindow.num_bytes = std::min(sizeof(Snap) * ((size_t)n + 1), want);
+        av.accessPolicyWindow.hitRatio = 1.0f;
+        av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        PG_CUDA(cudaStreamSetAttribute(s->stream, cudaStreamAttributeAccessPolicyWindow, &av));
+      }
+    }
     if (cfg->loop_mode == PG_LOOP_GRAPH) s->build_graph();
     tm.lap("graph instantiate");
     return s;
@@ -1151,8 +1216,8 @@ int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info) {
     g_err = "NULL argument";
     return PG_EINVAL;
   }
-  const int64_t v[] = {s->m, s->n, s->nnz, s->num_tiles, s->nsrow, s->nseg,
-                       s->tile_rows, s->tile_nnz, s->seg_nnz};
+  const int64_t v[] = {s->m, s->n, s->nnz, s->nslices, s->nsrow, s->nseg,
+                       s->short_rows, s->short_nnz, s->seg_nnz, s->nunits, s->sell_elems};
   for (int i = 0; i < n_info && i < (int)(sizeof(v) / sizeof(v[0])); ++i) info[i] = v[i];
   return PG_OK;
 }

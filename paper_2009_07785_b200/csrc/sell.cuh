@@ -1,0 +1,539 @@
+// sell.cuh -- one propagation round over a sliced-ELL copy of the matrix.
+//
+// Work units are the serial activity chains of cpu_par (par_engine.cpp:
+// 126-146, 99-123): every row of at most nnz_budget entries is ONE chain
+// (compute_row_activities in entry order, propcore.hpp:45-65), and a longer
+// row is split into chains of nnz_budget entries whose partial records are
+// combined pairwise afterwards (wide_row_activities).  Units are sorted by
+// length, descending, and cut into slices (kernels.cuh, SliceDesc): short
+// units one per lane, long units spread over G = 2/4/8 lanes so that no
+// warp carries a 1024-step dependent chain.
+//
+// Phase 1 (per slice, one warp): every lane loads its entries (coalesced,
+// one 256 B / 128 B request per step), gathers the column's 32 B snapshot
+// record (one L2 sector, kept resident with an evict_last policy while the
+// matrix streams through with evict_first), and forms the entry's min/max
+// contributions.  The G lanes of a unit hand their products to the unit's
+// owner lane in entry order (shuffles), so each sum is the reference's
+// sequential chain, bit for bit.  Each entry also stores a 4-byte filter
+// word: its filter term |a| q rounded up to float, with the two infinity
+// flags in the low mantissa bits (always >= the exact term, so a test on it
+// never drops an entry the exact test keeps).
+//
+// Phase 2 (same warp, whole rows only): row check (propcore.hpp:147-156),
+// row filter, then one pass over the slice's filter words; the entries that
+// may tighten are compacted into a per-warp queue and run through the exact
+// candidate pipeline 32 at a time (re-loading only those entries).  Chunks
+// of split rows write partial records; the last chunk combines them in
+// chunk order and queues the row's pieces for k_cand (cand.cuh).
+#pragma once
+
+#include "kernels.cuh"
+#include "setup.cuh"
+
+namespace pgb {
+
+#ifndef PG_SELL_UNROLL
+#define PG_SELL_UNROLL 4
+#endif
+#ifndef PG_SELL_HINTS
+#define PG_SELL_HINTS 1
+#endif
+#ifndef PG_SELL_PF
+#define PG_SELL_PF 1
+#endif
+#ifndef PG_SELL_LGU
+#define PG_SELL_LGU 2  // slices with lg >= this use PG_SELL_ULONG steps per group
+#endif
+#ifndef PG_SELL_ULONG
+#define PG_SELL_ULONG 2
+#endif
+#ifndef PG_SELL_LGMAX
+#define PG_SELL_LGMAX 3
+#endif
+#ifndef PG_SELL_MINB
+#define PG_SELL_MINB 2
+#endif
+constexpr int kSellUnroll = PG_SELL_UNROLL;
+constexpr int kSellThreads = 256;
+constexpr int kSellWarps = kSellThreads / 32;
+// lanes per unit by unit length: > 256 -> 8, > 128 -> 4, > 64 -> 2, else 1
+constexpr int kSellG8 = 256, kSellG4 = 128, kSellG2 = 64;
+
+// ---- memory access helpers ------------------------------------------------------
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ void ld_snap_keep(const Snap* p, uint64_t pol, double& lo, double& up,
+                                             double& q) {
+#if !PG_SELL_HINTS
+  ld_snap(p, lo, up, q);
+  return;
+#endif
+  long long f;
+  asm volatile("ld.global.nc.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(lo), "=d"(up), "=d"(q), "=l"(f)
+               : "l"(p), "l"(pol));
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
+#if !PG_SELL_HINTS
+  return __ldg(p);
+#endif
+  double v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+               : "=d"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t* p, uint64_t pol) {
+#if !PG_SELL_HINTS
+  return __ldg(p);
+#endif
+  int32_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+               : "=r"(v)
+               : "l"(p), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// ---- filter words -----------------------------------------------------------------
+// |a| q rounded toward +inf to float; bit 0 = min contribution infinite,
+// bit 1 = max contribution infinite.  +inf / NaN terms read back as NaN,
+// which every threshold test passes.
+// (+inf keeps its exponent; decoding sets the low bits of a positive word,
+// so it reads back as NaN)
+__device__ __forceinline__ uint32_t filt_encode(double x, bool imin, bool imax) {
+  const uint32_t b = __float_as_uint(__double2float_ru(x));
+  return (b & ~3u) | (imin ? 1u : 0u) | (imax ? 2u : 0u);
+}
+// a value >= the encoded term (low bits set for positive, cleared for negative)
+__device__ __forceinline__ double filt_term(uint32_t b) {
+  return (double)__uint_as_float((b & 0x80000000u) ? (b & ~3u) : (b | 3u));
+}
+__device__ __forceinline__ bool filt_may(const RowFilter& f, uint32_t b) {
+  const double x = filt_term(b);
+  return ((f.mode & 1) && !(f.tr > x)) || ((f.mode & 2) && !(f.tl > x)) ||
+         ((f.mode & 4) && (b & 1u)) || ((f.mode & 8) && (b & 2u));
+}
+
+// ---- per-warp shared state ----------------------------------------------------------
+struct SellWarpSmem {
+  double min_f[32], max_f[32], lhs[32], rhs[32], tr[32], tl[32];
+  int32_t min_i[32], max_i[32];
+  uint8_t mode[32], may[32];
+  // entries that survive the filter: element offset in the slice, unit
+  int32_t qe[64];
+  uint8_t qu[64];
+};
+
+// exact pipeline over queue entries [0, cnt), one per lane
+__device__ __forceinline__ bool sell_drain(const RoundArgs& A, const SellWarpSmem& W,
+                                           long long off, int cnt, int lane, uint64_t pol_keep,
+                                           const DevCfg& cfg) {
+  bool inf_flag = false;
+  if (lane < cnt) {
+    const int u = W.qu[lane];
+    const long long e = off + W.qe[lane];
+    const double a = A.sv[e];
+    const int32_t c = A.sc[e];
+    double lo, up, q;
+    ld_snap_keep(A.snap + (c & 0x7fffffff), pol_keep, lo, up, q);
+    const Act act = {W.min_f[u], W.max_f[u], W.min_i[u], W.max_i[u]};
+    inf_flag = entry_pipeline(act, a, lo, up, W.lhs[u], W.rhs[u], c, A.key_out, cfg);
+  }
+  return inf_flag;
+}
+
+// One step of a unit's chain on this lane: contributions (propcore.hpp:50-62:
+// b by the sign of a; an infinite b is counted, a finite one adds a*b),
+// filter term and word.  Adding +0.0 (an infinite b, or a padding entry) is
+// exact: the sums start at +0.0 and never become -0.0.  With G = 2^LG lanes
+// per unit, the G entries of the step sit on lanes u, u + H, .. and are
+// added in entry order (every lane of the unit forms the same sum).
+template <int LG>
+__device__ __forceinline__ void sell_step(double a, double lo, double up, double q, int u, Act& act,
+                                          double& xmax, uint32_t* pw) {
+  constexpr int G = 1 << LG, H = 32 >> LG;
+  const double bmin = a > 0 ? lo : up;
+  const double bmax = a > 0 ? up : lo;
+  const bool imin = isinf(bmin), imax = isinf(bmax);
+  const double pmin = imin ? 0.0 : __dmul_rn(a, bmin);
+  const double pmax = imax ? 0.0 : __dmul_rn(a, bmax);
+  act.min_i += imin;
+  act.max_i += imax;
+  const double x = fabs(a) * q;
+  xmax = fmax(xmax, x);
+  *pw = filt_encode(x, imin, imax);
+  if (LG == 0) {
+    act.min_f = __dadd_rn(act.min_f, pmin);
+    act.max_f = __dadd_rn(act.max_f, pmax);
+  } else {
+#pragma unroll
+    for (int jj = 0; jj < G; ++jj) {
+      const double vmin = __shfl_sync(0xffffffffu, pmin, u + H * jj);
+      const double vmax = __shfl_sync(0xffffffffu, pmax, u + H * jj);
+      act.min_f = __dadd_rn(act.min_f, vmin);
+      act.max_f = __dadd_rn(act.max_f, vmax);
+    }
+  }
+}
+
+// One slice by one warp.  LG = log2(lanes per unit); kDense: a full sweep
+// (no worklist), every lane walks every step of the slice.
+template <bool kRowCheck, int LG, bool kDense>
+__device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, const SliceDesc& sd,
+                                           int lane, bool full, const uint8_t* rflag,
+                                           uint64_t pol_keep, uint64_t pol_stream, bool& inf_flag,
+                                           const DevCfg& cfg) {
+  constexpr int G = 1 << LG, H = 32 >> LG;
+  const int j = lane >> (5 - LG), u = lane & (H - 1);
+  UnitDesc ud = {0, -1};
+  bool active = u < sd.count;
+  if (active) ud = A.units[sd.first + u];
+  if (!full && active) {
+    // worklist: the unit's row must carry a mark (split rows: all chunks of a
+    // marked row are marked, so its finisher sees every partial)
+    const int fr = ud.ref >= 0 ? ud.ref : A.srow[A.segs[-ud.ref - 1].rslot];
+    active = rflag[fr] != 0;
+  }
+  if (!__any_sync(0xffffffffu, active)) return;
+  const int len = active ? ud.len : 0;
+  const double* sv = A.sv + sd.off + lane;
+  const int32_t* sc = A.sc + sd.off + lane;
+  uint32_t* sw = A.sw + sd.off + lane;
+  const bool whole = ud.ref >= 0;
+  const int steps = sd.steps;
+
+  // ---- phase 1: the chains ------------------------------------------------------
+  Act act = {0.0, 0.0, 0, 0};
+  double xmax = -CUDART_INF;
+  if (kDense) {
+    constexpr int UL = LG >= PG_SELL_LGU ? PG_SELL_ULONG : kSellUnroll;
+    // every lane walks all `steps` of the slice: entries past a unit's end are
+    // padding (value 0, the padding column with bounds [0, 0]) and add +0.0
+    const double* pa = sv;
+    const int32_t* pc = sc;
+    uint32_t* pw = sw;
+    int t = 0;
+    for (; t + UL <= steps; t += UL) {
+      if (PG_SELL_PF && lane == 0 && t + 5 * UL <= steps) {
+        prefetch_l2(pa + 32 * 4 * UL, 256u * UL);
+        prefetch_l2(pc + 32 * 4 * UL, 128u * UL);
+      }
+      double a[UL], lo[UL], up[UL], q[UL];
+      int32_t c[UL];
+#pragma unroll
+      for (int k = 0; k < UL; ++k) {
+        a[k] = ld_stream_f64(pa + 32 * k, pol_stream);
+        c[k] = ld_stream_s32(pc + 32 * k, pol_stream);
+      }
+#pragma unroll
+      for (int k = 0; k < UL; ++k)
+        ld_snap_keep(A.snap + (c[k] & 0x7fffffff), pol_keep, lo[k], up[k], q[k]);
+#pragma unroll
+      for (int k = 0; k < UL; ++k)
+        sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xmax, pw + 32 * k);
+      pa += 32 * UL;
+      pc += 32 * UL;
+      pw += 32 * UL;
+    }
+    for (; t < steps; ++t) {
+      const double a1 = ld_stream_f64(pa, pol_stream);
+      const int32_t c1 = ld_stream_s32(pc, pol_stream);
+      double lo1, up1, q1;
+      ld_snap_keep(A.snap + (c1 & 0x7fffffff), pol_keep, lo1, up1, q1);
+      sell_step<LG>(a1, lo1, up1, q1, u, act, xmax, pw);
+      pa += 32;
+      pc += 32;
+      pw += 32;
+    }
+  } else {
+    // worklist rounds: only the marked units' entries
+    for (int t0 = 0; t0 < steps; t0 += kSellUnroll) {
+      double a[kSellUnroll], lo[kSellUnroll], up[kSellUnroll], q[kSellUnroll];
+      int32_t c[kSellUnroll];
+      bool in[kSellUnroll];
+#pragma unroll
+      for (int k = 0; k < kSellUnroll; ++k) {
+        in[k] = ((t0 + k) << LG) + j < len;
+        a[k] = 0.0;
+        c[k] = A.pad_col;
+        if (in[k]) {
+          a[k] = ld_stream_f64(sv + 32 * (t0 + k), pol_stream);
+          c[k] = ld_stream_s32(sc + 32 * (t0 + k), pol_stream);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kSellUnroll; ++k)
+        ld_snap_keep(A.snap + (c[k] & 0x7fffffff), pol_keep, lo[k], up[k], q[k]);
+#pragma unroll
+      for (int k = 0; k < kSellUnroll; ++k)
+        if (t0 + k < steps) sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xmax, sw + 32 * (t0 + k));
+    }
+  }
+  // order-free parts over the unit's lanes
+#pragma unroll
+  for (int o = H; o < 32; o <<= 1) {
+    act.min_i += __shfl_xor_sync(0xffffffffu, act.min_i, o);
+    act.max_i += __shfl_xor_sync(0xffffffffu, act.max_i, o);
+    xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+  }
+
+  // ---- row finish (owner lanes) ----------------------------------------------------
+  bool may = false;
+  if (j == 0 && active) {
+    if (whole) {
+      const int r = ud.ref;
+      const double l = A.lhs[r], h = A.rhs[r];
+      if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
+      const RowFilter f = row_filter(act, l, h);
+      may = row_may(f, xmax);
+      W.min_f[u] = act.min_f;
+      W.max_f[u] = act.max_f;
+      W.min_i[u] = act.min_i;
+      W.max_i[u] = act.max_i;
+      W.lhs[u] = l;
+      W.rhs[u] = h;
+      W.tr[u] = f.tr;
+      W.tl[u] = f.tl;
+      W.mode[u] = f.mode;
+    } else {
+      // a chunk of a split row: partial record; the last chunk combines them
+      const SegDesc d = A.segs[-ud.ref - 1];
+      volatile SegPartial* P = A.partial + d.out;
+      P->min_f = act.min_f;
+      P->max_f = act.max_f;
+      P->xmax = xmax;
+      P->min_i = act.min_i;
+      P->max_i = act.max_i;
+      __threadfence();
+      const int nch = A.sfirst[d.rslot + 1] - A.sfirst[d.rslot];
+      if (atomicAdd(&A.row_done[d.rslot], 1) == nch - 1) {
+        __threadfence();
+        A.row_done[d.rslot] = 0;
+        finish_split_row<kRowCheck>(A, d.rslot, inf_flag, cfg);
+      }
+    }
+  }
+  if (j == 0) W.may[u] = may;
+  if (!__any_sync(0xffffffffu, may)) return;
+
+  // ---- phase 2: filter words -> queue -> exact pipeline ------------------------------
+  __syncwarp();
+  const bool umay = W.may[u] != 0;
+  RowFilter f = {0.0, 0.0, 0};
+  if (umay) f = RowFilter{W.tr[u], W.tl[u], W.mode[u]};
+  int qn = 0;
+  for (int t0 = 0; t0 < steps; t0 += kSellUnroll) {
+    uint32_t b[kSellUnroll];
+    bool in[kSellUnroll];
+#pragma unroll
+    for (int k = 0; k < kSellUnroll; ++k) {
+      in[k] = umay && ((t0 + k) << LG) + j < len;
+      b[k] = in[k] ? sw[32 * (t0 + k)] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kSellUnroll; ++k) {
+      const bool pass = in[k] && filt_may(f, b[k]);
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (!m) continue;
+      if (pass) {
+        const int slot = qn + __popc(m & ((1u << lane) - 1u));
+        W.qe[slot] = 32 * (t0 + k) + lane;
+        W.qu[slot] = (uint8_t)u;
+      }
+      qn += __popc(m);
+      if (qn >= 32) {
+        __syncwarp();
+        inf_flag |= sell_drain(A, W, sd.off, 32, lane, pol_keep, cfg);
+        __syncwarp();
+        qn -= 32;
+        if (lane < qn) {
+          W.qe[lane] = W.qe[32 + lane];
+          W.qu[lane] = W.qu[32 + lane];
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (qn) {
+    __syncwarp();
+    inf_flag |= sell_drain(A, W, sd.off, qn, lane, pol_keep, cfg);
+  }
+  __syncwarp();
+}
+
+// Persistent, one warp per slice (longest first).  kDense: a full sweep;
+// otherwise a worklist round (only the marked rows' units).  Both are
+// launched when the worklist is on; the one that does not match the round
+// returns at once (the round's kind is known on the device only).
+template <bool kRowCheck, bool kDense>
+__global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const RoundArgs A,
+                                                                     const DevCfg cfg) {
+  __shared__ SellWarpSmem smem[kSellWarps];
+  const int lane = threadIdx.x & 31;
+  SellWarpSmem& W = smem[threadIdx.x >> 5];
+  const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
+  if (full != kDense) return;
+  const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
+  const uint8_t* rflag = A.dirty.row_flag + (size_t)par * A.dirty.ms;
+  const uint64_t pk = l2_policy_evict_last();
+  const uint64_t ps = l2_policy_evict_first();
+  bool inf_flag = false;
+  int next = 0;
+  if (lane == 0) next = atomicAdd(&A.st->work, 1);
+  next = __shfl_sync(0xffffffffu, next, 0);
+  while (next < A.nslices) {
+    const int s = next;
+    if (lane == 0) next = atomicAdd(&A.st->work, 1);
+    next = __shfl_sync(0xffffffffu, next, 0);
+    const SliceDesc sd = A.slices[s];
+#if PG_SELL_LGMAX >= 3
+    if (sd.lg == 3) {
+      sell_slice<kRowCheck, 3, kDense>(A, W, sd, lane, full, rflag, pk, ps, inf_flag, cfg);
+      continue;
+    }
+#endif
+#if PG_SELL_LGMAX >= 2
+    if (sd.lg == 2) {
+      sell_slice<kRowCheck, 2, kDense>(A, W, sd, lane, full, rflag, pk, ps, inf_flag, cfg);
+      continue;
+    }
+#endif
+#if PG_SELL_LGMAX >= 1
+    if (sd.lg == 1) {
+      sell_slice<kRowCheck, 1, kDense>(A, W, sd, lane, full, rflag, pk, ps, inf_flag, cfg);
+      continue;
+    }
+#endif
+    sell_slice<kRowCheck, 0, kDense>(A, W, sd, lane, full, rflag, pk, ps, inf_flag, cfg);
+  }
+  if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
+}
+
+// ---- session setup: units, slices, the sliced-ELL copy ---------------------------
+
+// every chain as a unit: the segments (a segment that is a whole row becomes
+// a row unit), then the short rows; key = descending length
+__global__ void k_make_units(const SegDesc* __restrict__ segs, int nseg,
+                             const int32_t* __restrict__ srow, const int32_t* __restrict__ sfirst,
+                             const TileLayout lay, const int32_t* __restrict__ row_ptr,
+                             int nunits, int maxlen, UnitDesc* __restrict__ units,
+                             int32_t* __restrict__ k0, uint32_t* __restrict__ key,
+                             int32_t* __restrict__ idx) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nunits; u += gridDim.x * blockDim.x) {
+    UnitDesc d;
+    if (u < nseg) {
+      const SegDesc g = segs[u];
+      const bool whole = sfirst[g.rslot + 1] - sfirst[g.rslot] == 1;
+      d = UnitDesc{g.len, whole ? srow[g.rslot] : -(u + 1)};
+      k0[u] = g.k0;
+    } else {
+      int i = u - nseg, L = lay.nclass - 1;
+      while (L > 0 && i >= lay.class_start[L + 1] - lay.class_start[L]) {
+        i -= lay.class_start[L + 1] - lay.class_start[L];
+        --L;
+      }
+      const int r = lay.class_start[L] + i;
+      d = UnitDesc{L, r};
+      k0[u] = row_ptr[r];
+    }
+    units[u] = d;
+    key[u] = (uint32_t)(maxlen - d.len);
+    idx[u] = u;
+  }
+}
+
+// units and their CSR starts into sorted order
+__global__ void k_order_units(const UnitDesc* __restrict__ in, const int32_t* __restrict__ k0in,
+                              const int32_t* __restrict__ order, int nunits,
+                              UnitDesc* __restrict__ out, int32_t* __restrict__ k0out) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nunits; u += gridDim.x * blockDim.x) {
+    out[u] = in[order[u]];
+    k0out[u] = k0in[order[u]];
+  }
+}
+
+// lanes per unit: by length, and at least 2^lg_min (small instances: more
+// lanes per unit, shorter chains, enough warps to fill the GPU)
+__host__ __device__ inline int sell_lg(int len, int lg_min) {
+  const int lg = len > kSellG8 ? 3 : len > kSellG4 ? 2 : len > kSellG2 ? 1 : 0;
+  return lg > lg_min ? lg : lg_min;
+}
+
+// region ends: cnt[lg] = one past the last unit with lanes-per-unit 2^lg
+// (units sorted by descending length; cnt must start zeroed)
+__global__ void k_unit_regions(const UnitDesc* __restrict__ units, int nunits, int lg_min,
+                               int32_t* __restrict__ cnt) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nunits; u += gridDim.x * blockDim.x) {
+    const int lg = sell_lg(units[u].len, lg_min);
+    if (u + 1 == nunits || sell_lg(units[u + 1].len, lg_min) != lg) cnt[lg] = u + 1;
+  }
+}
+
+struct SellRegions {
+  int32_t ustart[5];  // first unit of region k (lg = 3 - k), + end
+  int32_t sstart[5];  // first slice of region k, + total
+};
+
+// per slice: first unit, count, width, steps; elements for the scan
+__global__ void k_slice_desc(const UnitDesc* __restrict__ units, const SellRegions R,
+                             SliceDesc* __restrict__ slices, long long* __restrict__ elems) {
+  const int nslices = R.sstart[4];
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s <= nslices; s += gridDim.x * blockDim.x) {
+    if (s == nslices) {
+      elems[s] = 0;
+      continue;
+    }
+    int k = 0;
+    while (k < 3 && s >= R.sstart[k + 1]) ++k;
+    const int lg = 3 - k, H = 32 >> lg;
+    const int first = R.ustart[k] + (s - R.sstart[k]) * H;
+    const int count = min(H, R.ustart[k + 1] - first);
+    const int width = units[first].len;  // sorted descending
+    const int steps = (width + (1 << lg) - 1) >> lg;
+    const bool uniform = lg == 0 && count == H && units[first + count - 1].len == width;
+    slices[s] = SliceDesc{0, first, width, steps, (int16_t)count, (int8_t)lg, (int8_t)uniform};
+    elems[s] = 32LL * steps;
+  }
+}
+
+// the transposed copy (padding: value 0 in the padding column, bounds [0, 0])
+__global__ void k_fill_sell(const UnitDesc* __restrict__ units, const int32_t* __restrict__ k0,
+                            int nslices, const long long* __restrict__ off,
+                            const double* __restrict__ vals, const int32_t* __restrict__ colx,
+                            int32_t pad_col, SliceDesc* __restrict__ slices,
+                            double* __restrict__ sv, int32_t* __restrict__ sc) {
+  const int lane = threadIdx.x & 31;
+  for (int s = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; s < nslices;
+       s += (gridDim.x * blockDim.x) >> 5) {
+    const long long o = off[s];
+    SliceDesc d = slices[s];
+    const int lg = d.lg, H = 32 >> lg;
+    const int j = lane >> (5 - lg), u = lane & (H - 1);
+    const int len = u < d.count ? units[d.first + u].len : 0;
+    const int b = u < d.count ? k0[d.first + u] : 0;
+    for (int t = 0; t < d.steps; ++t) {
+      const int i = (t << lg) + j;
+      sv[o + 32LL * t + lane] = i < len ? vals[b + i] : 0.0;
+      sc[o + 32LL * t + lane] = i < len ? colx[b + i] : pad_col;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      d.off = o;
+      slices[s] = d;
+    }
+  }
+}
+
+}  // namespace pgb

@@ -1,4 +1,4 @@
-// setup.cuh -- device-side session setup (row order, tiles, segments).
+// setup.cuh -- device-side session setup (row order, segments).
 //
 // Untimed in the reference's protocol (its initialisation -- partition,
 // working copies, pool -- is excluded from `elapsed`), but part of the
@@ -30,12 +30,9 @@ __global__ void k_sorted_len(const int32_t* __restrict__ rp, const int32_t* __re
 
 constexpr int kMaxClasses = kShortMax + 2;
 struct TileLayout {
-  int32_t nclass;                   // short_max + 1 length classes 0..short_max
-  int32_t class_start[kMaxClasses];  // first sorted row of class L
-  int32_t tile_off[kMaxClasses];     // first tile of class L (+ total at nclass)
+  int32_t nclass;                    // short_max + 1 length classes 0..short_max
+  int32_t class_start[kMaxClasses];  // first sorted row of class L (+ end at nclass)
 };
-
-__device__ __forceinline__ int tile_cap(int L) { return L ? min(32, kWNnz / L) : 32; }
 
 // rows per length class
 __global__ void k_class_counts(const uint8_t* __restrict__ key, int m, int32_t* __restrict__ counts) {
@@ -47,21 +44,6 @@ __global__ void k_class_counts(const uint8_t* __restrict__ key, int m, int32_t* 
   __syncthreads();
   for (int c = threadIdx.x; c < kMaxClasses; c += blockDim.x)
     if (h[c]) atomicAdd(&counts[c], h[c]);
-}
-
-// warp tiles: class L's rows in runs of tile_cap(L) consecutive rows
-__global__ void k_make_tiles(const TileLayout lay, const int32_t* __restrict__ srp,
-                             TileDesc* __restrict__ tiles) {
-  const int total = lay.tile_off[lay.nclass];
-  for (int t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
-    int L = 0;
-    while (L + 1 < lay.nclass && lay.tile_off[L + 1] <= t) ++L;
-    const int cap = tile_cap(L);
-    const int r0 = lay.class_start[L] + (t - lay.tile_off[L]) * cap;
-    const int end = lay.class_start[L + 1];
-    const int nr = min(cap, end - r0);
-    tiles[t] = TileDesc{r0, nr, srp[r0], nr * L};
-  }
 }
 
 // chunks per segment row (rows [first, m) of the sorted order)
@@ -99,25 +81,11 @@ __global__ void k_emit_segs(const int32_t* __restrict__ srp, const int32_t* __re
   }
 }
 
-// segments into descending-length order; chunk -> sorted position
+// segments into descending-length order
 __global__ void k_order_segs(const SegDesc* __restrict__ in, const int32_t* __restrict__ order,
-                             int nseg, SegDesc* __restrict__ out, int32_t* __restrict__ chunk_seg,
-                             int32_t* __restrict__ nlong) {
-  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nseg; q += gridDim.x * blockDim.x) {
-    const SegDesc d = in[order[q]];
-    out[q] = d;
-    chunk_seg[d.out] = q;
-    if (d.len > kLongSeg && (q + 1 == nseg || in[order[q + 1]].len <= kLongSeg)) *nlong = q + 1;
-  }
-}
-
-// groups: 8 segments while they are long (short per-group critical path),
-// then 32
-__global__ void k_make_groups(int nseg, int n8, int ngroups, SegGroup* __restrict__ groups) {
-  for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ngroups; g += gridDim.x * blockDim.x) {
-    const int first = g < n8 ? 8 * g : 8 * n8 + 32 * (g - n8);
-    groups[g] = SegGroup{first, min(g < n8 ? 8 : 32, nseg - first)};
-  }
+                             int nseg, SegDesc* __restrict__ out) {
+  for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < nseg; q += gridDim.x * blockDim.x)
+    out[q] = in[order[q]];
 }
 
 }  // namespace pgb

@@ -93,8 +93,8 @@ def partition_row_blocks(instance: ProblemInstance, cfg: EngineConfig | None = N
 class Session:
     """One problem resident on the device (pg_session_*)."""
 
-    INFO_FIELDS = ("m", "n", "nnz", "num_tiles", "seg_rows", "segments", "tile_rows", "tile_nnz",
-                   "seg_nnz")
+    INFO_FIELDS = ("m", "n", "nnz", "slices", "seg_rows", "segments", "short_rows", "short_nnz",
+                   "seg_nnz", "chains", "sell_elems")
 
     def __init__(self, instance: ProblemInstance, cfg: EngineConfig | None = None):
         self.cfg = cfg or EngineConfig()

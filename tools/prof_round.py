@@ -14,7 +14,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--solve", action="store_true")
 ap.add_argument("--host-loop", action="store_true")
-ap.add_argument("--debug-flags", type=int, default=0)
+ap.add_argument("--debug-flags", type=lambda x: int(x, 0), default=0)
 ap.add_argument("--worklist", action="store_true")
 a = ap.parse_args()
 inst = G.config_instance(a.config)
@@ -31,6 +31,16 @@ if a.debug_flags:
     ns, b = C.c_double(), C.c_double()
     abi.check(lib.pg_session_time_round_kernel(h, a.reps, C.byref(ns), C.byref(b)), "time")
     print(f"k_round {ns.value/1e3:.1f} us (debug flags {a.debug_flags:#x})")
+    if a.solve:
+        from paper_2009_07785_b200.engine import new_c_result
+        best = None
+        for _ in range(3):
+            r, lo, up, prc = new_c_result(inst.num_cols(), cfg.round_limit)
+            r.lower = C.cast(None, C.POINTER(C.c_double))
+            r.upper = C.cast(None, C.POINTER(C.c_double))
+            abi.check(lib.pg_session_run(h, C.byref(r)), "run")
+            best = r.elapsed_ns if best is None else min(best, r.elapsed_ns)
+        print(f"solve status={r.status} rounds={r.rounds_executed} best={best/1e6:.3f} ms")
     sys.exit(0)
 with Session(inst, cfg) as s:
     print(s.info())
