@@ -224,7 +224,9 @@ def bench_single(args, inst, world, rank, local):
     from paper_2009_07785_b200.engine import Session, propagate_gpu
     from paper_2009_07785_b200.model import EngineConfig
 
-    cfg = EngineConfig(device=local, worklist=args.worklist)
+    from paper_2009_07785_b200.model import LoopMode
+    cfg = EngineConfig(device=local, worklist=args.worklist,
+                       loop_mode=LoopMode.Host if args.loop == "host" else LoopMode.Graph)
     m, n, nnz = inst.num_rows(), inst.num_cols(), inst.matrix.nnz()
     sess = Session(inst, cfg)
     info = sess.info()
@@ -421,6 +423,9 @@ def main():
     ap.add_argument("--nodes", type=int, default=8192, help="C4: number of B&B nodes")
     ap.add_argument("--worklist", type=int, default=0, help="device-side worklist (exact)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--loop", default="graph", choices=["graph", "host"],
+                    help="host: one launch per kernel per round (for ncu launch lists: ncu "
+                         "cannot profile kernel nodes of graphs with conditional nodes)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)

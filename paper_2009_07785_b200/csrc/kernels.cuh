@@ -251,7 +251,7 @@ struct CandItem {
   int32_t pad;
 };
 constexpr int kCandShort = 32;    // rows up to this length: batched 32 per warp
-constexpr int kCandPiece = 1024;  // longer rows: one warp per piece
+constexpr int kCandPiece = 128;   // longer rows: one warp per piece (one pass of 4 x 32)
 
 struct RoundArgs {
   // phase 1: chains over the sliced-ELL copy

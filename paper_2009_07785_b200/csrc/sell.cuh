@@ -42,6 +42,9 @@ namespace pgb {
 #ifndef PG_SELL_PF
 #define PG_SELL_PF 1
 #endif
+#ifndef PG_SELL_DEBUG
+#define PG_SELL_DEBUG 0  // 1: cfg.flags 0x10000 skips phase 2 (timing experiments)
+#endif
 #ifndef PG_SELL_LGU
 #define PG_SELL_LGU 2  // slices with lg >= this use PG_SELL_ULONG steps per group
 #endif
@@ -225,24 +228,45 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
     const int32_t* pc = sc;
     uint32_t* pw = sw;
     int t = 0;
-    for (; t + UL <= steps; t += UL) {
-      if (PG_SELL_PF && lane == 0 && t + 5 * UL <= steps) {
-        prefetch_l2(pa + 32 * 4 * UL, 256u * UL);
-        prefetch_l2(pc + 32 * 4 * UL, 128u * UL);
-      }
-      double a[UL], lo[UL], up[UL], q[UL];
-      int32_t c[UL];
+    double a[UL];
+    int32_t c[UL];
+    if (UL <= steps) {
 #pragma unroll
       for (int k = 0; k < UL; ++k) {
         a[k] = ld_stream_f64(pa + 32 * k, pol_stream);
         c[k] = ld_stream_s32(pc + 32 * k, pol_stream);
       }
+    }
+    for (; t + UL <= steps; t += UL) {
+      if (PG_SELL_PF && lane == 0 && t + 5 * UL <= steps) {
+        prefetch_l2(pa + 32 * 4 * UL, 256u * UL);
+        prefetch_l2(pc + 32 * 4 * UL, 128u * UL);
+      }
+      double lo[UL], up[UL], q[UL];
 #pragma unroll
       for (int k = 0; k < UL; ++k)
         ld_snap_keep(A.snap + (c[k] & 0x7fffffff), pol_keep, lo[k], up[k], q[k]);
+      // the next group's values and columns are in flight during this one
+      double an[UL];
+      int32_t cn[UL];
+      const bool more = t + 2 * UL <= steps;
+#pragma unroll
+      for (int k = 0; k < UL; ++k) {
+        an[k] = 0.0;
+        cn[k] = 0;
+        if (more) {
+          an[k] = ld_stream_f64(pa + 32 * (UL + k), pol_stream);
+          cn[k] = ld_stream_s32(pc + 32 * (UL + k), pol_stream);
+        }
+      }
 #pragma unroll
       for (int k = 0; k < UL; ++k)
         sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xmax, pw + 32 * k);
+#pragma unroll
+      for (int k = 0; k < UL; ++k) {
+        a[k] = an[k];
+        c[k] = cn[k];
+      }
       pa += 32 * UL;
       pc += 32 * UL;
       pw += 32 * UL;
@@ -326,6 +350,7 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
     }
   }
   if (j == 0) W.may[u] = may;
+  if (PG_SELL_DEBUG && (cfg.flags & 0x10000u)) return;  // timing experiments only: no phase 2
   if (!__any_sync(0xffffffffu, may)) return;
 
   // ---- phase 2: filter words -> queue -> exact pipeline ------------------------------
