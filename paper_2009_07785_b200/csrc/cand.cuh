@@ -108,8 +108,8 @@ __device__ __forceinline__ bool cand_entry(const RoundArgs& A, const CandWarpSme
   return entry_may(f, fabs(a) * q, isinf(bmin), isinf(bmax));
 }
 
-__global__ void __launch_bounds__(kCandThreads) k_cand(const RoundArgs A, const DevCfg cfg) {
-  __shared__ CandWarpSmem smem[kCandWarps];
+__device__ __forceinline__ void cand_sweep(const RoundArgs& A, const DevCfg& cfg,
+                                           CandWarpSmem* smem) {
   const int lane = threadIdx.x & 31;
   CandWarpSmem& W = smem[threadIdx.x >> 5];
   const int nlong = *((volatile int32_t*)&A.st->wl_long);
@@ -197,6 +197,11 @@ __global__ void __launch_bounds__(kCandThreads) k_cand(const RoundArgs A, const 
     __syncwarp();
   }
   if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
+}
+
+__global__ void __launch_bounds__(kCandThreads) k_cand(const RoundArgs A, const DevCfg cfg) {
+  __shared__ CandWarpSmem smem[kCandWarps];
+  cand_sweep(A, cfg, smem);
 }
 
 }  // namespace pgb

@@ -43,6 +43,8 @@
 #include "setup.cuh"
 #include "sell.cuh"
 #include "cand.cuh"
+#include "loop.cuh"
+#include "nodes.cuh"
 
 using namespace pgb;
 
@@ -198,6 +200,9 @@ struct pg_session {
   int num_sms = 148;
   int sell_per_sm = 1;   // resident k_sell CTAs per SM
   int cand_per_sm = 1;   // resident k_cand CTAs per SM
+  int loop_grid = 0;     // co-resident CTAs of the persistent loop kernel
+  int nodes_per_sm = 1;  // resident k_nodes CTAs per SM
+  int32_t max_row_len = 0;
 
   // device arrays
   int32_t* d_row_ptr = nullptr;
@@ -226,7 +231,7 @@ struct pg_session {
   double* d_sv = nullptr;
   int32_t* d_sc = nullptr;
   uint32_t* d_sw = nullptr;
-  int32_t nunits = 0, nslices = 0, lg_min = 0;
+  int32_t nunits = 0, nslices = 0, lg_min = 0, group_start = 0;
   int64_t sell_elems = 0;
   DevState* d_st = nullptr;
   long long* d_per_round = nullptr;
@@ -287,6 +292,7 @@ struct pg_session {
     RoundArgs A;
     A.slices = d_slices;
     A.nslices = nslices;
+    A.group_start = group_start;
     A.nunits = nunits;
     A.units = d_units;
     A.sv = d_sv;
@@ -359,8 +365,77 @@ struct pg_session {
     PG_CUDA(cudaGetLastError());
   }
 
+  // column -> rows index over the sorted rows (device counting sort);
+  // used by the worklist marks and the batched branch-and-bound nodes
+  void ensure_col_index() {
+    if (d_col_ptr) return;
+    cudaStream_t st = stream;
+    t_alloc_stream = st;
+    d_col_ptr = dalloc<int32_t>((size_t)n + 1);
+    d_col_item = dalloc<int32_t>(nnz);
+    int32_t* cnt = dalloc<int32_t>((size_t)n + 1);
+    PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)n + 1), st));
+    if (m) k_csc_count<<<grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(d_row_ptr, d_colx, m, cnt);
+    size_t tmp_bytes = 0;
+    PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, d_col_ptr, n + 1, st));
+    void* tmp = dalloc<unsigned char>(tmp_bytes);
+    PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, d_col_ptr, n + 1, st));
+    PG_CUDA(cudaMemcpyAsync(cnt, d_col_ptr, sizeof(int32_t) * ((size_t)n + 1),
+                            cudaMemcpyDeviceToDevice, st));
+    if (m) k_csc_fill<<<grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(d_row_ptr, d_colx, m, cnt,
+                                                                         d_col_item);
+    PG_CUDA(cudaGetLastError());
+    PG_CUDA(cudaStreamSynchronize(st));
+    dfree(tmp);
+    dfree(cnt);
+    dirty.col_ptr = d_col_ptr;
+    dirty.col_row = d_col_item;
+  }
+
+  // persistent round loop (loop.cuh): small instances and worklist solves,
+  // whose rounds are launch-latency bound; never with a communicator (the
+  // all-reduce is a host-enqueued NCCL call between phases)
+  bool use_persistent() const {
+    if (comm || loop_grid <= 0) return false;
+    static const long long thr = [] {
+      const char* e = getenv("PG_PERSIST_NNZ");
+      return e ? atoll(e) : 8000000LL;
+    }();
+    return nnz <= thr || dirty.enabled;
+  }
+
+  void enqueue_persistent() {
+    const RoundArgs A = round_args();
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(loop_grid);
+    lc.blockDim = dim3(kSellThreads);
+    lc.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    Snap* snap = d_snap;
+    long long* pr = d_per_round;
+    int nn = n;
+    if (cfg.flags & PG_FLAG_ROWCHECK)
+      PG_CUDA(cudaLaunchKernelEx(&lc, k_loop<true>, A, dcfg, snap, nn, pr));
+    else
+      PG_CUDA(cudaLaunchKernelEx(&lc, k_loop<false>, A, dcfg, snap, nn, pr));
+  }
+
   void build_graph() {
     PG_CUDA(cudaGraphCreate(&graph, 0));
+    if (use_persistent()) {
+      PG_CUDA(cudaStreamBeginCaptureToGraph(stream, graph, nullptr, nullptr, 0,
+                                            cudaStreamCaptureModeThreadLocal));
+      enqueue_reset(false, true);
+      enqueue_persistent();
+      cudaGraph_t g2 = nullptr;
+      PG_CUDA(cudaStreamEndCapture(stream, &g2));
+      PG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
+      return;
+    }
     PG_CUDA(cudaGraphConditionalHandleCreate(&cond, graph, 1, cudaGraphCondAssignDefault));
     // node 1: reset (+ warm-start marks), captured
     cudaGraphNode_t reset_node = nullptr;
@@ -487,10 +562,21 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
                                                           kSellThreads, 0));
     s->sell_per_sm = std::max(1, s->sell_per_sm);
     PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->cand_per_sm, k_cand, kCandThreads, 0));
+    {
+      int per = 0;
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_loop<true>, kSellThreads, 0));
+      int per2 = 0;
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_loop<false>, kSellThreads, 0));
+      s->loop_grid = std::min(per, per2) * s->num_sms;
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_nodes<true>, kNodeThreads, 0));
+      s->nodes_per_sm = std::max(1, per);
+    }
     s->cand_per_sm = std::max(1, s->cand_per_sm);
 
     s->m = p->num_rows;
     s->n = p->num_cols;
+    for (int32_t i = 0; i < p->num_rows; ++i)
+      s->max_row_len = std::max(s->max_row_len, p->row_ptr[i + 1] - p->row_ptr[i]);
     s->nnz = p->nnz;
     s->cfg = *cfg;
     s->dcfg.inf_thr = cfg->infinity_threshold;
@@ -682,9 +768,9 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       uint32_t* ukey2 = dalloc<uint32_t>(nu);
       int32_t* uidx = dalloc<int32_t>(nu);
       int32_t* uord = dalloc<int32_t>(nu);
-      int32_t* rcnt = dalloc<int32_t>(4);
+      int32_t* rcnt = dalloc<int32_t>(5);
       s->d_units = dalloc<UnitDesc>(nu);
-      PG_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(int32_t) * 4, st));
+      PG_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(int32_t) * 5, st));
       k_make_units<<<s->grid_for(nu, 256), 256, 0, st>>>(s->d_segs, s->nseg, s->d_srow, s->d_sfirst,
                                                            lay, s->d_row_ptr, nu, chunk, u_in, k0_in,
                                                            ukey, uidx);
@@ -702,7 +788,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       while (lg_min < 3 && ((int64_t)nu << lg_min) < resident * 32) ++lg_min;
       s->lg_min = lg_min;
       k_unit_regions<<<s->grid_for(nu, 256), 256, 0, st>>>(s->d_units, nu, lg_min, rcnt);
-      int32_t hc[4] = {0, 0, 0, 0};
+      int32_t hc[5] = {0, 0, 0, 0, 0};
       PG_CUDA(cudaMemcpyAsync(hc, rcnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
       PG_CUDA(cudaStreamSynchronize(st));
       SellRegions R{};
@@ -717,6 +803,13 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         R.sstart[k + 1] = R.sstart[k] + (R.ustart[k + 1] - R.ustart[k] + H - 1) / H;
       }
       s->nslices = R.sstart[4];
+      // narrow one-lane slices are handed out in groups (sell_group): the
+      // first slice of region 0 whose units are all <= PG_SELL_GROUPW long
+      s->group_start = s->nslices;
+      if (R.ustart[4] > R.ustart[3]) {
+        const int ub = std::max(hc[4], R.ustart[3]);  // first unit <= the grouping width
+        s->group_start = std::min(s->nslices, R.sstart[3] + (ub - R.ustart[3] + 31) / 32);
+      }
       s->d_slices = dalloc<SliceDesc>(s->nslices);
       long long* elems = dalloc<long long>((size_t)s->nslices + 1);
       long long* soff = dalloc<long long>((size_t)s->nslices + 1);
@@ -759,26 +852,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       if (D.enabled) {
         s->d_chg = dalloc<int32_t>(2 * (size_t)n);
         D.chg_list = s->d_chg;
-        s->d_col_ptr = dalloc<int32_t>((size_t)n + 1);
-        s->d_col_item = dalloc<int32_t>(nnz);
-        int32_t* cnt = dalloc<int32_t>((size_t)n + 1);
-        PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)n + 1), st));
-        if (m) k_csc_count<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
-            s->d_row_ptr, s->d_colx, m, cnt);
-        size_t tmp_bytes = 0;
-        PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, s->d_col_ptr, n + 1, st));
-        void* tmp = dalloc<unsigned char>(tmp_bytes);
-        PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, s->d_col_ptr, n + 1, st));
-        PG_CUDA(cudaMemcpyAsync(cnt, s->d_col_ptr, sizeof(int32_t) * ((size_t)n + 1),
-                                cudaMemcpyDeviceToDevice, st));
-        if (m) k_csc_fill<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
-            s->d_row_ptr, s->d_colx, m, cnt, s->d_col_item);
-        PG_CUDA(cudaGetLastError());
-        PG_CUDA(cudaStreamSynchronize(st));
-        dfree(tmp);
-        dfree(cnt);
-        D.col_ptr = s->d_col_ptr;
-        D.col_row = s->d_col_item;
+        s->ensure_col_index();
       }
     }
     s->upload_bounds(p->lower, p->upper);
@@ -1076,6 +1150,109 @@ int pg_session_propagate_nodes(pg_session* s, int32_t K, const int32_t* node_ptr
                         d_up + node_ptr[k]};
     if (K) PG_CUDA(cudaMemcpyAsync(d_ctls, ctls.data(), sizeof(NodeCtl) * K, cudaMemcpyHostToDevice, st));
     const size_t n = (size_t)s->n;
+    if (!getenv("PG_NODES_SERIAL")) {
+      // batched: one CTA per node, many nodes at once (nodes.cuh)
+      s->ensure_col_index();
+      const size_t m = (size_t)s->m;
+      const int chunk = s->cfg.nnz_budget;
+      const int maxc = s->max_row_len > chunk ? (s->max_row_len + chunk - 1) / chunk : 1;
+      const size_t per_slot = n * 44 + m * 12 + (size_t)kNodeThreads * maxc * sizeof(Act);
+      size_t free_b = 0, total_b = 0;
+      PG_CUDA(cudaMemGetInfo(&free_b, &total_b));
+      const size_t cap = std::max<size_t>(1, (free_b / 3) / std::max<size_t>(per_slot, 1));
+      const int slots = (int)std::max<size_t>(1, std::min<size_t>(
+          {(size_t)std::max(K, 1), (size_t)s->nodes_per_sm * s->num_sms, cap}));
+      double* s_lo = dalloc<double>(n * slots);
+      double* s_up = dalloc<double>(n * slots);
+      longlong2* s_key = dalloc<longlong2>(n * slots);
+      int32_t* s_cflag = dalloc<int32_t>(n * slots);
+      int32_t* s_touch = dalloc<int32_t>(n * slots);
+      int32_t* s_undo = dalloc<int32_t>(n * slots);
+      int32_t* s_rflag = dalloc<int32_t>(m * slots);
+      int32_t* s_rows = dalloc<int32_t>(2 * m * slots);
+      Act* s_part = dalloc<Act>((size_t)slots * kNodeThreads * maxc);
+      int32_t* d_res = dalloc<int32_t>(2 * (size_t)K + 1);
+      // bound vectors, when asked for, in batches of at most ~1 GiB
+      const bool want = lower_out || upper_out;
+      const int32_t kb = want ? std::max<int32_t>(1, (int32_t)std::min<size_t>(
+                                    K, (1ull << 30) / std::max<size_t>(16 * n, 1)))
+                              : std::max(K, 1);
+      double* d_blo = want ? dalloc<double>((size_t)kb * n) : nullptr;
+      double* d_bup = want ? dalloc<double>((size_t)kb * n) : nullptr;
+      std::vector<int32_t> hptr(node_ptr, node_ptr + K + 1);
+      int32_t* d_ptr = dalloc<int32_t>((size_t)K + 1);
+      PG_CUDA(cudaMemcpyAsync(d_ptr, hptr.data(), sizeof(int32_t) * (K + 1), cudaMemcpyHostToDevice, st));
+      PG_CUDA(cudaEventRecord(s->ev0, st));
+      for (int32_t b0 = 0; b0 < K; b0 += kb) {
+        const int32_t nb = std::min(kb, K - b0);
+        NodeArgs N;
+        N.row_ptr = s->d_row_ptr;
+        N.colx = s->d_colx;
+        N.vals = s->d_vals;
+        N.lhs = s->d_lhs;
+        N.rhs = s->d_rhs;
+        N.col_ptr = s->d_col_ptr;
+        N.col_row = s->d_col_item;
+        N.m = s->m;
+        N.n = s->n;
+        N.root_lo = s->d_root_lo;
+        N.root_up = s->d_root_up;
+        N.K = nb;
+        N.node_ptr = d_ptr + b0;
+        N.vars = d_vars;
+        N.nlo = d_lo;
+        N.nup = d_up;
+        N.status = d_res + b0;
+        N.rounds = d_res + K + b0;
+        N.lower_out = d_blo;
+        N.upper_out = d_bup;
+        N.ticket = d_res + 2 * K;
+        N.s_lo = s_lo;
+        N.s_up = s_up;
+        N.s_key = s_key;
+        N.s_cflag = s_cflag;
+        N.s_touch = s_touch;
+        N.s_undo = s_undo;
+        N.s_rflag = s_rflag;
+        N.s_rows = s_rows;
+        N.s_part = s_part;
+        N.maxc = maxc;
+        PG_CUDA(cudaMemsetAsync(N.ticket, 0, sizeof(int32_t), st));
+        const int grid = std::min(slots, std::max(nb, 1));
+        if (s->cfg.flags & PG_FLAG_ROWCHECK)
+          k_nodes<true><<<grid, kNodeThreads, 0, st>>>(N, s->dcfg);
+        else
+          k_nodes<false><<<grid, kNodeThreads, 0, st>>>(N, s->dcfg);
+        PG_CUDA(cudaGetLastError());
+        if (lower_out)
+          PG_CUDA(cudaMemcpyAsync(lower_out + (size_t)b0 * n, d_blo, sizeof(double) * n * nb,
+                                  cudaMemcpyDeviceToHost, st));
+        if (upper_out)
+          PG_CUDA(cudaMemcpyAsync(upper_out + (size_t)b0 * n, d_bup, sizeof(double) * n * nb,
+                                  cudaMemcpyDeviceToHost, st));
+      }
+      PG_CUDA(cudaEventRecord(s->ev1, st));
+      // the session's start bounds are the root fixpoint (as after serial nodes)
+      PG_CUDA(cudaMemcpyAsync(s->d_lo0, s->d_root_lo, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      PG_CUDA(cudaMemcpyAsync(s->d_up0, s->d_root_up, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+      std::vector<int32_t> res(2 * (size_t)K + 1);
+      if (K) PG_CUDA(cudaMemcpyAsync(res.data(), d_res, sizeof(int32_t) * 2 * K, cudaMemcpyDeviceToHost, st));
+      PG_CUDA(cudaStreamSynchronize(st));
+      float ms = 0.f;
+      PG_CUDA(cudaEventElapsedTime(&ms, s->ev0, s->ev1));
+      if (elapsed_ns) *elapsed_ns = (int64_t)((double)ms * 1e6);
+      for (int32_t k = 0; k < K; ++k) {
+        status[k] = res[k];
+        rounds[k] = res[K + k];
+      }
+      t_alloc_stream = st;
+      for (void* p : {(void*)s_lo, (void*)s_up, (void*)s_key, (void*)s_cflag, (void*)s_touch,
+                      (void*)s_undo, (void*)s_rflag, (void*)s_rows, (void*)s_part, (void*)d_res,
+                      (void*)d_blo, (void*)d_bup, (void*)d_ptr, (void*)d_vars, (void*)d_lo,
+                      (void*)d_up, (void*)d_ctls, (void*)d_out})
+        dfree(p);
+      return PG_OK;
+    }
     PG_CUDA(cudaEventRecord(s->ev0, st));
     for (int32_t k = 0; k < K; ++k) {
       // stream-ordered: root -> start bounds, overrides, warm control, solve

@@ -46,6 +46,8 @@ struct DevState {
   int32_t frac_any;                  // an integral column has a fractional start bound
   int32_t frac_tmp;                  // k_reset's accumulator of frac_any
   int32_t nchg[2];                   // changed-column list lengths, by round parity
+  uint32_t bar_count;                // grid barrier of the persistent round loop (loop.cuh)
+  uint32_t bar_gen;
 };
 
 // Device-side worklist (PG_FLAG_WORKLIST): a round only
@@ -257,6 +259,7 @@ struct RoundArgs {
   // phase 1: chains over the sliced-ELL copy
   const SliceDesc* slices;
   int32_t nslices;
+  int32_t group_start;    // first slice of the grouped narrow region (sell.cuh)
   int32_t nunits;
   const UnitDesc* units;
   const double* sv;
@@ -370,10 +373,11 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, in
 // Per variable (par_engine.cpp:191-197): count sides with out != in, flag
 // lo_out > up_out + abs, and write the next round's snapshot record.  The
 // last CTA takes the round decision of run_parallel (par_engine.cpp:248-266).
-__global__ void __launch_bounds__(kCommitThreads)
-    k_commit(Snap* __restrict__ snap, const longlong2* __restrict__ key_out, int n,
-             DevState* __restrict__ st, long long* __restrict__ per_round, const DevCfg cfg,
-             const Dirty D, cudaGraphConditionalHandle cond, int use_graph) {
+__device__ __forceinline__ void commit_body(Snap* __restrict__ snap,
+                                            const longlong2* __restrict__ key_out, int n,
+                                            DevState* __restrict__ st, long long* __restrict__ per_round,
+                                            const DevCfg& cfg, const Dirty& D,
+                                            cudaGraphConditionalHandle cond, int use_graph) {
   unsigned long long changes = 0;
   int inf = 0;
   const int R = *((volatile int32_t*)&st->round);  // rounds before this one
@@ -449,6 +453,13 @@ __global__ void __launch_bounds__(kCommitThreads)
       if (use_graph) cudaGraphSetConditional(cond, status >= 0 ? 0u : 1u);
     }
   }
+}
+
+__global__ void __launch_bounds__(kCommitThreads)
+    k_commit(Snap* __restrict__ snap, const longlong2* __restrict__ key_out, int n,
+             DevState* __restrict__ st, long long* __restrict__ per_round, const DevCfg cfg,
+             const Dirty D, cudaGraphConditionalHandle cond, int use_graph) {
+  commit_body(snap, key_out, n, st, per_round, cfg, D, cond, use_graph);
 }
 
 // Start of a solve: snapshot records and merge keys from the (normalised)
@@ -592,7 +603,7 @@ __global__ void k_apply_node(double* __restrict__ lo0, double* __restrict__ up0,
 
 // After the commit of round r: mark, for round r + 1, every row containing a
 // column changed in round r (one warp per changed column).
-__global__ void __launch_bounds__(256) k_mark(const Dirty D, DevState* __restrict__ st) {
+__device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__ st) {
   const int r = *((volatile int32_t*)&st->round);
   if (!D.enabled || *((volatile int32_t*)&st->done)) return;
   const int cb = r & 1, nb = (r + 1) & 1;
@@ -607,6 +618,9 @@ __global__ void __launch_bounds__(256) k_mark(const Dirty D, DevState* __restric
       if (!flag[row]) flag[row] = 1;  // read first: most rows are marked repeatedly
     }
   }
+}
+__global__ void __launch_bounds__(256) k_mark(const Dirty D, DevState* __restrict__ st) {
+  mark_body(D, st);
 }
 
 // ---- worklist index (session init) -----------------------------------------------

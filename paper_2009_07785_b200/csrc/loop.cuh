@@ -1,0 +1,68 @@
+// loop.cuh -- the whole round loop in one persistent kernel.
+//
+// For instances whose rounds are latency-bound (small matrices, and the
+// sparse worklist rounds of branch-and-bound nodes) three or four launches
+// per round cost more than the round itself.  k_loop runs run_parallel's
+// loop (par_engine.cpp:228-267) inside one cooperative launch: every CTA is
+// resident, and the phases of a round -- chains (sell.cuh), split-row
+// candidates (cand.cuh), commit + decision, worklist marks -- are separated
+// by grid barriers instead of kernel boundaries.  The phase bodies are the
+// same device functions the per-phase kernels run, so results are identical.
+#pragma once
+
+#include "cand.cuh"
+#include "sell.cuh"
+
+namespace pgb {
+
+// sense-free generation barrier over all CTAs of a cooperative launch
+__device__ __forceinline__ void grid_barrier(DevState* st) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile uint32_t* gen = &st->bar_gen;
+    const uint32_t g = *gen;
+    __threadfence();
+    if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
+      st->bar_count = 0;
+      __threadfence();
+      atomicAdd(&st->bar_gen, 1u);
+    } else {
+      while (*gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+union LoopSmem {
+  SellWarpSmem sell[kSellWarps];
+  CandWarpSmem cand[kCandWarps];
+};
+
+template <bool kRowCheck>
+__global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB)
+    k_loop(const RoundArgs A, const DevCfg cfg, Snap* __restrict__ snap, int n,
+           long long* __restrict__ per_round) {
+  __shared__ LoopSmem sm;
+  longlong2* key_out = reinterpret_cast<longlong2*>(A.key_out);
+  while (!*((volatile int32_t*)&A.st->done)) {
+    const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
+    if (full)
+      sell_sweep<kRowCheck, true>(A, cfg, sm.sell);
+    else
+      sell_sweep<kRowCheck, false>(A, cfg, sm.sell);
+    grid_barrier(A.st);
+    if (*((volatile int32_t*)&A.st->wl_long)) {
+      cand_sweep(A, cfg, sm.cand);
+      grid_barrier(A.st);
+    }
+    commit_body(snap, key_out, n, A.st, per_round, cfg, A.dirty, 0, 0);
+    grid_barrier(A.st);
+    if (A.dirty.enabled) {
+      mark_body(A.dirty, A.st);
+      grid_barrier(A.st);
+    }
+  }
+}
+
+}  // namespace pgb

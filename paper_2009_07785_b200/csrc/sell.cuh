@@ -42,6 +42,12 @@ namespace pgb {
 #ifndef PG_SELL_PF
 #define PG_SELL_PF 1
 #endif
+#ifndef PG_SELL_GROUP
+#define PG_SELL_GROUP 2  // narrow one-lane slices per work item
+#endif
+#ifndef PG_SELL_GROUPW
+#define PG_SELL_GROUPW 16  // slices at most this wide are grouped
+#endif
 #ifndef PG_SELL_DEBUG
 #define PG_SELL_DEBUG 0  // 1: cfg.flags 0x10000 skips phase 2 (timing experiments)
 #endif
@@ -60,6 +66,7 @@ namespace pgb {
 constexpr int kSellUnroll = PG_SELL_UNROLL;
 constexpr int kSellThreads = 256;
 constexpr int kSellWarps = kSellThreads / 32;
+constexpr int kSellGroup = PG_SELL_GROUP;
 // lanes per unit by unit length: > 256 -> 8, > 128 -> 4, > 64 -> 2, else 1
 constexpr int kSellG8 = 256, kSellG4 = 128, kSellG2 = 64;
 
@@ -191,6 +198,112 @@ __device__ __forceinline__ void sell_step(double a, double lo, double up, double
   }
 }
 
+// Second half of a slice, after its chains: order-free reductions over a
+// unit's lanes, row finish on the owner lanes (row check, filter; chunks of
+// split rows: partial record, last chunk combines), then phase 2 over the
+// slice's filter words.
+template <bool kRowCheck, int LG>
+__device__ __forceinline__ void slice_tail(const RoundArgs& A, SellWarpSmem& W, const SliceDesc& sd,
+                                           const UnitDesc& ud, bool active, int len, int lane,
+                                           Act act, double xmax, double lhs_r, double rhs_r,
+                                           uint64_t pol_keep, bool& inf_flag, const DevCfg& cfg) {
+  constexpr int H = 32 >> LG;
+  const int j = lane >> (5 - LG), u = lane & (H - 1);
+  const bool whole = ud.ref >= 0;
+  const int steps = sd.steps;
+  uint32_t* sw = A.sw + sd.off + lane;
+  // order-free parts over the unit's lanes
+#pragma unroll
+  for (int o = H; o < 32; o <<= 1) {
+    act.min_i += __shfl_xor_sync(0xffffffffu, act.min_i, o);
+    act.max_i += __shfl_xor_sync(0xffffffffu, act.max_i, o);
+    xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+  }
+
+  // ---- row finish (owner lanes) ----------------------------------------------------
+  bool may = false;
+  if (j == 0 && active) {
+    if (whole) {
+      const double l = lhs_r, h = rhs_r;
+      if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
+      const RowFilter f = row_filter(act, l, h);
+      may = row_may(f, xmax);
+      W.min_f[u] = act.min_f;
+      W.max_f[u] = act.max_f;
+      W.min_i[u] = act.min_i;
+      W.max_i[u] = act.max_i;
+      W.lhs[u] = l;
+      W.rhs[u] = h;
+      W.tr[u] = f.tr;
+      W.tl[u] = f.tl;
+      W.mode[u] = f.mode;
+    } else {
+      // a chunk of a split row: partial record; the last chunk combines them
+      const SegDesc d = A.segs[-ud.ref - 1];
+      volatile SegPartial* P = A.partial + d.out;
+      P->min_f = act.min_f;
+      P->max_f = act.max_f;
+      P->xmax = xmax;
+      P->min_i = act.min_i;
+      P->max_i = act.max_i;
+      __threadfence();
+      const int nch = A.sfirst[d.rslot + 1] - A.sfirst[d.rslot];
+      if (atomicAdd(&A.row_done[d.rslot], 1) == nch - 1) {
+        __threadfence();
+        A.row_done[d.rslot] = 0;
+        finish_split_row<kRowCheck>(A, d.rslot, inf_flag, cfg);
+      }
+    }
+  }
+  if (j == 0) W.may[u] = may;
+  if (PG_SELL_DEBUG && (cfg.flags & 0x10000u)) return;  // timing experiments only: no phase 2
+  if (!__any_sync(0xffffffffu, may)) return;
+
+  // ---- phase 2: filter words -> queue -> exact pipeline ------------------------------
+  __syncwarp();
+  const bool umay = W.may[u] != 0;
+  RowFilter f = {0.0, 0.0, 0};
+  if (umay) f = RowFilter{W.tr[u], W.tl[u], W.mode[u]};
+  int qn = 0;
+  for (int t0 = 0; t0 < steps; t0 += kSellUnroll) {
+    uint32_t b[kSellUnroll];
+    bool in[kSellUnroll];
+#pragma unroll
+    for (int k = 0; k < kSellUnroll; ++k) {
+      in[k] = umay && ((t0 + k) << LG) + j < len;
+      b[k] = in[k] ? sw[32 * (t0 + k)] : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < kSellUnroll; ++k) {
+      const bool pass = in[k] && filt_may(f, b[k]);
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
+      if (!m) continue;
+      if (pass) {
+        const int slot = qn + __popc(m & ((1u << lane) - 1u));
+        W.qe[slot] = 32 * (t0 + k) + lane;
+        W.qu[slot] = (uint8_t)u;
+      }
+      qn += __popc(m);
+      if (qn >= 32) {
+        __syncwarp();
+        inf_flag |= sell_drain(A, W, sd.off, 32, lane, pol_keep, cfg);
+        __syncwarp();
+        qn -= 32;
+        if (lane < qn) {
+          W.qe[lane] = W.qe[32 + lane];
+          W.qu[lane] = W.qu[32 + lane];
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (qn) {
+    __syncwarp();
+    inf_flag |= sell_drain(A, W, sd.off, qn, lane, pol_keep, cfg);
+  }
+  __syncwarp();
+}
+
 // One slice by one warp.  LG = log2(lanes per unit); kDense: a full sweep
 // (no worklist), every lane walks every step of the slice.
 template <bool kRowCheck, int LG, bool kDense>
@@ -305,97 +418,91 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
         if (t0 + k < steps) sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xmax, sw + 32 * (t0 + k));
     }
   }
-  // order-free parts over the unit's lanes
-#pragma unroll
-  for (int o = H; o < 32; o <<= 1) {
-    act.min_i += __shfl_xor_sync(0xffffffffu, act.min_i, o);
-    act.max_i += __shfl_xor_sync(0xffffffffu, act.max_i, o);
-    xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
-  }
+  slice_tail<kRowCheck, LG>(A, W, sd, ud, active, len, lane, act, xmax, ud.ref >= 0 ? A.lhs[ud.ref] : 0.0,
+                            ud.ref >= 0 ? A.rhs[ud.ref] : 0.0, pol_keep, inf_flag, cfg);
+}
 
-  // ---- row finish (owner lanes) ----------------------------------------------------
-  bool may = false;
-  if (j == 0 && active) {
-    if (whole) {
-      const int r = ud.ref;
-      const double l = A.lhs[r], h = A.rhs[r];
-      if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
-      const RowFilter f = row_filter(act, l, h);
-      may = row_may(f, xmax);
-      W.min_f[u] = act.min_f;
-      W.max_f[u] = act.max_f;
-      W.min_i[u] = act.min_i;
-      W.max_i[u] = act.max_i;
-      W.lhs[u] = l;
-      W.rhs[u] = h;
-      W.tr[u] = f.tr;
-      W.tl[u] = f.tl;
-      W.mode[u] = f.mode;
-    } else {
-      // a chunk of a split row: partial record; the last chunk combines them
-      const SegDesc d = A.segs[-ud.ref - 1];
-      volatile SegPartial* P = A.partial + d.out;
-      P->min_f = act.min_f;
-      P->max_f = act.max_f;
-      P->xmax = xmax;
-      P->min_i = act.min_i;
-      P->max_i = act.max_i;
-      __threadfence();
-      const int nch = A.sfirst[d.rslot + 1] - A.sfirst[d.rslot];
-      if (atomicAdd(&A.row_done[d.rslot], 1) == nch - 1) {
-        __threadfence();
-        A.row_done[d.rslot] = 0;
-        finish_split_row<kRowCheck>(A, d.rslot, inf_flag, cfg);
-      }
-    }
-  }
-  if (j == 0) W.may[u] = may;
-  if (PG_SELL_DEBUG && (cfg.flags & 0x10000u)) return;  // timing experiments only: no phase 2
-  if (!__any_sync(0xffffffffu, may)) return;
-
-  // ---- phase 2: filter words -> queue -> exact pipeline ------------------------------
-  __syncwarp();
-  const bool umay = W.may[u] != 0;
-  RowFilter f = {0.0, 0.0, 0};
-  if (umay) f = RowFilter{W.tr[u], W.tl[u], W.mode[u]};
-  int qn = 0;
-  for (int t0 = 0; t0 < steps; t0 += kSellUnroll) {
-    uint32_t b[kSellUnroll];
-    bool in[kSellUnroll];
+// R narrow slices (one lane per unit) by one warp: every lane runs R
+// independent chains, interleaved, so each step has R entries in flight per
+// lane and the per-slice latencies (descriptors, row sides, the ticket)
+// are paid once per R slices.  Full sweeps only.
+template <bool kRowCheck, int R>
+__device__ __forceinline__ void sell_group(const RoundArgs& A, SellWarpSmem& W, int s0, int nr,
+                                           int lane, uint64_t pol_keep, uint64_t pol_stream,
+                                           bool& inf_flag, const DevCfg& cfg) {
+  long long off[R];
+  int steps[R], cnt[R];
+  UnitDesc ud[R];
+  double l[R], h[R];
 #pragma unroll
-    for (int k = 0; k < kSellUnroll; ++k) {
-      in[k] = umay && ((t0 + k) << LG) + j < len;
-      b[k] = in[k] ? sw[32 * (t0 + k)] : 0u;
+  for (int r = 0; r < R; ++r) {
+    SliceDesc d = {0, 0, 0, 0, 0, 0, 0};
+    if (r < nr) d = A.slices[s0 + r];
+    off[r] = d.off + lane;
+    steps[r] = d.steps;
+    cnt[r] = d.count;
+    ud[r] = UnitDesc{0, -1};
+    if (lane < d.count) ud[r] = A.units[d.first + lane];
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    l[r] = h[r] = 0.0;
+    if (ud[r].ref >= 0) {
+      l[r] = A.lhs[ud[r].ref];
+      h[r] = A.rhs[ud[r].ref];
+    }
+  }
+  Act act[R];
+  double xmax[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    act[r] = Act{0.0, 0.0, 0, 0};
+    xmax[r] = -CUDART_INF;
+  }
+  const int tmax = steps[0];  // the group's first slice is its widest
+  double a[R];
+  int32_t c[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    a[r] = 0.0;
+    c[r] = A.pad_col;
+    if (0 < steps[r]) {
+      a[r] = ld_stream_f64(A.sv + off[r], pol_stream);
+      c[r] = ld_stream_s32(A.sc + off[r], pol_stream);
+    }
+  }
+  for (int t = 0; t < tmax; ++t) {
+    double lo[R], up[R], q[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) ld_snap_keep(A.snap + (c[r] & 0x7fffffff), pol_keep, lo[r], up[r], q[r]);
+    double an[R];
+    int32_t cn[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      an[r] = 0.0;
+      cn[r] = A.pad_col;
+      if (t + 1 < steps[r]) {
+        an[r] = ld_stream_f64(A.sv + off[r] + 32 * (t + 1), pol_stream);
+        cn[r] = ld_stream_s32(A.sc + off[r] + 32 * (t + 1), pol_stream);
+      }
     }
 #pragma unroll
-    for (int k = 0; k < kSellUnroll; ++k) {
-      const bool pass = in[k] && filt_may(f, b[k]);
-      const unsigned m = __ballot_sync(0xffffffffu, pass);
-      if (!m) continue;
-      if (pass) {
-        const int slot = qn + __popc(m & ((1u << lane) - 1u));
-        W.qe[slot] = 32 * (t0 + k) + lane;
-        W.qu[slot] = (uint8_t)u;
-      }
-      qn += __popc(m);
-      if (qn >= 32) {
-        __syncwarp();
-        inf_flag |= sell_drain(A, W, sd.off, 32, lane, pol_keep, cfg);
-        __syncwarp();
-        qn -= 32;
-        if (lane < qn) {
-          W.qe[lane] = W.qe[32 + lane];
-          W.qu[lane] = W.qu[32 + lane];
-        }
-        __syncwarp();
-      }
+    for (int r = 0; r < R; ++r)
+      if (t < steps[r]) sell_step<0>(a[r], lo[r], up[r], q[r], lane, act[r], xmax[r], A.sw + off[r] + 32 * t);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      a[r] = an[r];
+      c[r] = cn[r];
     }
   }
-  if (qn) {
-    __syncwarp();
-    inf_flag |= sell_drain(A, W, sd.off, qn, lane, pol_keep, cfg);
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (r < nr) {
+      const SliceDesc d = {off[r] - lane, 0, 0, steps[r], (int16_t)cnt[r], 0, 0};
+      slice_tail<kRowCheck, 0>(A, W, d, ud[r], lane < cnt[r], ud[r].len, lane, act[r], xmax[r],
+                               l[r], h[r], pol_keep, inf_flag, cfg);
+    }
   }
-  __syncwarp();
 }
 
 // Persistent, one warp per slice (longest first).  kDense: a full sweep;
@@ -403,13 +510,11 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
 // launched when the worklist is on; the one that does not match the round
 // returns at once (the round's kind is known on the device only).
 template <bool kRowCheck, bool kDense>
-__global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const RoundArgs A,
-                                                                     const DevCfg cfg) {
-  __shared__ SellWarpSmem smem[kSellWarps];
+__device__ __forceinline__ void sell_sweep(const RoundArgs& A, const DevCfg& cfg,
+                                           SellWarpSmem* smem) {
   const int lane = threadIdx.x & 31;
   SellWarpSmem& W = smem[threadIdx.x >> 5];
-  const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
-  if (full != kDense) return;
+  const bool full = kDense;
   const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
   const uint8_t* rflag = A.dirty.row_flag + (size_t)par * A.dirty.ms;
   const uint64_t pk = l2_policy_evict_last();
@@ -418,10 +523,24 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const Round
   int next = 0;
   if (lane == 0) next = atomicAdd(&A.st->work, 1);
   next = __shfl_sync(0xffffffffu, next, 0);
-  while (next < A.nslices) {
+  const int nitems = A.group_start + (A.nslices - A.group_start + kSellGroup - 1) / kSellGroup;
+  while (next < nitems) {
     const int s = next;
     if (lane == 0) next = atomicAdd(&A.st->work, 1);
     next = __shfl_sync(0xffffffffu, next, 0);
+    if (s >= A.group_start) {
+      // a group of narrow one-lane slices
+      const int s0 = A.group_start + (s - A.group_start) * kSellGroup;
+      const int nr = min(kSellGroup, A.nslices - s0);
+      if (kDense) {
+        sell_group<kRowCheck, kSellGroup>(A, W, s0, nr, lane, pk, ps, inf_flag, cfg);
+      } else {
+        for (int r = 0; r < nr; ++r)
+          sell_slice<kRowCheck, 0, kDense>(A, W, A.slices[s0 + r], lane, full, rflag, pk, ps,
+                                           inf_flag, cfg);
+      }
+      continue;
+    }
     const SliceDesc sd = A.slices[s];
 #if PG_SELL_LGMAX >= 3
     if (sd.lg == 3) {
@@ -444,6 +563,15 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const Round
     sell_slice<kRowCheck, 0, kDense>(A, W, sd, lane, full, rflag, pk, ps, inf_flag, cfg);
   }
   if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
+}
+
+template <bool kRowCheck, bool kDense>
+__global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const RoundArgs A,
+                                                                     const DevCfg cfg) {
+  __shared__ SellWarpSmem smem[kSellWarps];
+  const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
+  if (full != kDense) return;
+  sell_sweep<kRowCheck, kDense>(A, cfg, smem);
 }
 
 // ---- session setup: units, slices, the sliced-ELL copy ---------------------------
@@ -503,6 +631,9 @@ __global__ void k_unit_regions(const UnitDesc* __restrict__ units, int nunits, i
   for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nunits; u += gridDim.x * blockDim.x) {
     const int lg = sell_lg(units[u].len, lg_min);
     if (u + 1 == nunits || sell_lg(units[u + 1].len, lg_min) != lg) cnt[lg] = u + 1;
+    // cnt[4]: units longer than the grouping width (sorted descending)
+    if (units[u].len > PG_SELL_GROUPW && (u + 1 == nunits || units[u + 1].len <= PG_SELL_GROUPW))
+      cnt[4] = u + 1;
   }
 }
 
