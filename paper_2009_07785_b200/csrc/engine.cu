@@ -45,6 +45,7 @@
 #include "cand.cuh"
 #include "loop.cuh"
 #include "nodes.cuh"
+#include "narrow.cuh"
 
 using namespace pgb;
 
@@ -203,6 +204,8 @@ struct pg_session {
   int loop_grid = 0;     // co-resident CTAs of the persistent loop kernel
   int nodes_per_sm = 1;  // resident k_nodes CTAs per SM
   int32_t max_row_len = 0;
+  ActF* d_f32_part = nullptr;  // Narrow32: per-thread chunk partials
+  int f32_maxc = 1;
 
   // device arrays
   int32_t* d_row_ptr = nullptr;
@@ -275,7 +278,7 @@ struct pg_session {
     for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up}) dfree(p);
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
                     d_lo_res, d_up_res, d_segs, d_srow, d_sfirst, d_partial,
-                    d_ract, d_wl_short, d_wl_long, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
+                    d_ract, d_wl_short, d_wl_long, d_f32_part, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
                     d_flags, d_chg};
     for (void* p : ptrs) dfree(p);  // stream-ordered: no device sync here
     if (h_st) cudaFreeHost(h_st);
@@ -326,7 +329,15 @@ struct pg_session {
     const bool rowcheck = (cfg.flags & PG_FLAG_ROWCHECK) != 0;
     const RoundArgs A = round_args();
     if (k1_begin) PG_CUDA(cudaEventRecord(k1_begin, stream));
-    if (nslices > 0) {
+    if (cfg.scalar_mode == PG_NARROW32) {
+      if (m > 0) {
+        const int grid = grid_for(m, 256, 4);
+        if (rowcheck)
+          k_round_f32<true><<<grid, 256, 0, stream>>>(A, dcfg, m, d_f32_part, f32_maxc);
+        else
+          k_round_f32<false><<<grid, 256, 0, stream>>>(A, dcfg, m, d_f32_part, f32_maxc);
+      }
+    } else if (nslices > 0) {
       const int grid = std::max(1, std::min((nslices + 7) / 8, num_sms * sell_per_sm));
       if (rowcheck)
         k_sell<true, true><<<grid, kSellThreads, 0, stream>>>(A, dcfg);
@@ -396,7 +407,7 @@ struct pg_session {
   // whose rounds are launch-latency bound; never with a communicator (the
   // all-reduce is a host-enqueued NCCL call between phases)
   bool use_persistent() const {
-    if (comm || loop_grid <= 0) return false;
+    if (comm || loop_grid <= 0 || cfg.scalar_mode == PG_NARROW32) return false;
     static const long long thr = [] {
       const char* e = getenv("PG_PERSIST_NNZ");
       return e ? atoll(e) : 8000000LL;
@@ -530,6 +541,10 @@ struct pg_session {
     if (n) {
       k_normalize<<<grid_for(n, 256), 256, 0, stream>>>(d_lo0, n, cfg.infinity_threshold);
       k_normalize<<<grid_for(n, 256), 256, 0, stream>>>(d_up0, n, cfg.infinity_threshold);
+      if (cfg.scalar_mode == PG_NARROW32) {
+        k_to_f32<<<grid_for(n, 256), 256, 0, stream>>>(d_lo0, n);
+        k_to_f32<<<grid_for(n, 256), 256, 0, stream>>>(d_up0, n);
+      }
       PG_CUDA(cudaGetLastError());
     }
   }
@@ -549,8 +564,6 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     throw Error{PG_ENODEV, std::string("device is ") + prop.name + " (sm_" +
                                std::to_string(prop.major * 10 + prop.minor) +
                                "); this build targets sm_100a only"};
-  if (cfg->scalar_mode != PG_WIDE64)
-    throw Error{PG_EINVAL, "scalar_mode Narrow32 is not implemented on the GPU engine yet"};
 
   tm.lap("device query");
   auto* s = new pg_session;
@@ -754,6 +767,16 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       k_permute_rows<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
           t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, s->d_integral, s->d_colx,
           s->d_vals, s->d_lhs, s->d_rhs, m, cfg->infinity_threshold);
+      PG_CUDA(cudaGetLastError());
+    }
+    if (cfg->scalar_mode == PG_NARROW32) {
+      // the float working copy (engine_common.hpp:24-38) and chunk scratch
+      k_to_f32<<<s->grid_for(nnz, 256), 256, 0, st>>>(s->d_vals, nnz);
+      k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_lhs, m);
+      k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_rhs, m);
+      const int chunk = cfg->nnz_budget;
+      s->f32_maxc = s->max_row_len > chunk ? (s->max_row_len + chunk - 1) / chunk : 1;
+      s->d_f32_part = dalloc<ActF>((size_t)s->grid_for(m, 256, 4) * 256 * s->f32_maxc);
       PG_CUDA(cudaGetLastError());
     }
     // sliced-ELL copy (sell.cuh): units sorted by length, slices per
@@ -1005,6 +1028,7 @@ int pg_round(const pg_problem* p, const pg_config* cfg, const double* lb_in, con
   pg_config c = *cfg;
   c.round_limit = 1;
   c.loop_mode = PG_LOOP_HOST;
+  c.scalar_mode = PG_WIDE64;  // propagate_round_parallel always works in double (par_engine.cpp:282)
   c.flags &= ~PG_FLAG_ROWCHECK;
   pg_problem q = *p;
   q.lower = lb_in;
@@ -1150,7 +1174,7 @@ int pg_session_propagate_nodes(pg_session* s, int32_t K, const int32_t* node_ptr
                         d_up + node_ptr[k]};
     if (K) PG_CUDA(cudaMemcpyAsync(d_ctls, ctls.data(), sizeof(NodeCtl) * K, cudaMemcpyHostToDevice, st));
     const size_t n = (size_t)s->n;
-    if (!getenv("PG_NODES_SERIAL")) {
+    if (!getenv("PG_NODES_SERIAL") && s->cfg.scalar_mode == PG_WIDE64) {
       // batched: one CTA per node, many nodes at once (nodes.cuh)
       s->ensure_col_index();
       const size_t m = (size_t)s->m;
@@ -1259,7 +1283,8 @@ int pg_session_propagate_nodes(pg_session* s, int32_t K, const int32_t* node_ptr
       PG_CUDA(cudaMemcpyAsync(s->d_lo0, s->d_root_lo, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
       PG_CUDA(cudaMemcpyAsync(s->d_up0, s->d_root_up, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
       PG_CUDA(cudaMemcpyAsync(s->d_ctl, d_ctls + k, sizeof(NodeCtl), cudaMemcpyDeviceToDevice, st));
-      k_apply_node<<<4, 256, 0, st>>>(s->d_lo0, s->d_up0, s->d_ctl, s->cfg.infinity_threshold);
+      k_apply_node<<<4, 256, 0, st>>>(s->d_lo0, s->d_up0, s->d_ctl, s->cfg.infinity_threshold,
+                                      s->cfg.scalar_mode == PG_NARROW32);
       PG_CUDA(cudaGetLastError());
       if (s->cfg.loop_mode == PG_LOOP_GRAPH) {
         PG_CUDA(cudaGraphLaunch(s->exec, st));

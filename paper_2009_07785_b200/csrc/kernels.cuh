@@ -592,12 +592,18 @@ __global__ void __launch_bounds__(256)
 
 // start bounds of a node: the root fixpoint (copied before) + its overrides
 __global__ void k_apply_node(double* __restrict__ lo0, double* __restrict__ up0,
-                             const NodeCtl* __restrict__ ctl, double thr) {
+                             const NodeCtl* __restrict__ ctl, double thr, int f32) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ctl->nvars; i += gridDim.x * blockDim.x) {
     const int j = ctl->vars[i];
     const double l = ctl->lo[i], u = ctl->up[i];
-    lo0[j] = l >= thr ? CUDART_INF : (l <= -thr ? -CUDART_INF : l);
-    up0[j] = u >= thr ? CUDART_INF : (u <= -thr ? -CUDART_INF : u);
+    double nl = l >= thr ? CUDART_INF : (l <= -thr ? -CUDART_INF : l);
+    double nu = u >= thr ? CUDART_INF : (u <= -thr ? -CUDART_INF : u);
+    if (f32) {  // Narrow32 working copy (engine_common.hpp:24-38)
+      nl = (double)(float)nl;
+      nu = (double)(float)nu;
+    }
+    lo0[j] = nl;
+    up0[j] = nu;
   }
 }
 

@@ -130,3 +130,32 @@ def test_c4_warm_started_nodes(worklist):
         # solve confirms it in one round
         again = s.propagate()
         assert again.status == PropagationStatus.Converged and again.rounds_executed == 1
+
+
+@pytest.mark.parametrize("row_check", [False, True])
+def test_batched_nodes_many(row_check):
+    """The batched node kernel (one CTA per node, 200 nodes in flight) against
+    full cpu_par solves of each node's bounds; includes crossed overrides
+    (Infeasible after 0 rounds) and tight fixings."""
+    from paper_2009_07785_b200.engine import node_overrides
+    inst = G.gen_random(20000, 20000, 9, mean_row_nnz=8.0, integral_fraction=0.5)
+    cfg = EngineConfig(row_check=row_check, worklist=True)
+    ref_cfg = EngineConfig(row_check=row_check)
+    with Session(inst, cfg) as s:
+        root = s.set_root()
+        assert root.status == PropagationStatus.Converged
+        lo, up = G.gen_nodes(inst, root.bounds.lower, root.bounds.upper, K=200)
+        # a few crossed and a few fixed nodes
+        for k in range(0, 200, 37):
+            j = int(np.flatnonzero(np.isfinite(root.bounds.lower))[k])
+            lo[k, j] = root.bounds.upper[j] + 1.0
+        for k in range(5, 200, 41):
+            j = int(np.flatnonzero(inst.integral.astype(bool) & np.isfinite(root.bounds.lower))[k])
+            up[k, j] = lo[k, j]
+        ptr, vs, ls, us = node_overrides(root.bounds.lower, root.bounds.upper, lo, up)
+        st, rd, blo, bup, _ = s.propagate_nodes(ptr, vs, ls, us, want_bounds=True)
+        for k in range(200):
+            ref = O.propagate_parallel(inst, ref_cfg, lo[k], up[k])
+            assert st[k] == int(ref.status) and rd[k] == ref.rounds_executed, k
+            assert np.array_equal(O.canon(blo[k]), O.canon(ref.bounds.lower)), k
+            assert np.array_equal(O.canon(bup[k]), O.canon(ref.bounds.upper)), k

@@ -289,3 +289,49 @@ def test_worklist_modes_identical(worklist, row_check):
     inst = G.gen_powerlaw(20000, 20000, 77, cap=3000)
     cfg = EngineConfig(row_check=row_check, worklist=worklist, nnz_budget=256)
     assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg), inst.name)
+
+
+# ---- ScalarMode::Narrow32 (model.hpp:129) -------------------
+def _f32(row_check=False, **kw):
+    from paper_2009_07785_b200.model import ScalarMode
+    return EngineConfig(row_check=row_check, scalar_mode=ScalarMode.Narrow32, **kw)
+
+
+def test_f32_acceptance_suite_parity():
+    """Float working copy, float activities/candidates, double acceptance:
+    bit-identical to the oracle's run_parallel<float> (pinned to the reference
+    in tests/test_oracle.py::test_f32_mode_matches_reference)."""
+    cfg = _f32()
+    for r, c, seed, mx in G.acceptance_suite_params(80):
+        inst = G.gen_random(r, c, seed, max_nnz=mx)
+        assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg), (r, c, seed))
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+@pytest.mark.parametrize("row_check", [False, True])
+def test_f32_config1_parity(seed, row_check):
+    inst = G.config_instance("c1", seed)
+    cfg = _f32(row_check=row_check)
+    assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg), seed)
+
+
+@pytest.mark.parametrize("budget", [64, 256])
+def test_f32_chunked_long_rows(budget):
+    """Rows longer than nnz_budget: float chunk partials combined pairwise."""
+    inst = G.gen_random(300, 4000, 11, mean_row_nnz=400.0, integral_fraction=0.3)
+    cfg = _f32(nnz_budget=budget, vector_threshold=64)
+    assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg), budget)
+
+
+def test_f32_round_api_is_double():
+    """propagate_round_parallel always works in double (par_engine.cpp:282)."""
+    inst = G.gen_random(2000, 1500, 5, mean_row_nnz=8.0, integral_fraction=0.5)
+    lo = np.array(inst.bounds.lower, dtype=float)
+    up = np.array(inst.bounds.upper, dtype=float)
+    sa = RoundSnapshot(VariableBounds(lo.copy(), up.copy()))
+    sb = RoundSnapshot(VariableBounds(lo.copy(), up.copy()))
+    oa = propagate_round_gpu(inst, sa, _f32())
+    ob = propagate_round_gpu(inst, sb, PAR)
+    assert oa.changes == ob.changes and oa.changes > 0
+    assert np.array_equal(O.canon(sa.bounds_out.lower), O.canon(sb.bounds_out.lower))
+    assert np.array_equal(O.canon(sa.bounds_out.upper), O.canon(sb.bounds_out.upper))
