@@ -214,6 +214,7 @@ struct pg_session {
   double* d_lhs = nullptr;
   double* d_rhs = nullptr;
   Snap* d_snap = nullptr;
+  double2* d_bnd = nullptr;  // compact {lb, ub} records (sell.cuh gathers)
   uint8_t* d_integral = nullptr;
   int32_t* d_row_done = nullptr;
   longlong2* d_key_out = nullptr;
@@ -234,7 +235,7 @@ struct pg_session {
   double* d_sv = nullptr;
   int32_t* d_sc = nullptr;
   uint32_t* d_sw = nullptr;
-  int32_t nunits = 0, nslices = 0, lg_min = 0, group_start = 0;
+  int32_t nunits = 0, nslices = 0, lg_min = 0, group_start = 0, lg0_ustart = 0, lg0_sstart = 0;
   int64_t sell_elems = 0;
   DevState* d_st = nullptr;
   long long* d_per_round = nullptr;
@@ -243,11 +244,15 @@ struct pg_session {
   int32_t* d_col_item = nullptr;
   uint8_t* d_flags = nullptr;  // row marks, two buffers
   int32_t* d_chg = nullptr;    // changed-column lists, two buffers
+  int32_t *d_row_unit = nullptr, *d_part_unit = nullptr, *d_unit_slice = nullptr;
+  int32_t* d_wide_list = nullptr;
+  int32_t* d_unit_list = nullptr;
   Dirty dirty{};
 
   // host mirrors
   DevState* h_st = nullptr;  // pinned
-  int32_t nseg = 0, nsrow = 0;
+  int32_t nseg = 0, nsrow = 0, nsplit = 0;
+  int32_t* d_split = nullptr;  // split-row slots (k_split_finish)
   int64_t short_rows = 0, short_nnz = 0, seg_nnz = 0, wl_long_cap = 0;
 
   // graph
@@ -278,8 +283,8 @@ struct pg_session {
     for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up}) dfree(p);
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
                     d_lo_res, d_up_res, d_segs, d_srow, d_sfirst, d_partial,
-                    d_ract, d_wl_short, d_wl_long, d_f32_part, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
-                    d_flags, d_chg};
+                    d_ract, d_wl_short, d_wl_long, d_f32_part, d_split, d_bnd, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
+                    d_flags, d_chg, d_row_unit, d_part_unit, d_unit_slice, d_wide_list, d_unit_list};
     for (void* p : ptrs) dfree(p);  // stream-ordered: no device sync here
     if (h_st) cudaFreeHost(h_st);
     if (stream) cudaStreamDestroy(stream);
@@ -296,6 +301,8 @@ struct pg_session {
     A.slices = d_slices;
     A.nslices = nslices;
     A.group_start = group_start;
+    A.lg0_ustart = lg0_ustart;
+    A.lg0_sstart = lg0_sstart;
     A.nunits = nunits;
     A.units = d_units;
     A.sv = d_sv;
@@ -316,6 +323,7 @@ struct pg_session {
     A.wl_short = d_wl_short;
     A.wl_long = d_wl_long;
     A.snap = d_snap;
+    A.bnd = d_bnd;
     A.key_out = (long long*)d_key_out;
     A.st = d_st;
     A.dirty = dirty;
@@ -340,14 +348,21 @@ struct pg_session {
     } else if (nslices > 0) {
       const int grid = std::max(1, std::min((nslices + 7) / 8, num_sms * sell_per_sm));
       if (rowcheck)
-        k_sell<true, true><<<grid, kSellThreads, 0, stream>>>(A, dcfg);
+        k_sell<true, true><<<grid, kSellThreads, kSellSmem, stream>>>(A, dcfg);
       else
-        k_sell<false, true><<<grid, kSellThreads, 0, stream>>>(A, dcfg);
+        k_sell<false, true><<<grid, kSellThreads, kSellSmem, stream>>>(A, dcfg);
       if (dirty.enabled) {
         if (rowcheck)
-          k_sell<true, false><<<grid, kSellThreads, 0, stream>>>(A, dcfg);
+          k_sell<true, false><<<grid, kSellThreads, kSellSmem, stream>>>(A, dcfg);
         else
-          k_sell<false, false><<<grid, kSellThreads, 0, stream>>>(A, dcfg);
+          k_sell<false, false><<<grid, kSellThreads, kSellSmem, stream>>>(A, dcfg);
+      }
+      if (nsplit > 0) {
+        const int g = std::max(1, std::min((nsplit + kSplitWarps - 1) / kSplitWarps, num_sms * 8));
+        if (rowcheck)
+          k_split_finish<true><<<g, kSplitWarps * 32, 0, stream>>>(A, d_split, nsplit, dcfg);
+        else
+          k_split_finish<false><<<g, kSplitWarps * 32, 0, stream>>>(A, d_split, nsplit, dcfg);
       }
       k_cand<<<num_sms * cand_per_sm, kCandThreads, 0, stream>>>(A, dcfg);
     }
@@ -363,16 +378,16 @@ struct pg_session {
       if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllReduce: ") + g_nccl.error(rc)};
     }
     k_commit<<<grid_for(n, kCommitThreads), kCommitThreads, 0, stream>>>(
-        d_snap, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0);
+        d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0);
     if (dirty.enabled) k_mark<<<num_sms * 8, 256, 0, stream>>>(dirty, d_st);
     PG_CUDA(cudaGetLastError());
   }
 
   void enqueue_reset(bool use_graph, bool check_crossed) {
     k_reset<<<grid_for(n, kCommitThreads), kCommitThreads, 0, stream>>>(
-        d_lo0, d_up0, d_integral, d_snap, d_key_out, n, d_st, dcfg, dirty, d_ctl,
+        d_lo0, d_up0, d_integral, d_snap, d_bnd, d_key_out, n, d_st, dcfg, dirty, d_ctl,
         check_crossed ? 1 : 0, cond, use_graph ? 1 : 0);
-    if (dirty.enabled) k_mark_vars<<<num_sms * 2, 256, 0, stream>>>(dirty, d_ctl);
+    if (dirty.enabled) k_mark_vars<<<num_sms * 2, 256, 0, stream>>>(dirty, d_ctl, d_st);
     PG_CUDA(cudaGetLastError());
   }
 
@@ -420,6 +435,7 @@ struct pg_session {
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(loop_grid);
     lc.blockDim = dim3(kSellThreads);
+    lc.dynamicSmemBytes = sizeof(LoopSmem);
     lc.stream = stream;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeCooperative;
@@ -430,9 +446,11 @@ struct pg_session {
     long long* pr = d_per_round;
     int nn = n;
     if (cfg.flags & PG_FLAG_ROWCHECK)
-      PG_CUDA(cudaLaunchKernelEx(&lc, k_loop<true>, A, dcfg, snap, nn, pr));
+      PG_CUDA(cudaLaunchKernelEx(&lc, k_loop<true>, A, dcfg, snap, nn, pr,
+                                 (const int32_t*)d_split, nsplit));
     else
-      PG_CUDA(cudaLaunchKernelEx(&lc, k_loop<false>, A, dcfg, snap, nn, pr));
+      PG_CUDA(cudaLaunchKernelEx(&lc, k_loop<false>, A, dcfg, snap, nn, pr,
+                                 (const int32_t*)d_split, nsplit));
   }
 
   void build_graph() {
@@ -571,15 +589,22 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->dev = cfg->device;
     PG_CUDA(cudaSetDevice(s->dev));
     s->num_sms = prop.sms;
+    for (const void* f : {(const void*)k_sell<true, true>, (const void*)k_sell<false, true>,
+                          (const void*)k_sell<true, false>, (const void*)k_sell<false, false>})
+      PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem));
+    for (const void* f : {(const void*)k_loop<true>, (const void*)k_loop<false>})
+      PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LoopSmem)));
     PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->sell_per_sm, k_sell<true, true>,
-                                                          kSellThreads, 0));
+                                                          kSellThreads, kSellSmem));
     s->sell_per_sm = std::max(1, s->sell_per_sm);
     PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->cand_per_sm, k_cand, kCandThreads, 0));
     {
       int per = 0;
-      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_loop<true>, kSellThreads, 0));
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_loop<true>, kSellThreads,
+                                                            sizeof(LoopSmem)));
       int per2 = 0;
-      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_loop<false>, kSellThreads, 0));
+      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_loop<false>, kSellThreads,
+                                                            sizeof(LoopSmem)));
       s->loop_grid = std::min(per, per2) * s->num_sms;
       PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_nodes<true>, kNodeThreads, 0));
       s->nodes_per_sm = std::max(1, per);
@@ -738,6 +763,8 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       // term 0 * -inf is NaN, which fmax ignores)
       static const Snap pad = {0.0, 0.0, -std::numeric_limits<double>::infinity(), 0};
       PG_CUDA(cudaMemcpyAsync(s->d_snap + n, &pad, sizeof(Snap), cudaMemcpyHostToDevice, st));
+      s->d_bnd = dalloc<double2>((size_t)n + 1);
+      PG_CUDA(cudaMemsetAsync(s->d_bnd + n, 0, sizeof(double2), st));
     }
     s->d_key_out = dalloc<longlong2>((size_t)n + 1);  // + infeasibility slot
     s->d_lo0 = dalloc<double>(n);
@@ -758,6 +785,15 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     PG_CUDA(cudaMemsetAsync(s->d_ctl, 0, sizeof(NodeCtl), st));  // cold starts
     PG_CUDA(cudaMemsetAsync(s->d_st, 0, sizeof(DevState), st));
     PG_CUDA(cudaMemsetAsync(s->d_row_done, 0, sizeof(int32_t) * std::max<int32_t>(1, s->nsrow), st));
+    s->d_split = dalloc<int32_t>(std::max<int32_t>(1, s->nsrow) + 1);
+    if (s->nsrow) {
+      int32_t* cnt = s->d_split + s->nsrow;  // the count rides at the end
+      PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));
+      PG_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+      k_split_list<<<s->grid_for(s->nsrow, 256), 256, 0, st>>>(s->d_sfirst, s->nsrow, s->d_split, cnt);
+      PG_CUDA(cudaMemcpyAsync(&s->nsplit, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+      PG_CUDA(cudaStreamSynchronize(st));
+    }
     PG_CUDA(cudaMemsetAsync(s->d_colx, 0, sizeof(int32_t) * (nnz + 4), st));
     PG_CUDA(cudaMemsetAsync(s->d_vals, 0, sizeof(double) * (nnz + 2), st));
     // the ordering (stream 2) must be complete before the permutation
@@ -826,10 +862,12 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         R.sstart[k + 1] = R.sstart[k] + (R.ustart[k + 1] - R.ustart[k] + H - 1) / H;
       }
       s->nslices = R.sstart[4];
+      s->lg0_ustart = R.ustart[3];
+      s->lg0_sstart = R.sstart[3];
       // narrow one-lane slices are handed out in groups (sell_group): the
       // first slice of region 0 whose units are all <= PG_SELL_GROUPW long
       s->group_start = s->nslices;
-      if (R.ustart[4] > R.ustart[3]) {
+      if (!PG_SELL_ASYNC && R.ustart[4] > R.ustart[3]) {
         const int ub = std::max(hc[4], R.ustart[3]);  // first unit <= the grouping width
         s->group_start = std::min(s->nslices, R.sstart[3] + (ub - R.ustart[3] + 31) / 32);
       }
@@ -876,6 +914,32 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         s->d_chg = dalloc<int32_t>(2 * (size_t)n);
         D.chg_list = s->d_chg;
         s->ensure_col_index();
+        // dirty-slice lists of worklist rounds (sell.cuh)
+        s->d_row_unit = dalloc<int32_t>(m);
+        s->d_part_unit = dalloc<int32_t>(s->nseg);
+        s->d_unit_slice = dalloc<int32_t>(s->nunits);
+        s->d_wide_list = dalloc<int32_t>(2 * (size_t)s->nunits);
+        s->d_unit_list = dalloc<int32_t>(2 * (size_t)s->nunits);
+        PG_CUDA(cudaMemsetAsync(s->d_row_unit, 0xff, sizeof(int32_t) * std::max<int32_t>(m, 1), st));
+        if (s->nunits) {
+          k_unit_maps<<<s->grid_for(s->nunits, 256), 256, 0, st>>>(s->d_units, s->nunits, s->d_segs,
+                                                                 s->d_row_unit, s->d_part_unit);
+          k_slice_units<<<s->grid_for(s->nslices, 256), 256, 0, st>>>(s->d_slices, s->nslices,
+                                                                     s->d_units, s->d_unit_slice);
+        }
+        PG_CUDA(cudaGetLastError());
+        D.row_unit = s->d_row_unit;
+        D.part_unit = s->d_part_unit;
+        D.sfirst = s->d_sfirst;
+        D.unit_slice = s->d_unit_slice;
+        D.wide_list = s->d_wide_list;
+        D.nslices = s->nslices;
+        D.unit_list = s->d_unit_list;
+        D.nunits = s->nunits;
+        // changed columns above which ~1/4 of the rows are marked (mean column
+        // degree nnz / n): the next round is cheaper as a full sweep
+        D.dense_nchg = (int32_t)std::min<double>(
+            2e9, (double)m * (double)n / (4.0 * (double)std::max<int64_t>(nnz, 1)));
       }
     }
     s->upload_bounds(p->lower, p->upper);

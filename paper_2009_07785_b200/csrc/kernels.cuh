@@ -41,11 +41,14 @@ struct DevState {
   int32_t wl_short;                  // phase-2 queue lengths of the current round
   int32_t wl_long;
   int32_t work;                      // k_sell slice counter
+  int32_t work2;                     // k_sell unit-batch counter (worklist rounds)
   int32_t cand_work;                 // k_cand ticket counter
   int32_t full;                      // 1: every work item is dirty (first round)
   int32_t frac_any;                  // an integral column has a fractional start bound
   int32_t frac_tmp;                  // k_reset's accumulator of frac_any
   int32_t nchg[2];                   // changed-column list lengths, by round parity
+  int32_t nwide[2];                  // marked multi-lane unit list lengths, by round parity
+  int32_t nunit[2];                  // marked one-lane unit list lengths, by round parity
   uint32_t bar_count;                // grid barrier of the persistent round loop (loop.cuh)
   uint32_t bar_gen;
 };
@@ -67,7 +70,43 @@ struct Dirty {
   int32_t* chg_list;        // [2][n] changed columns of a round
   int32_t m, ms, n, first_seg_row;
   int32_t enabled;
+  // the units of the marked rows, so a worklist round visits only those
+  // (sell.cuh): row / chunk -> sliced-ELL unit
+  const int32_t* row_unit;   // [m] unit of a whole row, -1 for a split row
+  const int32_t* part_unit;  // [partials] unit of each chunk of a split row
+  const int32_t* sfirst;     // split-row slot -> first partial (+1 sentinel)
+  const int32_t* unit_slice; // [units] slice of a multi-lane unit, -1 for a one-lane unit
+  int32_t* wide_list;        // [2][nunits] marked multi-lane units, by round parity
+  int32_t* unit_list;        // [2][nunits] marked one-lane units
+  int32_t nslices, nunits;
+  int32_t dense_nchg;        // more changed columns than this: next round is a full sweep
 };
+
+// Row r (sorted) becomes marked for the round of parity `par` (exactly once:
+// the byte flag is set with an atomic on its word).  Its units go on that
+// round's lists: one-lane units (lg = 0, the bulk of the rows) on the unit
+// list (a lane each), longer units on the wide list (a warp each).
+__device__ __forceinline__ bool mark_row(uint8_t* flag, int r) {
+  uint32_t* w = reinterpret_cast<uint32_t*>(flag) + (r >> 2);
+  const uint32_t bit = 1u << (8 * (r & 3));
+  if (*((volatile uint32_t*)w) & bit) return false;
+  return !(atomicOr(w, bit) & bit);
+}
+__device__ __forceinline__ void mark_row_units(const Dirty& D, int r, int par, DevState* st) {
+  int32_t* ul = D.unit_list + (size_t)par * D.nunits;
+  int32_t* wl = D.wide_list + (size_t)par * D.nunits;
+  auto one = [&](int u) {
+    if (D.unit_slice[u] < 0) ul[atomicAdd(&st->nunit[par], 1)] = u;
+    else wl[atomicAdd(&st->nwide[par], 1)] = u;
+  };
+  const int u = D.row_unit[r];
+  if (u >= 0) {
+    one(u);
+  } else {
+    const int rs = r - D.first_seg_row;
+    for (int p = D.sfirst[rs]; p < D.sfirst[rs + 1]; ++p) one(D.part_unit[p]);
+  }
+}
 
 // Start of the next solve (device memory, set by stream-ordered copies):
 // warm = 1 for a branch-and-bound node started from the session's root
@@ -260,6 +299,8 @@ struct RoundArgs {
   const SliceDesc* slices;
   int32_t nslices;
   int32_t group_start;    // first slice of the grouped narrow region (sell.cuh)
+  int32_t lg0_ustart;     // first unit / slice of the one-lane region
+  int32_t lg0_sstart;
   int32_t nunits;
   const UnitDesc* units;
   const double* sv;
@@ -282,6 +323,7 @@ struct RoundArgs {
   int32_t* wl_short;      // queued rows with <= kCandShort entries
   CandItem* wl_long;      // pieces of longer queued rows
   const Snap* snap;
+  const double2* bnd;     // [n+1] {lb, ub} of the round's input bounds (compact gathers)
   long long* key_out;
   DevState* st;
   Dirty dirty;
@@ -373,7 +415,7 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, in
 // Per variable (par_engine.cpp:191-197): count sides with out != in, flag
 // lo_out > up_out + abs, and write the next round's snapshot record.  The
 // last CTA takes the round decision of run_parallel (par_engine.cpp:248-266).
-__device__ __forceinline__ void commit_body(Snap* __restrict__ snap,
+__device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __restrict__ bnd,
                                             const longlong2* __restrict__ key_out, int n,
                                             DevState* __restrict__ st, long long* __restrict__ per_round,
                                             const DevCfg& cfg, const Dirty& D,
@@ -385,10 +427,25 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap,
   const int cb = nb ^ 1;                            // buffer this round consumed
   const int gstride = gridDim.x * blockDim.x;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
-  for (int j = gtid; j < n; j += gstride) {
-    const longlong2 ko = key_out[j];
+  constexpr int U = 4;  // columns in flight per thread
+  for (int j0 = gtid; j0 < n; j0 += U * gstride) {
+    longlong2 kob[U];
+    double2 inb[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int j = j0 + u * gstride;
+      if (j < n) {
+        kob[u] = key_out[j];
+        inb[u] = *reinterpret_cast<const double2*>(&snap[j].lo);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+    const int j = j0 + u * gstride;
+    if (j >= n) break;
+    const longlong2 ko = kob[u];
     const double lo = key_dec(ko.x), up = key_dec(-ko.y);
-    const double2 in = *reinterpret_cast<const double2*>(&snap[j].lo);
+    const double2 in = inb[u];
     // a change is a strict improvement, so comparing values is exact
     const int c = (lo != in.x) + (up != in.y);
     if (c) {
@@ -396,6 +453,7 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap,
       const bool integral = snap[j].flags & 1;
       Snap s = {lo, up, column_q(lo, up, integral, cfg), snap[j].flags};
       snap[j] = s;
+      bnd[j] = make_double2(lo, up);
     }
     if (D.enabled) {
       // changed columns of this round -> list (one atomic per warp)
@@ -410,6 +468,7 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap,
       }
     }
     if (lo > __dadd_rn(up, cfg.imp_abs)) inf = 1;
+    }
   }
   if (D.enabled) {
     // the consumed marks become the round-after-next's mark set
@@ -446,9 +505,13 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap,
       st->wl_short = 0;
       st->wl_long = 0;
       st->work = 0;
+      st->work2 = 0;
       st->cand_work = 0;
-      st->full = 0;
+      // many changed columns: the next round is a full sweep (no marks)
+      st->full = *((volatile int32_t*)&st->nchg[cb]) > D.dense_nchg ? 1 : 0;
       st->nchg[nb] = 0;  // the list k_mark consumed after the previous commit
+      st->nwide[cb] = 0;  // this round's unit lists
+      st->nunit[cb] = 0;
       __threadfence();
       if (use_graph) cudaGraphSetConditional(cond, status >= 0 ? 0u : 1u);
     }
@@ -456,17 +519,17 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap,
 }
 
 __global__ void __launch_bounds__(kCommitThreads)
-    k_commit(Snap* __restrict__ snap, const longlong2* __restrict__ key_out, int n,
-             DevState* __restrict__ st, long long* __restrict__ per_round, const DevCfg cfg,
+    k_commit(Snap* __restrict__ snap, double2* __restrict__ bnd, const longlong2* __restrict__ key_out,
+             int n, DevState* __restrict__ st, long long* __restrict__ per_round, const DevCfg cfg,
              const Dirty D, cudaGraphConditionalHandle cond, int use_graph) {
-  commit_body(snap, key_out, n, st, per_round, cfg, D, cond, use_graph);
+  commit_body(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph);
 }
 
 // Start of a solve: snapshot records and merge keys from the (normalised)
 // start bounds, state reset, bounds_crossed pre-check (engine_common.hpp:51-58).
 __global__ void __launch_bounds__(kCommitThreads)
     k_reset(const double* __restrict__ lo0, const double* __restrict__ up0,
-            const uint8_t* __restrict__ integral, Snap* __restrict__ snap,
+            const uint8_t* __restrict__ integral, Snap* __restrict__ snap, double2* __restrict__ bnd,
             longlong2* __restrict__ key_out, int n, DevState* __restrict__ st, const DevCfg cfg,
             const Dirty D, const NodeCtl* __restrict__ ctl, int check_crossed,
             cudaGraphConditionalHandle cond, int use_graph) {
@@ -481,6 +544,7 @@ __global__ void __launch_bounds__(kCommitThreads)
     const double l = lo0[j], u = up0[j];
     const bool in = integral[j] != 0;
     snap[j] = Snap{l, u, column_q(l, u, in, cfg), in ? 1LL : 0LL};
+    bnd[j] = make_double2(l, u);
     key_out[j] = make_longlong2(key_enc(l), -key_enc(u));
     if (l > __dadd_rn(u, cfg.imp_abs)) crossed = 1;
     if (in && (l != floor(l) || u != ceil(u))) frac = 1;  // floor(+-inf) = +-inf
@@ -506,11 +570,14 @@ __global__ void __launch_bounds__(kCommitThreads)
       st->wl_short = 0;
       st->wl_long = 0;
       st->work = 0;
+      st->work2 = 0;
       st->cand_work = 0;
       // warm start from a root fixpoint: round 1 visits only the rows that
       // k_mark_vars marks (see NodeCtl)
       st->full = (D.enabled && ctl->warm) ? 0 : 1;
       st->nchg[0] = st->nchg[1] = 0;
+      st->nwide[0] = st->nwide[1] = 0;
+      st->nunit[0] = st->nunit[1] = 0;
       st->frac_any = atomicAdd(&st->frac_tmp, 0);
       st->frac_tmp = 0;
       st->ticket_reset = 0;
@@ -579,14 +646,17 @@ __global__ void k_permute_rows(const int32_t* __restrict__ rp, const int32_t* __
 // overridden column can produce anything; marking exactly those keeps the
 // trajectory identical to a full sweep.
 __global__ void __launch_bounds__(256)
-    k_mark_vars(const Dirty D, const NodeCtl* __restrict__ ctl) {
+    k_mark_vars(const Dirty D, const NodeCtl* __restrict__ ctl, DevState* __restrict__ st) {
   if (!D.enabled || !ctl->warm) return;
   uint8_t* flag = D.row_flag + (size_t)1 * D.ms;  // round 1 reads buffer (0 + 1) & 1
   const int lane = threadIdx.x & 31;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < ctl->nvars;
        w += (gridDim.x * blockDim.x) >> 5) {
     const int j = ctl->vars[w];
-    for (int e = D.col_ptr[j] + lane; e < D.col_ptr[j + 1]; e += 32) flag[D.col_row[e]] = 1;
+    for (int e = D.col_ptr[j] + lane; e < D.col_ptr[j + 1]; e += 32) {
+      const int r = D.col_row[e];
+      if (mark_row(flag, r)) mark_row_units(D, r, 1, st);
+    }
   }
 }
 
@@ -611,7 +681,7 @@ __global__ void k_apply_node(double* __restrict__ lo0, double* __restrict__ up0,
 // column changed in round r (one warp per changed column).
 __device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__ st) {
   const int r = *((volatile int32_t*)&st->round);
-  if (!D.enabled || *((volatile int32_t*)&st->done)) return;
+  if (!D.enabled || *((volatile int32_t*)&st->done) || *((volatile int32_t*)&st->full)) return;
   const int cb = r & 1, nb = (r + 1) & 1;
   const int nchg = *((volatile int32_t*)&st->nchg[cb]);
   uint8_t* flag = D.row_flag + (size_t)nb * D.ms;
@@ -621,7 +691,25 @@ __device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__
     const int j = D.chg_list[(size_t)cb * D.n + w];
     for (int e = D.col_ptr[j] + lane; e < D.col_ptr[j + 1]; e += 32) {
       const int row = D.col_row[e];
-      if (!flag[row]) flag[row] = 1;  // read first: most rows are marked repeatedly
+      // the common case -- a whole row in a one-lane slice -- is appended
+      // with one atomic per warp
+      bool single = false;
+      int u = -1;
+      if (mark_row(flag, row)) {
+        u = D.row_unit[row];
+        single = u >= 0 && D.unit_slice[u] < 0;
+        if (!single) mark_row_units(D, row, nb, st);
+      }
+      const unsigned act = __activemask();
+      const unsigned bal = __ballot_sync(act, single);
+      if (bal) {
+        const int leader = __ffs(act) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&st->nunit[nb], __popc(bal));
+        base = __shfl_sync(act, base, leader);
+        if (single)
+          D.unit_list[(size_t)nb * D.nunits + base + __popc(bal & ((1u << lane) - 1u))] = u;
+      }
     }
   }
 }

@@ -37,26 +37,31 @@ __device__ __forceinline__ void grid_barrier(DevState* st) {
 union LoopSmem {
   SellWarpSmem sell[kSellWarps];
   CandWarpSmem cand[kCandWarps];
+  SplitSmem<64> split[kSellWarps];
 };
 
 template <bool kRowCheck>
 __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB)
     k_loop(const RoundArgs A, const DevCfg cfg, Snap* __restrict__ snap, int n,
-           long long* __restrict__ per_round) {
-  __shared__ LoopSmem sm;
+           long long* __restrict__ per_round, const int32_t* __restrict__ split, int nsplit) {
+  extern __shared__ __align__(16) unsigned char loop_dyn[];  // LoopSmem
+  LoopSmem& sm = *reinterpret_cast<LoopSmem*>(loop_dyn);
   longlong2* key_out = reinterpret_cast<longlong2*>(A.key_out);
   while (!*((volatile int32_t*)&A.st->done)) {
-    const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
-    if (full)
+    if (sell_dense_round(A))
       sell_sweep<kRowCheck, true>(A, cfg, sm.sell);
     else
       sell_sweep<kRowCheck, false>(A, cfg, sm.sell);
     grid_barrier(A.st);
+    if (nsplit) {
+      split_finish_body<kRowCheck, 64>(A, split, nsplit, sm.split, cfg);
+      grid_barrier(A.st);
+    }
     if (*((volatile int32_t*)&A.st->wl_long)) {
       cand_sweep(A, cfg, sm.cand);
       grid_barrier(A.st);
     }
-    commit_body(snap, key_out, n, A.st, per_round, cfg, A.dirty, 0, 0);
+    commit_body(snap, const_cast<double2*>(A.bnd), key_out, n, A.st, per_round, cfg, A.dirty, 0, 0);
     grid_barrier(A.st);
     if (A.dirty.enabled) {
       mark_body(A.dirty, A.st);

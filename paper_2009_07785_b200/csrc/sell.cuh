@@ -30,6 +30,7 @@
 
 #include "kernels.cuh"
 #include "setup.cuh"
+#include "split.cuh"
 
 namespace pgb {
 
@@ -42,8 +43,26 @@ namespace pgb {
 #ifndef PG_SELL_PF
 #define PG_SELL_PF 1
 #endif
+#ifndef PG_SELL_B16
+#define PG_SELL_B16 1  // gather 16 B {lb, ub} from the compact bounds array
+#endif
+#ifndef PG_SELL_ASYNC
+#define PG_SELL_ASYNC 0  // dense chains through a per-lane cp.async ring
+#endif
+#ifndef PG_SELL_DEPTH
+#define PG_SELL_DEPTH 8
+#endif
 #ifndef PG_SELL_GROUP
 #define PG_SELL_GROUP 2  // narrow one-lane slices per work item
+#endif
+#ifndef PG_SELL_B16
+#define PG_SELL_B16 1  // gather 16 B {lb, ub} from the compact bounds array
+#endif
+#ifndef PG_SELL_ASYNC
+#define PG_SELL_ASYNC 0  // dense chains through a per-lane cp.async ring
+#endif
+#ifndef PG_SELL_DEPTH
+#define PG_SELL_DEPTH 8
 #endif
 #ifndef PG_SELL_GROUPW
 #define PG_SELL_GROUPW 16  // slices at most this wide are grouped
@@ -67,6 +86,7 @@ constexpr int kSellUnroll = PG_SELL_UNROLL;
 constexpr int kSellThreads = 256;
 constexpr int kSellWarps = kSellThreads / 32;
 constexpr int kSellGroup = PG_SELL_GROUP;
+constexpr int kSellLaneUnit = 16;  // worklist rounds: longer units get a warp each
 // lanes per unit by unit length: > 256 -> 8, > 128 -> 4, > 64 -> 2, else 1
 constexpr int kSellG8 = 256, kSellG4 = 128, kSellG2 = 64;
 
@@ -116,6 +136,34 @@ __device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
 
+// filter coefficient from the bounds (column_q): an infinite bound makes
+// (up - lo) infinite; a NaN (both bounds the same infinity) reads as +inf
+__device__ __forceinline__ double column_q_inline(double lo, double up, bool integral,
+                                                  bool frac_any, const DevCfg& c) {
+  const double thr = integral ? c.int_eps : c.imp_abs + c.imp_rel;
+  double q = ((up - lo) - thr) + (fabs(lo) + fabs(up)) * kMargin;
+  if (frac_any && integral && (lo != floor(lo) || up != ceil(up))) q = CUDART_INF;
+  return q == q ? q : CUDART_INF;
+}
+
+// the gathered record of column c: {lb, ub} and the filter coefficient q --
+// 16 B from the compact bounds array (half the L2 footprint of the snapshot
+// records; q recomputed, column_q) or the 32 B snapshot record
+__device__ __forceinline__ void ld_col(const RoundArgs& A, int32_t c, uint64_t pol, bool frac_any,
+                                       const DevCfg& cfg, double& lo, double& up, double& q) {
+#if PG_SELL_B16
+  double2 b;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+               : "=d"(b.x), "=d"(b.y)
+               : "l"(A.bnd + (c & 0x7fffffff)), "l"(pol));
+  lo = b.x;
+  up = b.y;
+  q = column_q_inline(lo, up, c < 0, frac_any, cfg);
+#else
+  ld_snap_keep(A.snap + (c & 0x7fffffff), pol, lo, up, q);
+#endif
+}
+
 // ---- filter words -----------------------------------------------------------------
 // |a| q rounded toward +inf to float; bit 0 = min contribution infinite,
 // bit 1 = max contribution infinite.  +inf / NaN terms read back as NaN,
@@ -144,7 +192,16 @@ struct SellWarpSmem {
   // entries that survive the filter: element offset in the slice, unit
   int32_t qe[64];
   uint8_t qu[64];
+  double2 wbuf[256];  // worklist rounds: {min, max} contributions of a wide unit's block
+#if PG_SELL_ASYNC
+  // per lane, PG_SELL_DEPTH steps in flight: the {lb, ub} record and the
+  // value of each step land here by cp.async (no registers held)
+  double2 rrec[PG_SELL_DEPTH][32];
+  double ra[PG_SELL_DEPTH][32];
+#endif
 };
+
+constexpr size_t kSellSmem = sizeof(SellWarpSmem) * kSellWarps;
 
 // exact pipeline over queue entries [0, cnt), one per lane
 __device__ __forceinline__ bool sell_drain(const RoundArgs& A, const SellWarpSmem& W,
@@ -157,7 +214,7 @@ __device__ __forceinline__ bool sell_drain(const RoundArgs& A, const SellWarpSme
     const double a = A.sv[e];
     const int32_t c = A.sc[e];
     double lo, up, q;
-    ld_snap_keep(A.snap + (c & 0x7fffffff), pol_keep, lo, up, q);
+    ld_col(A, c, pol_keep, *((volatile int32_t*)&A.st->frac_any) != 0, cfg, lo, up, q);
     const Act act = {W.min_f[u], W.max_f[u], W.min_i[u], W.max_i[u]};
     inf_flag = entry_pipeline(act, a, lo, up, W.lhs[u], W.rhs[u], c, A.key_out, cfg);
   }
@@ -196,6 +253,21 @@ __device__ __forceinline__ void sell_step(double a, double lo, double up, double
       act.max_f = __dadd_rn(act.max_f, vmax);
     }
   }
+}
+
+// a chunk of a split row: its partial record; after the sweep,
+// k_split_finish combines the partials of every row whose chunks all ran
+template <bool kRowCheck>
+__device__ __forceinline__ void chunk_done(const RoundArgs& A, const UnitDesc& ud, const Act& act,
+                                           double xmax, bool& inf_flag, const DevCfg& cfg) {
+  const SegDesc d = A.segs[-ud.ref - 1];
+  volatile SegPartial* P = A.partial + d.out;
+  P->min_f = act.min_f;
+  P->max_f = act.max_f;
+  P->xmax = xmax;
+  P->min_i = act.min_i;
+  P->max_i = act.max_i;
+  atomicAdd(&A.row_done[d.rslot], 1);  // k_split_finish combines complete rows
 }
 
 // Second half of a slice, after its chains: order-free reductions over a
@@ -238,21 +310,7 @@ __device__ __forceinline__ void slice_tail(const RoundArgs& A, SellWarpSmem& W, 
       W.tl[u] = f.tl;
       W.mode[u] = f.mode;
     } else {
-      // a chunk of a split row: partial record; the last chunk combines them
-      const SegDesc d = A.segs[-ud.ref - 1];
-      volatile SegPartial* P = A.partial + d.out;
-      P->min_f = act.min_f;
-      P->max_f = act.max_f;
-      P->xmax = xmax;
-      P->min_i = act.min_i;
-      P->max_i = act.max_i;
-      __threadfence();
-      const int nch = A.sfirst[d.rslot + 1] - A.sfirst[d.rslot];
-      if (atomicAdd(&A.row_done[d.rslot], 1) == nch - 1) {
-        __threadfence();
-        A.row_done[d.rslot] = 0;
-        finish_split_row<kRowCheck>(A, d.rslot, inf_flag, cfg);
-      }
+      chunk_done<kRowCheck>(A, ud, act, xmax, inf_flag, cfg);
     }
   }
   if (j == 0) W.may[u] = may;
@@ -304,6 +362,72 @@ __device__ __forceinline__ void slice_tail(const RoundArgs& A, SellWarpSmem& W, 
   __syncwarp();
 }
 
+// ---- dense chains through a per-lane cp.async ring --------------------------------
+__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+
+#if PG_SELL_ASYNC
+// Every lane keeps PG_SELL_DEPTH steps of its chain in flight: the column
+// index of a step is loaded a block ahead into registers, the 16 B {lb, ub}
+// gather and the value go to shared memory by cp.async (per-lane groups, no
+// barrier), and a step is consumed in entry order once its group landed.
+template <int LG>
+__device__ __forceinline__ void sell_chain_async(const double* sv, const int32_t* sc, uint32_t* sw,
+                                                 int steps, int u, int lane, const double2* bnd,
+                                                 SellWarpSmem& W, bool frac_any, const DevCfg& cfg,
+                                                 Act& act, double& xmax) {
+  constexpr int D = PG_SELL_DEPTH;
+  int32_t cc[D], cn[D];
+#pragma unroll
+  for (int d = 0; d < D; ++d) {
+    cc[d] = 0;
+    if (d < steps) {
+      cc[d] = __ldg(sc + 32 * d);
+      cp_async16(&W.rrec[d][lane], bnd + (cc[d] & 0x7fffffff));
+      cp_async8(&W.ra[d][lane], sv + 32 * d);
+    }
+    cp_async_commit();
+  }
+#pragma unroll
+  for (int d = 0; d < D; ++d) cn[d] = D + d < steps ? __ldg(sc + 32 * (D + d)) : 0;
+  for (int t0 = 0; t0 < steps; t0 += D) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int t = t0 + d;
+      cp_async_wait<D - 1>();
+      if (t < steps) {
+        const double2 b = W.rrec[d][lane];
+        const double a = W.ra[d][lane];
+        const double q = column_q_inline(b.x, b.y, cc[d] < 0, frac_any, cfg);
+        sell_step<LG>(a, b.x, b.y, q, u, act, xmax, sw + 32 * t);
+      }
+      if (t + D < steps) {
+        cp_async16(&W.rrec[d][lane], bnd + (cn[d] & 0x7fffffff));
+        cp_async8(&W.ra[d][lane], sv + 32 * (t + D));
+      }
+      cp_async_commit();
+      cc[d] = cn[d];
+      cn[d] = t + 2 * D < steps ? __ldg(sc + 32 * (t + 2 * D)) : 0;
+    }
+  }
+  cp_async_wait<0>();
+}
+#endif
+
 // One slice by one warp.  LG = log2(lanes per unit); kDense: a full sweep
 // (no worklist), every lane walks every step of the slice.
 template <bool kRowCheck, int LG, bool kDense>
@@ -329,11 +453,17 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
   uint32_t* sw = A.sw + sd.off + lane;
   const bool whole = ud.ref >= 0;
   const int steps = sd.steps;
+  const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
 
   // ---- phase 1: the chains ------------------------------------------------------
   Act act = {0.0, 0.0, 0, 0};
   double xmax = -CUDART_INF;
-  if (kDense) {
+  if (kDense && PG_SELL_ASYNC) {
+#if PG_SELL_ASYNC
+    sell_chain_async<LG>(sv, sc, sw, steps, u, lane, A.bnd, W,
+                         *((volatile int32_t*)&A.st->frac_any) != 0, cfg, act, xmax);
+#endif
+  } else if (kDense) {
     constexpr int UL = LG >= PG_SELL_LGU ? PG_SELL_ULONG : kSellUnroll;
     // every lane walks all `steps` of the slice: entries past a unit's end are
     // padding (value 0, the padding column with bounds [0, 0]) and add +0.0
@@ -358,7 +488,7 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
       double lo[UL], up[UL], q[UL];
 #pragma unroll
       for (int k = 0; k < UL; ++k)
-        ld_snap_keep(A.snap + (c[k] & 0x7fffffff), pol_keep, lo[k], up[k], q[k]);
+        ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
       // the next group's values and columns are in flight during this one
       double an[UL];
       int32_t cn[UL];
@@ -388,7 +518,7 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
       const double a1 = ld_stream_f64(pa, pol_stream);
       const int32_t c1 = ld_stream_s32(pc, pol_stream);
       double lo1, up1, q1;
-      ld_snap_keep(A.snap + (c1 & 0x7fffffff), pol_keep, lo1, up1, q1);
+      ld_col(A, c1, pol_keep, frac_any, cfg, lo1, up1, q1);
       sell_step<LG>(a1, lo1, up1, q1, u, act, xmax, pw);
       pa += 32;
       pc += 32;
@@ -412,11 +542,15 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
       }
 #pragma unroll
       for (int k = 0; k < kSellUnroll; ++k)
-        ld_snap_keep(A.snap + (c[k] & 0x7fffffff), pol_keep, lo[k], up[k], q[k]);
+        ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
 #pragma unroll
       for (int k = 0; k < kSellUnroll; ++k)
         if (t0 + k < steps) sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xmax, sw + 32 * (t0 + k));
     }
+  }
+  if (PG_SELL_DEBUG && (cfg.flags & 0x40000u)) {  // timing experiments only: chains alone
+    if (act.min_f == 12345.678 && xmax == 1.0) A.st->infeasible = 1;
+    return;
   }
   slice_tail<kRowCheck, LG>(A, W, sd, ud, active, len, lane, act, xmax, ud.ref >= 0 ? A.lhs[ud.ref] : 0.0,
                             ud.ref >= 0 ? A.rhs[ud.ref] : 0.0, pol_keep, inf_flag, cfg);
@@ -460,6 +594,7 @@ __device__ __forceinline__ void sell_group(const RoundArgs& A, SellWarpSmem& W, 
     xmax[r] = -CUDART_INF;
   }
   const int tmax = steps[0];  // the group's first slice is its widest
+  const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
   double a[R];
   int32_t c[R];
 #pragma unroll
@@ -474,7 +609,7 @@ __device__ __forceinline__ void sell_group(const RoundArgs& A, SellWarpSmem& W, 
   for (int t = 0; t < tmax; ++t) {
     double lo[R], up[R], q[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) ld_snap_keep(A.snap + (c[r] & 0x7fffffff), pol_keep, lo[r], up[r], q[r]);
+    for (int r = 0; r < R; ++r) ld_col(A, c[r], pol_keep, frac_any, cfg, lo[r], up[r], q[r]);
     double an[R];
     int32_t cn[R];
 #pragma unroll
@@ -509,6 +644,177 @@ __device__ __forceinline__ void sell_group(const RoundArgs& A, SellWarpSmem& W, 
 // otherwise a worklist round (only the marked rows' units).  Both are
 // launched when the worklist is on; the one that does not match the round
 // returns at once (the round's kind is known on the device only).
+// Worklist round, multi-lane (long) units: a warp per unit over its CSR
+// entries (coalesced), 256 entries per block; the lanes form the
+// contributions, lane 0 adds them in entry order from shared memory (the
+// reference's chain), then row finish and phase 2 with the exact filter.
+template <bool kRowCheck>
+__device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, int par,
+                                          uint64_t pol_keep, bool& inf_flag, const DevCfg& cfg) {
+  const int lane = threadIdx.x & 31;
+  const int nw = *((volatile int32_t*)&A.st->nwide[par]);
+  const int32_t* wl = A.dirty.wide_list + (size_t)par * A.dirty.nunits;
+  const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
+  // static striding by warp (few, similar items: no ticket contention)
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (int t = gw; t < nw; t += nwarps) {
+    const int u = wl[t];
+    const UnitDesc ud = A.units[u];
+    const int k0 = ud.ref >= 0 ? A.row_ptr[ud.ref] : A.segs[-ud.ref - 1].k0;
+    const int len = ud.len;
+    int cmin = 0, cmax = 0;
+    double xm = -CUDART_INF, smin = 0.0, smax = 0.0;
+    for (int base = 0; base < len; base += 256) {
+#pragma unroll
+      for (int s8 = 0; s8 < 8; ++s8) {
+        const int e = base + 32 * s8 + lane;
+        double pmin = 0.0, pmax = 0.0;
+        if (e < len) {
+          const double a = A.vals[k0 + e];
+          const int32_t c = A.colx[k0 + e];
+          double lo, up, q;
+          ld_col(A, c, pol_keep, frac_any, cfg, lo, up, q);
+          const double bmin = a > 0 ? lo : up;
+          const double bmax = a > 0 ? up : lo;
+          const bool imin = isinf(bmin), imax = isinf(bmax);
+          pmin = imin ? 0.0 : __dmul_rn(a, bmin);
+          pmax = imax ? 0.0 : __dmul_rn(a, bmax);
+          cmin += imin;
+          cmax += imax;
+          xm = fmax(xm, fabs(a) * q);
+        }
+        W.wbuf[32 * s8 + lane] = make_double2(pmin, pmax);
+      }
+      __syncwarp();
+      if (lane < 2) {
+        // lane 0 runs the min chain, lane 1 the max chain, in entry order
+        // (a block is padded with +0.0 entries, which add exactly)
+        const double* wb = reinterpret_cast<const double*>(W.wbuf) + lane;
+        const int nb = min(256, len - base);
+        double acc = lane ? smax : smin;
+        for (int i = 0; i < nb; i += 8) {
+          double v[8];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) v[k] = wb[2 * (i + k)];
+#pragma unroll
+          for (int k = 0; k < 8; ++k) acc = __dadd_rn(acc, v[k]);
+        }
+        if (lane) smax = acc; else smin = acc;
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      cmin += __shfl_xor_sync(0xffffffffu, cmin, o);
+      cmax += __shfl_xor_sync(0xffffffffu, cmax, o);
+      xm = fmax(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+    }
+    const Act act = {__shfl_sync(0xffffffffu, smin, 0), __shfl_sync(0xffffffffu, smax, 1), cmin, cmax};
+    if (ud.ref < 0) {
+      if (lane == 0) chunk_done<kRowCheck>(A, ud, act, xm, inf_flag, cfg);
+      continue;
+    }
+    const double l = A.lhs[ud.ref], h = A.rhs[ud.ref];
+    if (kRowCheck && lane == 0 && row_infeasible(act, l, h, cfg)) inf_flag = true;
+    const RowFilter f = row_filter(act, l, h);
+    if (!row_may(f, xm)) continue;
+    // phase 2: 8 entries per lane in flight, then the survivors' pipeline
+    for (int e0 = 0; e0 < len; e0 += 256) {
+      double a[8], lo[8], up[8];
+      int32_t c[8];
+      unsigned pass = 0;
+#pragma unroll
+      for (int s8 = 0; s8 < 8; ++s8) {
+        const int e = e0 + 32 * s8 + lane;
+        a[s8] = 0.0;
+        c[s8] = A.pad_col;
+        if (e < len) {
+          a[s8] = A.vals[k0 + e];
+          c[s8] = A.colx[k0 + e];
+        }
+      }
+#pragma unroll
+      for (int s8 = 0; s8 < 8; ++s8) {
+        double q;
+        ld_col(A, c[s8], pol_keep, frac_any, cfg, lo[s8], up[s8], q);
+        const double bmin = a[s8] > 0 ? lo[s8] : up[s8];
+        const double bmax = a[s8] > 0 ? up[s8] : lo[s8];
+        if (e0 + 32 * s8 + lane < len && entry_may(f, fabs(a[s8]) * q, isinf(bmin), isinf(bmax)))
+          pass |= 1u << s8;
+      }
+#pragma unroll
+      for (int s8 = 0; s8 < 8; ++s8)
+        if ((pass >> s8) & 1u)
+          if (entry_pipeline(act, a[s8], lo[s8], up[s8], l, h, c[s8], A.key_out, cfg)) inf_flag = true;
+    }
+  }
+}
+
+// Worklist round, one-lane units: a warp takes 32 marked units (any slices),
+// one per lane; the chain reads the unit's column of its slice (entry i at
+// off + 32 i + position), then row finish and an in-lane phase 2 over the
+// unit's filter words.  Exact like the slice path; used when few rows are
+// marked, so the uncoalesced lane streams do not matter.
+template <bool kRowCheck>
+__device__ __forceinline__ void sell_units(const RoundArgs& A, int par, uint64_t pol_keep,
+                                           bool& inf_flag, const DevCfg& cfg) {
+  const int lane = threadIdx.x & 31;
+  const int nu = *((volatile int32_t*)&A.st->nunit[par]);
+  const int32_t* ul = A.dirty.unit_list + (size_t)par * A.dirty.nunits;
+  const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
+  // static striding: warp w takes batches w, w + W, .. of 32 units (the
+  // batches after the wide units' warps, so both kinds start at once)
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  const int nwide = *((volatile int32_t*)&A.st->nwide[par]);
+  for (int b = (gw + nwarps - nwide % nwarps) % nwarps; 32 * b < nu; b += nwarps) {
+    const int i = 32 * b + lane;
+    if (i >= nu) continue;
+    const int u = ul[i];
+    const UnitDesc ud = A.units[u];
+    const int k = u - A.lg0_ustart;
+    const long long off = A.slices[A.lg0_sstart + (k >> 5)].off + (k & 31);
+    const double* sv = A.sv + off;
+    const int32_t* sc = A.sc + off;
+    uint32_t* sw = A.sw + off;
+    Act act = {0.0, 0.0, 0, 0};
+    double xmax = -CUDART_INF;
+    for (int t0 = 0; t0 < ud.len; t0 += 4) {
+      double a[4], lo[4], up[4], q[4];
+      int32_t c[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        a[k] = 0.0;
+        c[k] = A.pad_col;
+        if (t0 + k < ud.len) {
+          a[k] = sv[32 * (t0 + k)];
+          c[k] = sc[32 * (t0 + k)];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (t0 + k < ud.len) sell_step<0>(a[k], lo[k], up[k], q[k], 0, act, xmax, sw + 32 * (t0 + k));
+    }
+    if (ud.ref < 0) {
+      chunk_done<kRowCheck>(A, ud, act, xmax, inf_flag, cfg);
+      continue;
+    }
+    const double l = A.lhs[ud.ref], h = A.rhs[ud.ref];
+    if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
+    const RowFilter f = row_filter(act, l, h);
+    if (!row_may(f, xmax)) continue;
+    for (int t = 0; t < ud.len; ++t) {
+      if (!filt_may(f, sw[32 * t])) continue;
+      const double a = sv[32 * t];
+      const int32_t c = sc[32 * t];
+      double lo, up, q;
+      ld_col(A, c, pol_keep, frac_any, cfg, lo, up, q);
+      if (entry_pipeline(act, a, lo, up, l, h, c, A.key_out, cfg)) inf_flag = true;
+    }
+  }
+}
+
 template <bool kRowCheck, bool kDense>
 __device__ __forceinline__ void sell_sweep(const RoundArgs& A, const DevCfg& cfg,
                                            SellWarpSmem* smem) {
@@ -520,6 +826,13 @@ __device__ __forceinline__ void sell_sweep(const RoundArgs& A, const DevCfg& cfg
   const uint64_t pk = l2_policy_evict_last();
   const uint64_t ps = l2_policy_evict_first();
   bool inf_flag = false;
+  if (!kDense) {
+    // worklist round: only the units of the marked rows
+    if (!(PG_SELL_DEBUG && (cfg.flags & 0x80000u))) sell_wide<kRowCheck>(A, W, par, pk, inf_flag, cfg);
+    if (!(PG_SELL_DEBUG && (cfg.flags & 0x100000u))) sell_units<kRowCheck>(A, par, pk, inf_flag, cfg);
+    if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
+    return;
+  }
   int next = 0;
   if (lane == 0) next = atomicAdd(&A.st->work, 1);
   next = __shfl_sync(0xffffffffu, next, 0);
@@ -565,12 +878,24 @@ __device__ __forceinline__ void sell_sweep(const RoundArgs& A, const DevCfg& cfg
   if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
 }
 
+// a full sweep: no worklist, the first round, or more than half of the
+// slices dirty (then visiting all of them is cheaper than the list; exact
+// either way)
+__device__ __forceinline__ bool sell_dense_round(const RoundArgs& A) {
+  if (!A.dirty.enabled || *((volatile int32_t*)&A.st->full)) return true;
+  const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
+  // marked one-lane units + 8 per long unit, against a quarter of all units
+  const long long work = (long long)*((volatile int32_t*)&A.st->nunit[par]) +
+                         8LL * *((volatile int32_t*)&A.st->nwide[par]);
+  return 4 * work > (long long)A.nunits;
+}
+
 template <bool kRowCheck, bool kDense>
 __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const RoundArgs A,
                                                                      const DevCfg cfg) {
-  __shared__ SellWarpSmem smem[kSellWarps];
-  const bool full = !A.dirty.enabled || *((volatile int32_t*)&A.st->full);
-  if (full != kDense) return;
+  extern __shared__ __align__(16) unsigned char sell_dyn[];  // kSellWarps x SellWarpSmem
+  SellWarpSmem* smem = reinterpret_cast<SellWarpSmem*>(sell_dyn);
+  if (sell_dense_round(A) != kDense) return;
   sell_sweep<kRowCheck, kDense>(A, cfg, smem);
 }
 
@@ -689,6 +1014,27 @@ __global__ void k_fill_sell(const UnitDesc* __restrict__ units, const int32_t* _
       d.off = o;
       slices[s] = d;
     }
+  }
+}
+
+// worklist maps: whole row -> unit, chunk (partial index) -> unit, unit -> slice
+__global__ void k_unit_maps(const UnitDesc* __restrict__ units, int nunits,
+                            const SegDesc* __restrict__ segs, int32_t* __restrict__ row_unit,
+                            int32_t* __restrict__ part_unit) {
+  for (int u = blockIdx.x * blockDim.x + threadIdx.x; u < nunits; u += gridDim.x * blockDim.x) {
+    const UnitDesc d = units[u];
+    if (d.ref >= 0) row_unit[d.ref] = u;
+    else part_unit[segs[-d.ref - 1].out] = u;
+  }
+}
+// unit_slice < 0: a short one-lane unit, visited by a lane in worklist
+// rounds; otherwise (longer units) by a warp
+__global__ void k_slice_units(const SliceDesc* __restrict__ slices, int nslices,
+                              const UnitDesc* __restrict__ units, int32_t* __restrict__ unit_slice) {
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nslices; s += gridDim.x * blockDim.x) {
+    const SliceDesc d = slices[s];
+    for (int i = 0; i < d.count; ++i)
+      unit_slice[d.first + i] = (d.lg == 0 && units[d.first + i].len <= kSellLaneUnit) ? -1 : s;
   }
 }
 
