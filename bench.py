@@ -421,7 +421,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--nodes", type=int, default=8192, help="C4: number of B&B nodes")
-    ap.add_argument("--worklist", type=int, default=0, help="device-side worklist (exact)")
+    ap.add_argument("--worklist", type=int, default=None,
+                    help="device-side worklist (exact); default: on for c5 (cascading fixings), "
+                         "off otherwise (the dense sweep is faster there)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--loop", default="graph", choices=["graph", "host"],
                     help="host: one launch per kernel per round (for ncu launch lists: ncu "
@@ -429,6 +431,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.worklist is None:
+        args.worklist = args.config == "c5"
     args.worklist = bool(args.worklist)
 
     world, rank, local = dist_init()

@@ -112,8 +112,8 @@ __device__ __forceinline__ void cand_sweep(const RoundArgs& A, const DevCfg& cfg
                                            CandWarpSmem* smem) {
   const int lane = threadIdx.x & 31;
   CandWarpSmem& W = smem[threadIdx.x >> 5];
-  const int nlong = *((volatile int32_t*)&A.st->wl_long);
-  const int nshort = *((volatile int32_t*)&A.st->wl_short);
+  const int nlong = ld_gpu(&A.st->wl_long);
+  const int nshort = ld_gpu(&A.st->wl_short);
   const int nbatch = (nshort + 31) / 32;
   bool inf_flag = false;
   for (;;) {

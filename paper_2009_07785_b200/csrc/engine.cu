@@ -377,9 +377,9 @@ struct pg_session {
                                        kNcclMax, comm, stream);
       if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllReduce: ") + g_nccl.error(rc)};
     }
-    k_commit<<<grid_for(n, kCommitThreads), kCommitThreads, 0, stream>>>(
+    k_commit<<<grid_for(n, kCommitThreads, 4), kCommitThreads, 0, stream>>>(
         d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0);
-    if (dirty.enabled) k_mark<<<num_sms * 8, 256, 0, stream>>>(dirty, d_st);
+    if (dirty.enabled) k_mark<<<num_sms * 2, 256, 0, stream>>>(dirty, d_st);
     PG_CUDA(cudaGetLastError());
   }
 
@@ -513,7 +513,12 @@ struct pg_session {
       enqueue_reset(false, check_crossed);
       PG_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(DevState), cudaMemcpyDeviceToHost, stream));
       PG_CUDA(cudaStreamSynchronize(stream));
+      static const bool dbg = getenv("PG_DEBUG_ROUNDS") != nullptr;
       while (!h_st->done) {
+        if (dbg)
+          fprintf(stderr, "[pg] round %d: full=%d nunit={%d,%d} nwide={%d,%d} nchg={%d,%d}\n",
+                  h_st->round + 1, h_st->full, h_st->nunit[0], h_st->nunit[1], h_st->nwide[0],
+                  h_st->nwide[1], h_st->nchg[0], h_st->nchg[1]);
         enqueue_round(false);
         PG_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(DevState), cudaMemcpyDeviceToHost, stream));
         PG_CUDA(cudaStreamSynchronize(stream));

@@ -89,7 +89,7 @@ struct Dirty {
 __device__ __forceinline__ bool mark_row(uint8_t* flag, int r) {
   uint32_t* w = reinterpret_cast<uint32_t*>(flag) + (r >> 2);
   const uint32_t bit = 1u << (8 * (r & 3));
-  if (*((volatile uint32_t*)w) & bit) return false;
+  if (ld_gpu(w) & bit) return false;
   return !(atomicOr(w, bit) & bit);
 }
 __device__ __forceinline__ void mark_row_units(const Dirty& D, int r, int par, DevState* st) {
@@ -210,20 +210,26 @@ __device__ __forceinline__ bool entry_may(const RowFilter& f, double x, bool pmi
 }
 
 // ---- exact candidate pipeline ---------------------------------------------------
+// fire-and-forget 64-bit max at L2 (no load before it: a candidate never
+// waits on the current merged value)
+__device__ __forceinline__ void red_max(long long* p, long long k) {
+  asm volatile("red.relaxed.gpu.global.max.s64 [%0], %1;" ::"l"(p), "l"(k) : "memory");
+}
+
 __device__ __forceinline__ void commit_side(long long* key_out, int j, int kind, double cl,
                                             double cu) {
   // merge_lower / merge_upper (par_engine.cpp:56-71) as exact 64-bit max/min
   if (kind & 1) {
     const long long k = key_enc(canon0(cl));
     long long* p = key_out + 2 * (size_t)j;
-    if (*((volatile long long*)p) < k) atomicMax(p, k);
+    red_max(p, k);
   }
   if (kind & 2) {
     // upper bounds are kept as NEGATED keys so that one max-reduction merges
     // both sides (one NCCL all-reduce on the row-sharded path)
     const long long k = -key_enc(canon0(cu));
     long long* p = key_out + 2 * (size_t)j + 1;
-    if (*((volatile long long*)p) < k) atomicMax(p, k);
+    red_max(p, k);
   }
 }
 
@@ -422,13 +428,16 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
                                             cudaGraphConditionalHandle cond, int use_graph) {
   unsigned long long changes = 0;
   int inf = 0;
-  const int R = *((volatile int32_t*)&st->round);  // rounds before this one
+  const int R = ld_gpu(&st->round);  // rounds before this one
   const int nb = R & 1;                             // buffer of the next round's lists
   const int cb = nb ^ 1;                            // buffer this round consumed
   const int gstride = gridDim.x * blockDim.x;
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   constexpr int U = 4;  // columns in flight per thread
-  for (int j0 = gtid; j0 < n; j0 += U * gstride) {
+  const int lane = threadIdx.x & 31;
+  // the loop bound is warp-uniform (j0 - lane is), so the warp stays
+  // converged for the list appends
+  for (int j0 = gtid; j0 - lane < n; j0 += U * gstride) {
     longlong2 kob[U];
     double2 inb[U];
 #pragma unroll
@@ -441,33 +450,32 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-    const int j = j0 + u * gstride;
-    if (j >= n) break;
-    const longlong2 ko = kob[u];
-    const double lo = key_dec(ko.x), up = key_dec(-ko.y);
-    const double2 in = inb[u];
-    // a change is a strict improvement, so comparing values is exact
-    const int c = (lo != in.x) + (up != in.y);
-    if (c) {
-      changes += c;
-      const bool integral = snap[j].flags & 1;
-      Snap s = {lo, up, column_q(lo, up, integral, cfg), snap[j].flags};
-      snap[j] = s;
-      bnd[j] = make_double2(lo, up);
-    }
-    if (D.enabled) {
-      // changed columns of this round -> list (one atomic per warp)
-      const unsigned act = __activemask();
-      const unsigned chm = __ballot_sync(act, c != 0);
-      if (chm) {
-        const int leader = __ffs(act) - 1;
-        int base = 0;
-        if ((int)(threadIdx.x & 31) == leader) base = atomicAdd(&st->nchg[cb], __popc(chm));
-        base = __shfl_sync(act, base, leader);
-        if (c) D.chg_list[(size_t)cb * D.n + base + __popc(chm & ((1u << (threadIdx.x & 31)) - 1u))] = j;
+      const int j = j0 + u * gstride;
+      int c = 0;
+      if (j < n) {
+        const longlong2 ko = kob[u];
+        const double lo = key_dec(ko.x), up = key_dec(-ko.y);
+        const double2 in = inb[u];
+        // a change is a strict improvement, so comparing values is exact
+        c = (lo != in.x) + (up != in.y);
+        if (c) {
+          changes += c;
+          const long long fl = snap[j].flags;
+          snap[j] = Snap{lo, up, column_q(lo, up, fl & 1, cfg), fl};
+          bnd[j] = make_double2(lo, up);
+        }
+        if (lo > __dadd_rn(up, cfg.imp_abs)) inf = 1;
       }
-    }
-    if (lo > __dadd_rn(up, cfg.imp_abs)) inf = 1;
+      if (D.enabled) {
+        // changed columns of this round -> list (one atomic per warp)
+        const unsigned chm = __ballot_sync(0xffffffffu, c != 0);
+        if (chm) {
+          int base = 0;
+          if (lane == 0) base = atomicAdd(&st->nchg[cb], __popc(chm));
+          base = __shfl_sync(0xffffffffu, base, 0);
+          if (c) D.chg_list[(size_t)cb * D.n + base + __popc(chm & ((1u << lane) - 1u))] = j;
+        }
+      }
     }
   }
   if (D.enabled) {
@@ -486,9 +494,9 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
       __threadfence();
       const long long ch = (long long)atomicAdd(&st->round_changes, 0ull);
       // key_out[n].x: the all-reduced infeasibility of every rank (row shards)
-      volatile long long* slot = (volatile long long*)&key_out[n].x;
-      const int infeasible = atomicAdd(&st->infeasible, 0) | (*slot != 0);
-      *slot = 0;
+      long long* slot = const_cast<long long*>(&key_out[n].x);
+      const int infeasible = atomicAdd(&st->infeasible, 0) | (ld_gpu(slot) != 0);
+      st_gpu(slot, 0);
       const int r = R + 1;
       st->round = r;
       if (r - 1 < cfg.round_limit) per_round[r - 1] = ch;
@@ -508,7 +516,7 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
       st->work2 = 0;
       st->cand_work = 0;
       // many changed columns: the next round is a full sweep (no marks)
-      st->full = *((volatile int32_t*)&st->nchg[cb]) > D.dense_nchg ? 1 : 0;
+      st->full = ld_gpu(&st->nchg[cb]) > D.dense_nchg ? 1 : 0;
       st->nchg[nb] = 0;  // the list k_mark consumed after the previous commit
       st->nwide[cb] = 0;  // this round's unit lists
       st->nunit[cb] = 0;
@@ -590,7 +598,7 @@ __global__ void __launch_bounds__(kCommitThreads)
 // Row-sharded rounds: this rank's infeasibility into the slot that rides the
 // bound all-reduce (max over {lb key, -ub key, flag}).
 __global__ void k_flag_to_slot(const DevState* __restrict__ st, longlong2* __restrict__ slot) {
-  if (threadIdx.x == 0) slot->x = *((volatile const int32_t*)&st->infeasible) ? 1 : 0;
+  if (threadIdx.x == 0) slot->x = ld_gpu(&st->infeasible) ? 1 : 0;
 }
 
 // keys -> doubles (result download)
@@ -680,10 +688,10 @@ __global__ void k_apply_node(double* __restrict__ lo0, double* __restrict__ up0,
 // After the commit of round r: mark, for round r + 1, every row containing a
 // column changed in round r (one warp per changed column).
 __device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__ st) {
-  const int r = *((volatile int32_t*)&st->round);
-  if (!D.enabled || *((volatile int32_t*)&st->done) || *((volatile int32_t*)&st->full)) return;
+  const int r = ld_gpu(&st->round);
+  if (!D.enabled || ld_gpu(&st->done) || ld_gpu(&st->full)) return;
   const int cb = r & 1, nb = (r + 1) & 1;
-  const int nchg = *((volatile int32_t*)&st->nchg[cb]);
+  const int nchg = ld_gpu(&st->nchg[cb]);
   uint8_t* flag = D.row_flag + (size_t)nb * D.ms;
   const int lane = threadIdx.x & 31;
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchg;

@@ -19,15 +19,15 @@ namespace pgb {
 __device__ __forceinline__ void grid_barrier(DevState* st) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile uint32_t* gen = &st->bar_gen;
-    const uint32_t g = *gen;
+    const uint32_t* gen = &st->bar_gen;
+    const uint32_t g = ld_gpu(gen);
     __threadfence();
     if (atomicAdd(&st->bar_count, 1u) == gridDim.x - 1) {
       st->bar_count = 0;
       __threadfence();
       atomicAdd(&st->bar_gen, 1u);
     } else {
-      while (*gen == g) __nanosleep(20);
+      while (ld_gpu(gen) == g) __nanosleep(20);
     }
     __threadfence();
   }
@@ -47,7 +47,7 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB)
   extern __shared__ __align__(16) unsigned char loop_dyn[];  // LoopSmem
   LoopSmem& sm = *reinterpret_cast<LoopSmem*>(loop_dyn);
   longlong2* key_out = reinterpret_cast<longlong2*>(A.key_out);
-  while (!*((volatile int32_t*)&A.st->done)) {
+  while (!ld_gpu(&A.st->done)) {
     if (sell_dense_round(A))
       sell_sweep<kRowCheck, true>(A, cfg, sm.sell);
     else
@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB)
       split_finish_body<kRowCheck, 64>(A, split, nsplit, sm.split, cfg);
       grid_barrier(A.st);
     }
-    if (*((volatile int32_t*)&A.st->wl_long)) {
+    if (ld_gpu(&A.st->wl_long)) {
       cand_sweep(A, cfg, sm.cand);
       grid_barrier(A.st);
     }

@@ -123,12 +123,12 @@ __device__ __forceinline__ int node_entry(const Act& act, double a, double lo, d
   if (kind & 1) {
     const long long k = key_enc(canon0(cl));
     long long* p = &key[j].x;
-    if (*((volatile long long*)p) < k && atomicMax(p, k) < k) moved = 2;
+    if (ld_gpu(p) < k && atomicMax(p, k) < k) moved = 2;
   }
   if (kind & 2) {
     const long long k = -key_enc(canon0(cu));
     long long* p = &key[j].y;
-    if (*((volatile long long*)p) < k && atomicMax(p, k) < k) moved = 2;
+    if (ld_gpu(p) < k && atomicMax(p, k) < k) moved = 2;
   }
   return moved;
 }

@@ -24,6 +24,29 @@ struct DevCfg {
   int32_t pad;
 };
 
+// ---- GPU-scope relaxed loads -------------------------------------------------
+// Device state written by other CTAs (earlier kernels, or before a grid
+// barrier) is read with ld.relaxed.gpu: coherent at L2, without the
+// system-scope (STRONG.SYS) cost of a volatile access.
+__device__ __forceinline__ int32_t ld_gpu(const int32_t* p) {
+  int32_t v;
+  asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint32_t ld_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ long long ld_gpu(const long long* p) {
+  long long v;
+  asm volatile("ld.relaxed.gpu.global.s64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_gpu(long long* p, long long v) {
+  asm volatile("st.relaxed.gpu.global.s64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
 // ---- ordered-bits keys ------------------------------------------------------
 // A monotone map double -> int64 so that exact bound merges (merge_lower /
 // merge_upper, par_engine.cpp:56-71) become single 64-bit atomicMax/atomicMin.

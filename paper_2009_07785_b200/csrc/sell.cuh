@@ -67,6 +67,9 @@ namespace pgb {
 #ifndef PG_SELL_GROUPW
 #define PG_SELL_GROUPW 16  // slices at most this wide are grouped
 #endif
+#ifndef PG_SELL_LANEUNIT
+#define PG_SELL_LANEUNIT 32
+#endif
 #ifndef PG_SELL_DEBUG
 #define PG_SELL_DEBUG 0  // 1: cfg.flags 0x10000 skips phase 2 (timing experiments)
 #endif
@@ -86,7 +89,7 @@ constexpr int kSellUnroll = PG_SELL_UNROLL;
 constexpr int kSellThreads = 256;
 constexpr int kSellWarps = kSellThreads / 32;
 constexpr int kSellGroup = PG_SELL_GROUP;
-constexpr int kSellLaneUnit = 16;  // worklist rounds: longer units get a warp each
+constexpr int kSellLaneUnit = PG_SELL_LANEUNIT;  // worklist rounds: longer units get a warp each
 // lanes per unit by unit length: > 256 -> 8, > 128 -> 4, > 64 -> 2, else 1
 constexpr int kSellG8 = 256, kSellG4 = 128, kSellG2 = 64;
 
@@ -193,6 +196,7 @@ struct SellWarpSmem {
   int32_t qe[64];
   uint8_t qu[64];
   double2 wbuf[256];  // worklist rounds: {min, max} contributions of a wide unit's block
+  double2 wbuf2[256];
 #if PG_SELL_ASYNC
   // per lane, PG_SELL_DEPTH steps in flight: the {lb, ub} record and the
   // value of each step land here by cp.async (no registers held)
@@ -214,7 +218,7 @@ __device__ __forceinline__ bool sell_drain(const RoundArgs& A, const SellWarpSme
     const double a = A.sv[e];
     const int32_t c = A.sc[e];
     double lo, up, q;
-    ld_col(A, c, pol_keep, *((volatile int32_t*)&A.st->frac_any) != 0, cfg, lo, up, q);
+    ld_col(A, c, pol_keep, ld_gpu(&A.st->frac_any) != 0, cfg, lo, up, q);
     const Act act = {W.min_f[u], W.max_f[u], W.min_i[u], W.max_i[u]};
     inf_flag = entry_pipeline(act, a, lo, up, W.lhs[u], W.rhs[u], c, A.key_out, cfg);
   }
@@ -261,7 +265,7 @@ template <bool kRowCheck>
 __device__ __forceinline__ void chunk_done(const RoundArgs& A, const UnitDesc& ud, const Act& act,
                                            double xmax, bool& inf_flag, const DevCfg& cfg) {
   const SegDesc d = A.segs[-ud.ref - 1];
-  volatile SegPartial* P = A.partial + d.out;
+  SegPartial* P = A.partial + d.out;
   P->min_f = act.min_f;
   P->max_f = act.max_f;
   P->xmax = xmax;
@@ -453,7 +457,7 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
   uint32_t* sw = A.sw + sd.off + lane;
   const bool whole = ud.ref >= 0;
   const int steps = sd.steps;
-  const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
+  const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
 
   // ---- phase 1: the chains ------------------------------------------------------
   Act act = {0.0, 0.0, 0, 0};
@@ -461,7 +465,7 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
   if (kDense && PG_SELL_ASYNC) {
 #if PG_SELL_ASYNC
     sell_chain_async<LG>(sv, sc, sw, steps, u, lane, A.bnd, W,
-                         *((volatile int32_t*)&A.st->frac_any) != 0, cfg, act, xmax);
+                         ld_gpu(&A.st->frac_any) != 0, cfg, act, xmax);
 #endif
   } else if (kDense) {
     constexpr int UL = LG >= PG_SELL_LGU ? PG_SELL_ULONG : kSellUnroll;
@@ -594,7 +598,7 @@ __device__ __forceinline__ void sell_group(const RoundArgs& A, SellWarpSmem& W, 
     xmax[r] = -CUDART_INF;
   }
   const int tmax = steps[0];  // the group's first slice is its widest
-  const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
+  const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
   double a[R];
   int32_t c[R];
 #pragma unroll
@@ -652,9 +656,9 @@ template <bool kRowCheck>
 __device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, int par,
                                           uint64_t pol_keep, bool& inf_flag, const DevCfg& cfg) {
   const int lane = threadIdx.x & 31;
-  const int nw = *((volatile int32_t*)&A.st->nwide[par]);
+  const int nw = ld_gpu(&A.st->nwide[par]);
   const int32_t* wl = A.dirty.wide_list + (size_t)par * A.dirty.nunits;
-  const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
+  const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
   // static striding by warp (few, similar items: no ticket contention)
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
   for (int t = gw; t < nw; t += nwarps) {
@@ -662,18 +666,37 @@ __device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, i
     const UnitDesc ud = A.units[u];
     const int k0 = ud.ref >= 0 ? A.row_ptr[ud.ref] : A.segs[-ud.ref - 1].k0;
     const int len = ud.len;
+#if PG_SELL_DEBUG
+    const long long dbg_t0 = clock64();
+    long long dbg_t1 = 0;
+#endif
     int cmin = 0, cmax = 0;
     double xm = -CUDART_INF, smin = 0.0, smax = 0.0;
-    for (int base = 0; base < len; base += 256) {
+    // double-buffered blocks of 256 entries: the loads and gathers of block
+    // b + 1 are in flight while lanes 0 / 1 add block b's contributions
+    double a8[8];
+    int32_t c8[8];
+    auto load_block = [&](int base) {
 #pragma unroll
       for (int s8 = 0; s8 < 8; ++s8) {
         const int e = base + 32 * s8 + lane;
+        a8[s8] = 0.0;
+        c8[s8] = A.pad_col;
+        if (e < len) {
+          a8[s8] = A.vals[k0 + e];
+          c8[s8] = A.colx[k0 + e];
+        }
+      }
+    };
+    auto product_block = [&](int base, double2* buf) {
+#pragma unroll
+      for (int s8 = 0; s8 < 8; ++s8) {
+        const int e = base + 32 * s8 + lane;
+        double lo, up, q;
+        ld_col(A, c8[s8], pol_keep, frac_any, cfg, lo, up, q);
         double pmin = 0.0, pmax = 0.0;
         if (e < len) {
-          const double a = A.vals[k0 + e];
-          const int32_t c = A.colx[k0 + e];
-          double lo, up, q;
-          ld_col(A, c, pol_keep, frac_any, cfg, lo, up, q);
+          const double a = a8[s8];
           const double bmin = a > 0 ? lo : up;
           const double bmax = a > 0 ? up : lo;
           const bool imin = isinf(bmin), imax = isinf(bmax);
@@ -683,13 +706,21 @@ __device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, i
           cmax += imax;
           xm = fmax(xm, fabs(a) * q);
         }
-        W.wbuf[32 * s8 + lane] = make_double2(pmin, pmax);
+        buf[32 * s8 + lane] = make_double2(pmin, pmax);
       }
-      __syncwarp();
+    };
+    load_block(0);
+    product_block(0, W.wbuf);
+    __syncwarp();
+    for (int base = 0; base < len; base += 256) {
+      double2* cur = base & 256 ? W.wbuf2 : W.wbuf;
+      double2* nxt = base & 256 ? W.wbuf : W.wbuf2;
+      const bool more = base + 256 < len;
+      if (more) load_block(base + 256);
       if (lane < 2) {
         // lane 0 runs the min chain, lane 1 the max chain, in entry order
-        // (a block is padded with +0.0 entries, which add exactly)
-        const double* wb = reinterpret_cast<const double*>(W.wbuf) + lane;
+        // (entries past the end are +0.0, which adds exactly)
+        const double* wb = reinterpret_cast<const double*>(cur) + lane;
         const int nb = min(256, len - base);
         double acc = lane ? smax : smin;
         for (int i = 0; i < nb; i += 8) {
@@ -701,6 +732,7 @@ __device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, i
         }
         if (lane) smax = acc; else smin = acc;
       }
+      if (more) product_block(base + 256, nxt);
       __syncwarp();
     }
 #pragma unroll
@@ -710,8 +742,15 @@ __device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, i
       xm = fmax(xm, __shfl_xor_sync(0xffffffffu, xm, o));
     }
     const Act act = {__shfl_sync(0xffffffffu, smin, 0), __shfl_sync(0xffffffffu, smax, 1), cmin, cmax};
+#if PG_SELL_DEBUG
+    dbg_t1 = clock64();
+#endif
     if (ud.ref < 0) {
       if (lane == 0) chunk_done<kRowCheck>(A, ud, act, xm, inf_flag, cfg);
+#if PG_SELL_DEBUG
+      if (lane == 0 && (cfg.flags & 0x200000u))
+        printf("[wide] chunk len %d phase1 %lld cyc\n", len, dbg_t1 - dbg_t0);
+#endif
       continue;
     }
     const double l = A.lhs[ud.ref], h = A.rhs[ud.ref];
@@ -747,6 +786,10 @@ __device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, i
         if ((pass >> s8) & 1u)
           if (entry_pipeline(act, a[s8], lo[s8], up[s8], l, h, c[s8], A.key_out, cfg)) inf_flag = true;
     }
+#if PG_SELL_DEBUG
+    if (lane == 0 && (cfg.flags & 0x200000u))
+      printf("[wide] row len %d phase1 %lld phase2 %lld cyc\n", len, dbg_t1 - dbg_t0, clock64() - dbg_t1);
+#endif
   }
 }
 
@@ -759,13 +802,13 @@ template <bool kRowCheck>
 __device__ __forceinline__ void sell_units(const RoundArgs& A, int par, uint64_t pol_keep,
                                            bool& inf_flag, const DevCfg& cfg) {
   const int lane = threadIdx.x & 31;
-  const int nu = *((volatile int32_t*)&A.st->nunit[par]);
+  const int nu = ld_gpu(&A.st->nunit[par]);
   const int32_t* ul = A.dirty.unit_list + (size_t)par * A.dirty.nunits;
-  const bool frac_any = *((volatile int32_t*)&A.st->frac_any) != 0;
+  const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
   // static striding: warp w takes batches w, w + W, .. of 32 units (the
   // batches after the wide units' warps, so both kinds start at once)
   const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
-  const int nwide = *((volatile int32_t*)&A.st->nwide[par]);
+  const int nwide = ld_gpu(&A.st->nwide[par]);
   for (int b = (gw + nwarps - nwide % nwarps) % nwarps; 32 * b < nu; b += nwarps) {
     const int i = 32 * b + lane;
     if (i >= nu) continue;
@@ -804,13 +847,29 @@ __device__ __forceinline__ void sell_units(const RoundArgs& A, int par, uint64_t
     if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
     const RowFilter f = row_filter(act, l, h);
     if (!row_may(f, xmax)) continue;
-    for (int t = 0; t < ud.len; ++t) {
-      if (!filt_may(f, sw[32 * t])) continue;
-      const double a = sv[32 * t];
-      const int32_t c = sc[32 * t];
-      double lo, up, q;
-      ld_col(A, c, pol_keep, frac_any, cfg, lo, up, q);
-      if (entry_pipeline(act, a, lo, up, l, h, c, A.key_out, cfg)) inf_flag = true;
+    for (int t0 = 0; t0 < ud.len; t0 += 4) {
+      // four entries' filter words, then the survivors' loads, then pipelines
+      bool pass[4];
+      double a[4], lo[4], up[4], q[4];
+      int32_t c[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) pass[k] = t0 + k < ud.len && filt_may(f, sw[32 * (t0 + k)]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        a[k] = 0.0;
+        c[k] = A.pad_col;
+        if (pass[k]) {
+          a[k] = sv[32 * (t0 + k)];
+          c[k] = sc[32 * (t0 + k)];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (pass[k]) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (pass[k] && entry_pipeline(act, a[k], lo[k], up[k], l, h, c[k], A.key_out, cfg))
+          inf_flag = true;
     }
   }
 }
@@ -821,7 +880,7 @@ __device__ __forceinline__ void sell_sweep(const RoundArgs& A, const DevCfg& cfg
   const int lane = threadIdx.x & 31;
   SellWarpSmem& W = smem[threadIdx.x >> 5];
   const bool full = kDense;
-  const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
+  const int par = (ld_gpu(&A.st->round) + 1) & 1;
   const uint8_t* rflag = A.dirty.row_flag + (size_t)par * A.dirty.ms;
   const uint64_t pk = l2_policy_evict_last();
   const uint64_t ps = l2_policy_evict_first();
@@ -882,12 +941,11 @@ __device__ __forceinline__ void sell_sweep(const RoundArgs& A, const DevCfg& cfg
 // slices dirty (then visiting all of them is cheaper than the list; exact
 // either way)
 __device__ __forceinline__ bool sell_dense_round(const RoundArgs& A) {
-  if (!A.dirty.enabled || *((volatile int32_t*)&A.st->full)) return true;
-  const int par = (*((volatile int32_t*)&A.st->round) + 1) & 1;
-  // marked one-lane units + 8 per long unit, against a quarter of all units
-  const long long work = (long long)*((volatile int32_t*)&A.st->nunit[par]) +
-                         8LL * *((volatile int32_t*)&A.st->nwide[par]);
-  return 4 * work > (long long)A.nunits;
+  if (!A.dirty.enabled || ld_gpu(&A.st->full)) return true;
+  const int par = (ld_gpu(&A.st->round) + 1) & 1;
+  // marked one-lane units + 2 per long unit, against half of all units
+  const long long work = (long long)ld_gpu(&A.st->nunit[par]) + 2LL * ld_gpu(&A.st->nwide[par]);
+  return 2 * work > (long long)A.nunits;
 }
 
 template <bool kRowCheck, bool kDense>

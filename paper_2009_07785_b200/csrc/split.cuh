@@ -35,7 +35,7 @@ __device__ __forceinline__ void split_finish_body(const RoundArgs& A, const int3
     const int rs = split[w];
     const int first = A.sfirst[rs];
     const int np = A.sfirst[rs + 1] - first;
-    if (*((volatile int32_t*)&A.row_done[rs]) != np) continue;  // not all chunks ran
+    if (ld_gpu(&A.row_done[rs]) != np) continue;  // not all chunks ran
     __syncwarp();
     if (lane == 0) A.row_done[rs] = 0;
     if (np > MAXP) {
