@@ -47,6 +47,18 @@ def b_round(m, n, nnz):
     return 12 * nnz + 4 * (m + 1) + 16 * m + 33 * n
 
 
+def _ncu_traffic(config, kernel):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (tools/ncu_traffic.py -> profiles/roofline_traffic.json), or None."""
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "roofline_traffic.json")
+    try:
+        with open(path) as f:
+            ks = json.load(f)[config]["kernels"]
+        return next(int(v["dram_bytes"]) for k, v in ks.items() if kernel in k)
+    except (OSError, KeyError, StopIteration, ValueError):
+        return None
+
+
 def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -290,7 +302,11 @@ def bench_single(args, inst, world, rank, local):
         "wall_ms_per_step": round(wall_ms / args.steps, 3),
         "roofline": {"kernel": "k_sell+k_cand (dense first round)", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peak, "peak_kind": peak_kind,
-                     "unit": "GB/s", "frac": round(achieved / peak, 4), "traffic": None,
+                     "unit": "GB/s", "frac": round(achieved / peak, 4),
+                     "traffic": _ncu_traffic(args.config, "k_sell"),
+                     "traffic_source": "dram__bytes_read.sum + dram__bytes_write.sum of k_sell "
+                                       "(dense first round), one ncu --set full capture "
+                                       "(profiles/roofline_traffic.json)",
                      "bytes_per_launch": k_bytes, "launch_us": round(k_ns / 1e3, 3),
                      "share_of_round": round(k_ns / 1e6 / (ms / max(R, 1)), 3)},
         "e2e": {"value": round(e2e_ms, 3), "unit": "ms",
