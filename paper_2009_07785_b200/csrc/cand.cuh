@@ -53,13 +53,14 @@ __device__ __forceinline__ void cand_row_load(const RoundArgs& A, CandWarpSmem& 
 
 // run the exact pipeline over queue entries [0, cnt), one per lane
 __device__ __forceinline__ bool cand_drain(const CandWarpSmem& W, int cnt, int lane,
-                                           long long* key_out, const DevCfg& cfg) {
+                                           long long* key_out, const DevCfg& cfg,
+                                           const Touch* touch = nullptr) {
   bool inf_flag = false;
   if (lane < cnt) {
     const int r = W.qr[lane];
     const Act act = {W.min_f[r], W.max_f[r], W.min_i[r], W.max_i[r]};
     inf_flag = entry_pipeline(act, W.qa[lane], W.qlo[lane], W.qup[lane], W.lhs[r], W.rhs[r],
-                              W.qc[lane], key_out, cfg);
+                              W.qc[lane], key_out, cfg, touch);
   }
   return inf_flag;
 }
@@ -67,7 +68,8 @@ __device__ __forceinline__ bool cand_drain(const CandWarpSmem& W, int cnt, int l
 // append this lane's surviving entry (if any); drain full batches of 32
 __device__ __forceinline__ void cand_push(CandWarpSmem& W, int& qn, bool pass, double a,
                                           double lo, double up, int32_t c, int slot, int lane,
-                                          bool& inf_flag, long long* key_out, const DevCfg& cfg) {
+                                          bool& inf_flag, long long* key_out, const DevCfg& cfg,
+                                          const Touch* touch) {
   const unsigned m = __ballot_sync(0xffffffffu, pass);
   if (!m) return;
   if (pass) {
@@ -81,7 +83,7 @@ __device__ __forceinline__ void cand_push(CandWarpSmem& W, int& qn, bool pass, d
   qn += __popc(m);
   if (qn >= 32) {
     __syncwarp();
-    inf_flag |= cand_drain(W, 32, lane, key_out, cfg);
+    inf_flag |= cand_drain(W, 32, lane, key_out, cfg, touch);
     __syncwarp();
     qn -= 32;
     if (lane < qn) {
@@ -115,6 +117,7 @@ __device__ __forceinline__ void cand_sweep(const RoundArgs& A, const DevCfg& cfg
   const int nlong = ld_gpu(&A.st->wl_long);
   const int nshort = ld_gpu(&A.st->wl_short);
   const int nbatch = (nshort + 31) / 32;
+  const Touch* touch = A.dirty.enabled && ld_gpu(&A.st->sparse_round) ? &A.touch : nullptr;
   bool inf_flag = false;
   for (;;) {
     int t = 0;
@@ -138,7 +141,7 @@ __device__ __forceinline__ void cand_sweep(const RoundArgs& A, const DevCfg& cfg
         }
 #pragma unroll
         for (int u = 0; u < kCandUnroll; ++u)
-          cand_push(W, qn, pass[u], a[u], lo[u], up[u], c[u], 0, lane, inf_flag, A.key_out, cfg);
+          cand_push(W, qn, pass[u], a[u], lo[u], up[u], c[u], 0, lane, inf_flag, A.key_out, cfg, touch);
       }
     } else {
       // a batch of up to 32 short rows, entries flattened over the lanes
@@ -187,12 +190,12 @@ __device__ __forceinline__ void cand_sweep(const RoundArgs& A, const DevCfg& cfg
 #pragma unroll
         for (int u = 0; u < kCandUnroll; ++u)
           cand_push(W, qn, pass[u], a[u], lo[u], up[u], c[u], slot[u], lane, inf_flag, A.key_out,
-                    cfg);
+                    cfg, touch);
       }
     }
     if (qn) {
       __syncwarp();
-      inf_flag |= cand_drain(W, qn, lane, A.key_out, cfg);
+      inf_flag |= cand_drain(W, qn, lane, A.key_out, cfg, touch);
     }
     __syncwarp();
   }

@@ -248,6 +248,9 @@ struct pg_session {
   int32_t* d_wide_list = nullptr;
   int32_t* d_unit_list = nullptr;
   Dirty dirty{};
+  Touch touch{};           // worklist rounds: merged-into columns
+  uint32_t* d_tflag = nullptr;
+  int32_t* d_tlist = nullptr;
 
   // host mirrors
   DevState* h_st = nullptr;  // pinned
@@ -284,7 +287,7 @@ struct pg_session {
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
                     d_lo_res, d_up_res, d_segs, d_srow, d_sfirst, d_partial,
                     d_ract, d_wl_short, d_wl_long, d_f32_part, d_split, d_bnd, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
-                    d_flags, d_chg, d_row_unit, d_part_unit, d_unit_slice, d_wide_list, d_unit_list};
+                    d_flags, d_chg, d_row_unit, d_part_unit, d_unit_slice, d_wide_list, d_unit_list, d_tflag, d_tlist};
     for (void* p : ptrs) dfree(p);  // stream-ordered: no device sync here
     if (h_st) cudaFreeHost(h_st);
     if (stream) cudaStreamDestroy(stream);
@@ -327,6 +330,7 @@ struct pg_session {
     A.key_out = (long long*)d_key_out;
     A.st = d_st;
     A.dirty = dirty;
+    A.touch = touch;
     return A;
   }
 
@@ -379,6 +383,9 @@ struct pg_session {
     }
     k_commit<<<grid_for(n, kCommitThreads, 4), kCommitThreads, 0, stream>>>(
         d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0);
+    if (dirty.enabled)
+      k_commit_list<<<num_sms * 2, kCommitThreads, 0, stream>>>(
+          d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, touch, cond, use_graph ? 1 : 0);
     if (dirty.enabled) k_mark<<<num_sms * 2, 256, 0, stream>>>(dirty, d_st);
     PG_CUDA(cudaGetLastError());
   }
@@ -938,6 +945,10 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         D.sfirst = s->d_sfirst;
         D.unit_slice = s->d_unit_slice;
         D.wide_list = s->d_wide_list;
+        s->d_tflag = dalloc<uint32_t>(n);
+        s->d_tlist = dalloc<int32_t>(n);
+        PG_CUDA(cudaMemsetAsync(s->d_tflag, 0, sizeof(uint32_t) * std::max(n, 1), st));
+        s->touch = Touch{s->d_tflag, s->d_tlist, &s->d_st->ntouch};
         D.nslices = s->nslices;
         D.unit_list = s->d_unit_list;
         D.nunits = s->nunits;

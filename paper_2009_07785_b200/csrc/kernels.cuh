@@ -49,6 +49,9 @@ struct DevState {
   int32_t nchg[2];                   // changed-column list lengths, by round parity
   int32_t nwide[2];                  // marked multi-lane unit list lengths, by round parity
   int32_t nunit[2];                  // marked one-lane unit list lengths, by round parity
+  int32_t ntouch;                    // columns merged into this (worklist) round
+  int32_t sparse_commit;             // the last commit visited only the touched columns
+  int32_t sparse_round;              // this round is a worklist round (set by the dense k_sell)
   uint32_t bar_count;                // grid barrier of the persistent round loop (loop.cuh)
   uint32_t bar_gen;
 };
@@ -216,8 +219,20 @@ __device__ __forceinline__ void red_max(long long* p, long long k) {
   asm volatile("red.relaxed.gpu.global.max.s64 [%0], %1;" ::"l"(p), "l"(k) : "memory");
 }
 
+// Worklist rounds: the columns a round merged into, so the commit visits
+// only those (each column listed once per round).
+struct Touch {
+  uint32_t* flag;   // [n]
+  int32_t* list;    // [n]
+  int32_t* count;
+};
+__device__ __forceinline__ void touch_col(const Touch* t, int j) {
+  if (t && !atomicOr(&t->flag[j], 1u)) t->list[atomicAdd(t->count, 1)] = j;
+}
+
 __device__ __forceinline__ void commit_side(long long* key_out, int j, int kind, double cl,
-                                            double cu) {
+                                            double cu, const Touch* t = nullptr) {
+  if (kind) touch_col(t, j);
   // merge_lower / merge_upper (par_engine.cpp:56-71) as exact 64-bit max/min
   if (kind & 1) {
     const long long k = key_enc(canon0(cl));
@@ -237,13 +252,14 @@ __device__ __forceinline__ void commit_side(long long* key_out, int j, int kind,
 // (propcore.hpp:78-208, par_engine.cpp:158-168).  Returns true on EmptyDomain.
 __device__ __forceinline__ bool entry_pipeline(const Act& act, double a, double lo, double up,
                                                double lhs, double rhs, int32_t cx,
-                                               long long* key_out, const DevCfg& c) {
+                                               long long* key_out, const DevCfg& c,
+                                               const Touch* t = nullptr) {
   double min_res, max_res, cl, cu;
   residual(act, a, lo, up, min_res, max_res);
   candidates(a, lhs, rhs, min_res, max_res, cx < 0, c, cl, cu);
   const int kind = tighten(lo, up, cl, cu, c);
   if (kind == 4) return true;  // EmptyDomain: flag, skip the merge (par_engine.cpp:163-166)
-  if (kind) commit_side(key_out, cx & 0x7fffffff, kind, cl, cu);
+  if (kind) commit_side(key_out, cx & 0x7fffffff, kind, cl, cu, t);
   return false;
 }
 
@@ -333,6 +349,7 @@ struct RoundArgs {
   long long* key_out;
   DevState* st;
   Dirty dirty;
+  Touch touch;            // worklist rounds: merged-into columns (kernels.cuh)
 };
 
 // A row's activity is complete: row check (propcore.hpp:147-156, cpu_seq's
@@ -421,11 +438,26 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, in
 // Per variable (par_engine.cpp:191-197): count sides with out != in, flag
 // lo_out > up_out + abs, and write the next round's snapshot record.  The
 // last CTA takes the round decision of run_parallel (par_engine.cpp:248-266).
+// A worklist round visits only the marked rows' units when few are marked
+// (sell.cuh); otherwise it is a full sweep.  Evaluated identically by the
+// sweep and the commit of the round.
+__device__ __forceinline__ bool round_is_sparse(DevState* st, const Dirty& D) {
+  if (!D.enabled || ld_gpu(&st->full)) return false;
+  const int par = (ld_gpu(&st->round) + 1) & 1;
+  // marked one-lane units + 2 per long unit, against half of all units
+  const long long work = (long long)ld_gpu(&st->nunit[par]) + 2LL * ld_gpu(&st->nwide[par]);
+  return 2 * work <= (long long)D.nunits;
+}
+
+// kList: a worklist round -- only the columns on the touched list (their
+// flags are cleared); otherwise every column.
+template <bool kList = false>
 __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __restrict__ bnd,
                                             const longlong2* __restrict__ key_out, int n,
                                             DevState* __restrict__ st, long long* __restrict__ per_round,
                                             const DevCfg& cfg, const Dirty& D,
-                                            cudaGraphConditionalHandle cond, int use_graph) {
+                                            cudaGraphConditionalHandle cond, int use_graph,
+                                            const Touch* touch = nullptr) {
   unsigned long long changes = 0;
   int inf = 0;
   const int R = ld_gpu(&st->round);  // rounds before this one
@@ -435,24 +467,28 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
   const int gtid = blockIdx.x * blockDim.x + threadIdx.x;
   constexpr int U = 4;  // columns in flight per thread
   const int lane = threadIdx.x & 31;
+  const int nj = kList ? ld_gpu(touch->count) : n;
   // the loop bound is warp-uniform (j0 - lane is), so the warp stays
   // converged for the list appends
-  for (int j0 = gtid; j0 - lane < n; j0 += U * gstride) {
+  for (int j0 = gtid; j0 - lane < nj; j0 += U * gstride) {
     longlong2 kob[U];
     double2 inb[U];
+    int jj[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * gstride;
-      if (j < n) {
-        kob[u] = key_out[j];
-        inb[u] = *reinterpret_cast<const double2*>(&snap[j].lo);
+      const int i = j0 + u * gstride;
+      jj[u] = i < nj ? (kList ? touch->list[i] : i) : -1;
+      if (jj[u] >= 0) {
+        kob[u] = key_out[jj[u]];
+        inb[u] = *reinterpret_cast<const double2*>(&snap[jj[u]].lo);
+        if (kList) touch->flag[jj[u]] = 0u;
       }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int j = j0 + u * gstride;
+      const int j = jj[u];
       int c = 0;
-      if (j < n) {
+      if (j >= 0) {
         const longlong2 ko = kob[u];
         const double lo = key_dec(ko.x), up = key_dec(-ko.y);
         const double2 in = inb[u];
@@ -520,6 +556,8 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
       st->nchg[nb] = 0;  // the list k_mark consumed after the previous commit
       st->nwide[cb] = 0;  // this round's unit lists
       st->nunit[cb] = 0;
+      st->ntouch = 0;
+      st->sparse_commit = kList;
       __threadfence();
       if (use_graph) cudaGraphSetConditional(cond, status >= 0 ? 0u : 1u);
     }
@@ -530,7 +568,18 @@ __global__ void __launch_bounds__(kCommitThreads)
     k_commit(Snap* __restrict__ snap, double2* __restrict__ bnd, const longlong2* __restrict__ key_out,
              int n, DevState* __restrict__ st, long long* __restrict__ per_round, const DevCfg cfg,
              const Dirty D, cudaGraphConditionalHandle cond, int use_graph) {
+  if (ld_gpu(&st->sparse_round)) return;  // k_commit_list commits this round
   commit_body(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph);
+}
+
+// the commit of a worklist round: only the columns merged into
+__global__ void __launch_bounds__(kCommitThreads)
+    k_commit_list(Snap* __restrict__ snap, double2* __restrict__ bnd,
+                  const longlong2* __restrict__ key_out, int n, DevState* __restrict__ st,
+                  long long* __restrict__ per_round, const DevCfg cfg, const Dirty D, const Touch T,
+                  cudaGraphConditionalHandle cond, int use_graph) {
+  if (!ld_gpu(&st->sparse_round)) return;
+  commit_body<true>(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph, &T);
 }
 
 // Start of a solve: snapshot records and merge keys from the (normalised)
@@ -584,6 +633,8 @@ __global__ void __launch_bounds__(kCommitThreads)
       // k_mark_vars marks (see NodeCtl)
       st->full = (D.enabled && ctl->warm) ? 0 : 1;
       st->nchg[0] = st->nchg[1] = 0;
+      st->ntouch = 0;
+      st->sparse_round = 0;
       st->nwide[0] = st->nwide[1] = 0;
       st->nunit[0] = st->nunit[1] = 0;
       st->frac_any = atomicAdd(&st->frac_tmp, 0);

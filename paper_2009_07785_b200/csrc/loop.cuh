@@ -48,7 +48,9 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB)
   LoopSmem& sm = *reinterpret_cast<LoopSmem*>(loop_dyn);
   longlong2* key_out = reinterpret_cast<longlong2*>(A.key_out);
   while (!ld_gpu(&A.st->done)) {
-    if (sell_dense_round(A))
+    const bool sparse = round_is_sparse(A.st, A.dirty);  // the round's kind, before any phase
+    if (blockIdx.x == 0 && threadIdx.x == 0) A.st->sparse_round = sparse ? 1 : 0;  // for cand_sweep
+    if (!sparse)
       sell_sweep<kRowCheck, true>(A, cfg, sm.sell);
     else
       sell_sweep<kRowCheck, false>(A, cfg, sm.sell);
@@ -61,7 +63,11 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB)
       cand_sweep(A, cfg, sm.cand);
       grid_barrier(A.st);
     }
-    commit_body(snap, const_cast<double2*>(A.bnd), key_out, n, A.st, per_round, cfg, A.dirty, 0, 0);
+    if (sparse)
+      commit_body<true>(snap, const_cast<double2*>(A.bnd), key_out, n, A.st, per_round, cfg, A.dirty,
+                        0, 0, &A.touch);
+    else
+      commit_body(snap, const_cast<double2*>(A.bnd), key_out, n, A.st, per_round, cfg, A.dirty, 0, 0);
     grid_barrier(A.st);
     if (A.dirty.enabled) {
       mark_body(A.dirty, A.st);

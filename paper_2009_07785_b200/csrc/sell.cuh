@@ -784,7 +784,8 @@ __device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, i
 #pragma unroll
       for (int s8 = 0; s8 < 8; ++s8)
         if ((pass >> s8) & 1u)
-          if (entry_pipeline(act, a[s8], lo[s8], up[s8], l, h, c[s8], A.key_out, cfg)) inf_flag = true;
+          if (entry_pipeline(act, a[s8], lo[s8], up[s8], l, h, c[s8], A.key_out, cfg, &A.touch))
+            inf_flag = true;
     }
 #if PG_SELL_DEBUG
     if (lane == 0 && (cfg.flags & 0x200000u))
@@ -868,7 +869,7 @@ __device__ __forceinline__ void sell_units(const RoundArgs& A, int par, uint64_t
         if (pass[k]) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (pass[k] && entry_pipeline(act, a[k], lo[k], up[k], l, h, c[k], A.key_out, cfg))
+        if (pass[k] && entry_pipeline(act, a[k], lo[k], up[k], l, h, c[k], A.key_out, cfg, &A.touch))
           inf_flag = true;
     }
   }
@@ -941,11 +942,7 @@ __device__ __forceinline__ void sell_sweep(const RoundArgs& A, const DevCfg& cfg
 // slices dirty (then visiting all of them is cheaper than the list; exact
 // either way)
 __device__ __forceinline__ bool sell_dense_round(const RoundArgs& A) {
-  if (!A.dirty.enabled || ld_gpu(&A.st->full)) return true;
-  const int par = (ld_gpu(&A.st->round) + 1) & 1;
-  // marked one-lane units + 2 per long unit, against half of all units
-  const long long work = (long long)ld_gpu(&A.st->nunit[par]) + 2LL * ld_gpu(&A.st->nwide[par]);
-  return 2 * work > (long long)A.nunits;
+  return !round_is_sparse(A.st, A.dirty);
 }
 
 template <bool kRowCheck, bool kDense>
@@ -953,7 +950,10 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const Round
                                                                      const DevCfg cfg) {
   extern __shared__ __align__(16) unsigned char sell_dyn[];  // kSellWarps x SellWarpSmem
   SellWarpSmem* smem = reinterpret_cast<SellWarpSmem*>(sell_dyn);
-  if (sell_dense_round(A) != kDense) return;
+  const bool dense = sell_dense_round(A);
+  // the round's kind, for the commit kernels (written before any of them runs)
+  if (kDense && blockIdx.x == 0 && threadIdx.x == 0) A.st->sparse_round = dense ? 0 : 1;
+  if (dense != kDense) return;
   sell_sweep<kRowCheck, kDense>(A, cfg, smem);
 }
 
