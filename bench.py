@@ -438,8 +438,8 @@ def main():
     ap.add_argument("--seed", type=int, default=None)
     ap.add_argument("--nodes", type=int, default=8192, help="C4: number of B&B nodes")
     ap.add_argument("--worklist", type=int, default=None,
-                    help="device-side worklist (exact); default: on for c5 (cascading fixings), "
-                         "off otherwise (the dense sweep is faster there)")
+                    help="device-side worklist (exact); default: on for c2 and c5 (few rows "
+                         "change after the first rounds), off for c1/c3 (faster as full sweeps)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--loop", default="graph", choices=["graph", "host"],
                     help="host: one launch per kernel per round (for ncu launch lists: ncu "
@@ -448,7 +448,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.worklist is None:
-        args.worklist = args.config == "c5"
+        args.worklist = args.config in ("c2", "c5")
     args.worklist = bool(args.worklist)
 
     world, rank, local = dist_init()

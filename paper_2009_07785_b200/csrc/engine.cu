@@ -434,7 +434,7 @@ struct pg_session {
       const char* e = getenv("PG_PERSIST_NNZ");
       return e ? atoll(e) : 8000000LL;
     }();
-    return nnz <= thr || dirty.enabled;
+    return nnz <= thr;
   }
 
   void enqueue_persistent() {

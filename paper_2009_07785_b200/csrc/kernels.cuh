@@ -52,6 +52,7 @@ struct DevState {
   int32_t ntouch;                    // columns merged into this (worklist) round
   int32_t sparse_commit;             // the last commit visited only the touched columns
   int32_t sparse_round;              // this round is a worklist round (set by the dense k_sell)
+  long long last_changes;            // changes of the previous round (worklist heuristics)
   uint32_t bar_count;                // grid barrier of the persistent round loop (loop.cuh)
   uint32_t bar_gen;
 };
@@ -468,6 +469,10 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
   constexpr int U = 4;  // columns in flight per thread
   const int lane = threadIdx.x & 31;
   const int nj = kList ? ld_gpu(touch->count) : n;
+  // a full-sweep round after a round with many changes will have many too:
+  // skip the changed-column list (the next round is a full sweep anyway)
+  const bool list = D.enabled && (kList || !ld_gpu(&st->full) ||
+                                  ld_gpu(&st->last_changes) <= 4LL * D.dense_nchg);
   // the loop bound is warp-uniform (j0 - lane is), so the warp stays
   // converged for the list appends
   for (int j0 = gtid; j0 - lane < nj; j0 += U * gstride) {
@@ -502,7 +507,7 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
         }
         if (lo > __dadd_rn(up, cfg.imp_abs)) inf = 1;
       }
-      if (D.enabled) {
+      if (list) {
         // changed columns of this round -> list (one atomic per warp)
         const unsigned chm = __ballot_sync(0xffffffffu, c != 0);
         if (chm) {
@@ -551,8 +556,9 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
       st->work = 0;
       st->work2 = 0;
       st->cand_work = 0;
-      // many changed columns: the next round is a full sweep (no marks)
-      st->full = ld_gpu(&st->nchg[cb]) > D.dense_nchg ? 1 : 0;
+      // many changed columns (or no list): the next round is a full sweep (no marks)
+      st->full = (!list || ld_gpu(&st->nchg[cb]) > D.dense_nchg) ? 1 : 0;
+      st->last_changes = ch;
       st->nchg[nb] = 0;  // the list k_mark consumed after the previous commit
       st->nwide[cb] = 0;  // this round's unit lists
       st->nunit[cb] = 0;
@@ -635,6 +641,7 @@ __global__ void __launch_bounds__(kCommitThreads)
       st->nchg[0] = st->nchg[1] = 0;
       st->ntouch = 0;
       st->sparse_round = 0;
+      st->last_changes = 0x7fffffffffffffffLL;  // round 1 is a full sweep: no list
       st->nwide[0] = st->nwide[1] = 0;
       st->nunit[0] = st->nunit[1] = 0;
       st->frac_any = atomicAdd(&st->frac_tmp, 0);
