@@ -203,7 +203,7 @@ struct pg_session {
   int cand_per_sm = 1;   // resident k_cand CTAs per SM
   int loop_grid = 0;     // co-resident CTAs of the persistent loop kernel
   int nodes_per_sm = 1;  // resident k_nodes CTAs per SM
-  int32_t max_row_len = 0;
+  int32_t max_row_len = -1;  // lazily: max_len()
   ActF* d_f32_part = nullptr;  // Narrow32: per-thread chunk partials
   int f32_maxc = 1;
 
@@ -396,6 +396,18 @@ struct pg_session {
         check_crossed ? 1 : 0, cond, use_graph ? 1 : 0);
     if (dirty.enabled) k_mark_vars<<<num_sms * 2, 256, 0, stream>>>(dirty, d_ctl, d_st);
     PG_CUDA(cudaGetLastError());
+  }
+
+  // longest row (computed on first use: Narrow32 scratch, B&B node scratch)
+  int32_t max_len() {
+    if (max_row_len >= 0) return max_row_len;
+    int32_t* d = dalloc<int32_t>(1);
+    PG_CUDA(cudaMemsetAsync(d, 0, sizeof(int32_t), stream));
+    if (m) k_max_row_len<<<grid_for(m, 256), 256, 0, stream>>>(d_row_ptr, m, d);
+    PG_CUDA(cudaMemcpyAsync(&max_row_len, d, sizeof(int32_t), cudaMemcpyDeviceToHost, stream));
+    PG_CUDA(cudaStreamSynchronize(stream));
+    dfree(d);
+    return max_row_len;
   }
 
   // column -> rows index over the sorted rows (device counting sort);
@@ -601,32 +613,44 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->dev = cfg->device;
     PG_CUDA(cudaSetDevice(s->dev));
     s->num_sms = prop.sms;
-    for (const void* f : {(const void*)k_sell<true, true>, (const void*)k_sell<false, true>,
-                          (const void*)k_sell<true, false>, (const void*)k_sell<false, false>})
-      PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem));
-    for (const void* f : {(const void*)k_loop<true>, (const void*)k_loop<false>})
-      PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(LoopSmem)));
-    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->sell_per_sm, k_sell<true, true>,
-                                                          kSellThreads, kSellSmem));
-    s->sell_per_sm = std::max(1, s->sell_per_sm);
-    PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&s->cand_per_sm, k_cand, kCandThreads, 0));
     {
-      int per = 0;
-      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_loop<true>, kSellThreads,
-                                                            sizeof(LoopSmem)));
-      int per2 = 0;
-      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_loop<false>, kSellThreads,
-                                                            sizeof(LoopSmem)));
-      s->loop_grid = std::min(per, per2) * s->num_sms;
-      PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_nodes<true>, kNodeThreads, 0));
-      s->nodes_per_sm = std::max(1, per);
+      // kernel attributes and occupancies, once per device (they cost ~0.7 ms)
+      struct Occ {
+        bool ok = false;
+        int sell = 1, cand = 1, loop_grid = 0, nodes = 1;
+      };
+      static Occ occ[64];
+      static std::mutex mu;
+      std::lock_guard<std::mutex> lock(mu);
+      Occ& o = occ[s->dev];
+      if (!o.ok) {
+        for (const void* f : {(const void*)k_sell<true, true>, (const void*)k_sell<false, true>,
+                              (const void*)k_sell<true, false>, (const void*)k_sell<false, false>})
+          PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem));
+        for (const void* f : {(const void*)k_loop<true>, (const void*)k_loop<false>})
+          PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)sizeof(LoopSmem)));
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.sell, k_sell<true, true>,
+                                                              kSellThreads, kSellSmem));
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.cand, k_cand, kCandThreads, 0));
+        int per = 0, per2 = 0;
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_loop<true>, kSellThreads,
+                                                              sizeof(LoopSmem)));
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per2, k_loop<false>, kSellThreads,
+                                                              sizeof(LoopSmem)));
+        o.loop_grid = std::min(per, per2) * s->num_sms;
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_nodes<true>, kNodeThreads, 0));
+        o.nodes = per;
+        o.ok = true;
+      }
+      s->sell_per_sm = std::max(1, o.sell);
+      s->cand_per_sm = std::max(1, o.cand);
+      s->loop_grid = o.loop_grid;
+      s->nodes_per_sm = std::max(1, o.nodes);
     }
-    s->cand_per_sm = std::max(1, s->cand_per_sm);
 
     s->m = p->num_rows;
     s->n = p->num_cols;
-    for (int32_t i = 0; i < p->num_rows; ++i)
-      s->max_row_len = std::max(s->max_row_len, p->row_ptr[i + 1] - p->row_ptr[i]);
     s->nnz = p->nnz;
     s->cfg = *cfg;
     s->dcfg.inf_thr = cfg->infinity_threshold;
@@ -812,7 +836,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     PG_CUDA(cudaEventRecord(s->ev_join, s2));
     PG_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
     if (m) {
-      k_permute_rows<<<s->grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(
+      k_permute_rows<<<s->grid_for((int64_t)m, 256, 16), 256, 0, st>>>(
           t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, s->d_integral, s->d_colx,
           s->d_vals, s->d_lhs, s->d_rhs, m, cfg->infinity_threshold);
       PG_CUDA(cudaGetLastError());
@@ -823,7 +847,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_lhs, m);
       k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_rhs, m);
       const int chunk = cfg->nnz_budget;
-      s->f32_maxc = s->max_row_len > chunk ? (s->max_row_len + chunk - 1) / chunk : 1;
+      s->f32_maxc = s->max_len() > chunk ? (s->max_len() + chunk - 1) / chunk : 1;
       s->d_f32_part = dalloc<ActF>((size_t)s->grid_for(m, 256, 4) * 256 * s->f32_maxc);
       PG_CUDA(cudaGetLastError());
     }
@@ -1259,7 +1283,7 @@ int pg_session_propagate_nodes(pg_session* s, int32_t K, const int32_t* node_ptr
       s->ensure_col_index();
       const size_t m = (size_t)s->m;
       const int chunk = s->cfg.nnz_budget;
-      const int maxc = s->max_row_len > chunk ? (s->max_row_len + chunk - 1) / chunk : 1;
+      const int maxc = s->max_len() > chunk ? (s->max_len() + chunk - 1) / chunk : 1;
       const size_t per_slot = n * 44 + m * 12 + (size_t)kNodeThreads * maxc * sizeof(Act);
       size_t free_b = 0, total_b = 0;
       PG_CUDA(cudaMemGetInfo(&free_b, &total_b));

@@ -687,20 +687,40 @@ __global__ void k_permute_rows(const int32_t* __restrict__ rp, const int32_t* __
                                const uint8_t* __restrict__ integral, int32_t* __restrict__ colx,
                                double* __restrict__ new_vals, double* __restrict__ new_lhs,
                                double* __restrict__ new_rhs, int m, double thr) {
+  // a warp per 32 consecutive new rows: their entries are contiguous in the
+  // new order, so the lanes walk them flat (coalesced stores) and find each
+  // entry's row by a binary search over the batch's starts (shuffles)
   const int lane = threadIdx.x & 31;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m;
-       i += (gridDim.x * blockDim.x) >> 5) {
-    const int old = perm[i];
-    const int b = rp[old], len = rp[old + 1] - b, nb = new_rp[i];
-    for (int k = lane; k < len; k += 32) {
-      const int32_t c = cols[b + k];
-      colx[nb + k] = integral[c] ? (int32_t)(c | 0x80000000u) : c;
-      new_vals[nb + k] = vals[b + k];
-    }
-    if (lane == 0) {
+  for (int i0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; i0 < m;
+       i0 += ((gridDim.x * blockDim.x) >> 5) * 32) {
+    const int cnt = min(32, m - i0);
+    const int i = i0 + lane;
+    int nb = 0, ob = 0;
+    if (lane < cnt) {
+      const int old = perm[i];
+      nb = new_rp[i];
+      ob = rp[old];
       const double l = lhs[old], h = rhs[old];
       new_lhs[i] = l >= thr ? CUDART_INF : (l <= -thr ? -CUDART_INF : l);
       new_rhs[i] = h >= thr ? CUDART_INF : (h <= -thr ? -CUDART_INF : h);
+    }
+    const int start = __shfl_sync(0xffffffffu, nb, 0);
+    const int end = new_rp[i0 + cnt];
+    for (int k0 = start; k0 < end; k0 += 32) {
+      const int k = k0 + lane;
+      int r = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const int cand = r + step;
+        const int v = __shfl_sync(0xffffffffu, nb, cand & 31);
+        if (cand < cnt && v <= k) r = cand;
+      }
+      const int src = __shfl_sync(0xffffffffu, ob, r) + (k - __shfl_sync(0xffffffffu, nb, r));
+      if (k < end) {
+        const int32_t c = cols[src];
+        colx[k] = integral[c] ? (int32_t)(c | 0x80000000u) : c;
+        new_vals[k] = vals[src];
+      }
     }
   }
 }
@@ -781,6 +801,14 @@ __device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__
 }
 __global__ void __launch_bounds__(256) k_mark(const Dirty D, DevState* __restrict__ st) {
   mark_body(D, st);
+}
+
+__global__ void k_max_row_len(const int32_t* __restrict__ rp, int m, int32_t* __restrict__ out) {
+  int mx = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    mx = max(mx, rp[i + 1] - rp[i]);
+  for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0 && mx) atomicMax(out, mx);
 }
 
 // ---- worklist index (session init) -----------------------------------------------
