@@ -26,6 +26,9 @@
 namespace pgb {
 
 constexpr int kCommitThreads = 256;
+#ifndef PG_SPARSE_COST
+#define PG_SPARSE_COST 2
+#endif
 
 // Device-resident loop state.
 struct DevState {
@@ -445,9 +448,10 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, in
 __device__ __forceinline__ bool round_is_sparse(DevState* st, const Dirty& D) {
   if (!D.enabled || ld_gpu(&st->full)) return false;
   const int par = (ld_gpu(&st->round) + 1) & 1;
-  // marked one-lane units + 2 per long unit, against half of all units
+  // worklist round while the marked units (a long unit counts twice) stay
+  // below 1 / PG_SPARSE_COST of all units (tuned on C2 / C5)
   const long long work = (long long)ld_gpu(&st->nunit[par]) + 2LL * ld_gpu(&st->nwide[par]);
-  return 2 * work <= (long long)D.nunits;
+  return PG_SPARSE_COST * work <= (long long)D.nunits;
 }
 
 // kList: a worklist round -- only the columns on the touched list (their
