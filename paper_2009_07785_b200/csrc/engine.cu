@@ -382,8 +382,9 @@ struct pg_session {
       if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllReduce: ") + g_nccl.error(rc)};
     }
     k_commit<<<grid_for(n, kCommitThreads, 4), kCommitThreads, 0, stream>>>(
-        d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0);
-    if (dirty.enabled)
+        d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0,
+        comm ? 0 : 1);
+    if (dirty.enabled && !comm)
       k_commit_list<<<num_sms * 2, kCommitThreads, 0, stream>>>(
           d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, touch, cond, use_graph ? 1 : 0);
     if (dirty.enabled) k_mark<<<num_sms * 2, 256, 0, stream>>>(dirty, d_st);

@@ -577,8 +577,10 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
 __global__ void __launch_bounds__(kCommitThreads)
     k_commit(Snap* __restrict__ snap, double2* __restrict__ bnd, const longlong2* __restrict__ key_out,
              int n, DevState* __restrict__ st, long long* __restrict__ per_round, const DevCfg cfg,
-             const Dirty D, cudaGraphConditionalHandle cond, int use_graph) {
-  if (ld_gpu(&st->sparse_round)) return;  // k_commit_list commits this round
+             const Dirty D, cudaGraphConditionalHandle cond, int use_graph, int allow_list) {
+  // a worklist round of a single session is committed by k_commit_list; with
+  // row shards every column may have moved on another rank: always in full
+  if (allow_list && ld_gpu(&st->sparse_round)) return;
   commit_body(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph);
 }
 

@@ -55,8 +55,9 @@ def test_c4_nodes_match_oracle():
         assert np.array_equal(O.canon(bup[k]), O.canon(ref.bounds.upper))
 
 
+@pytest.mark.parametrize("worklist", [False, True])
 @pytest.mark.parametrize("loop", [LoopMode.Graph, LoopMode.Host])
-def test_row_sharded_nccl_world1(loop):
+def test_row_sharded_nccl_world1(loop, worklist):
     """The row-sharded path (NCCL max all-reduce of the bound keys inside the
     device loop) with one rank: identical to the plain engine and the oracle."""
     try:
@@ -66,7 +67,7 @@ def test_row_sharded_nccl_world1(loop):
         pytest.skip(f"NCCL unavailable: {e}")
     for inst in (G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003),
                  G.gen_random(4000, 4000, 9, mean_row_nnz=10.0, integral_fraction=0.5)):
-        cfg = EngineConfig(row_check=False, loop_mode=loop)
+        cfg = EngineConfig(row_check=False, loop_mode=loop, worklist=worklist)
         rs = RowShardedSession(inst, cfg, rank=0, world=1)
         try:
             assert_bit_exact(rs.propagate(), O.propagate_parallel(inst, PAR), inst.name)
