@@ -272,10 +272,13 @@ def test_nnz_budget_changes_long_row_order(budget):
 @pytest.mark.slow
 def test_config2_full_size_bit_exact():
     """C2 (1M x 1M power-law, ~12M entries): the full solve is bit-identical
-    to the restated cpu_par (status, rounds, per-round changes, bounds)."""
+    to the restated cpu_par (status, rounds, per-round changes, bounds), with
+    full sweeps and with worklist rounds (the bench's mode)."""
     inst = G.config_instance("c2")
-    gpu = propagate_gpu(inst, PAR)
-    assert_bit_exact(gpu, O.propagate_parallel(inst, PAR), "c2")
+    ref = O.propagate_parallel(inst, PAR)
+    assert_bit_exact(propagate_gpu(inst, PAR), ref, "c2")
+    assert_bit_exact(propagate_gpu(inst, EngineConfig(row_check=False, worklist=True)), ref,
+                     "c2 worklist")
 
 
 @pytest.mark.parametrize("worklist", [False, True])
