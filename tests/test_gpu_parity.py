@@ -338,3 +338,30 @@ def test_f32_round_api_is_double():
     assert oa.changes == ob.changes and oa.changes > 0
     assert np.array_equal(O.canon(sa.bounds_out.lower), O.canon(sb.bounds_out.lower))
     assert np.array_equal(O.canon(sa.bounds_out.upper), O.canon(sb.bounds_out.upper))
+
+
+@pytest.mark.parametrize("mode", ["dense", "worklist", "f32", "host", "f32_worklist"])
+def test_modes_on_edge_instances(mode):
+    """Every engine mode on degenerate shapes: empty rows / columns, a single
+    entry, all-infinite bounds, a crossed start (0 rounds), a chunked row."""
+    from paper_2009_07785_b200.model import ScalarMode
+    kw = dict(row_check=False)
+    if "worklist" in mode:
+        kw["worklist"] = True
+    if "f32" in mode:
+        kw["scalar_mode"] = ScalarMode.Narrow32
+    if mode == "host":
+        kw["loop_mode"] = LoopMode.Host
+    cfg = EngineConfig(**kw)
+    cases = [
+        ProblemInstance.from_arrays([0, 0, 2, 2], [0, 2], [1.0, 1.0], [-kInf, -kInf, -kInf],
+                                    [1.0, 4.0, -1.0], [0.0] * 4, [9.0] * 4),
+        ProblemInstance.from_arrays([0, 1], [0], [2.0], [-kInf], [3.0], [-kInf], [kInf]),
+        ProblemInstance.from_arrays([0, 2], [0, 1], [1.0, -1.0], [0.0], [0.0], [-kInf, 2.0],
+                                    [kInf, 5.0]),
+        ProblemInstance.from_arrays([0, 1], [0], [1.0], [-kInf], [1.0], [3.0], [2.0]),  # crossed
+        G.gen_random(50, 3000, 17, mean_row_nnz=300.0, integral_fraction=0.5),
+        G.gen_cascade(30),
+    ]
+    for k, inst in enumerate(cases):
+        assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg), (mode, k))
