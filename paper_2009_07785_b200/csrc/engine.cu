@@ -904,7 +904,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       // narrow one-lane slices are handed out in groups (sell_group): the
       // first slice of region 0 whose units are all <= PG_SELL_GROUPW long
       s->group_start = s->nslices;
-      if (!PG_SELL_ASYNC && R.ustart[4] > R.ustart[3]) {
+      if (R.ustart[4] > R.ustart[3]) {
         const int ub = std::max(hc[4], R.ustart[3]);  // first unit <= the grouping width
         s->group_start = std::min(s->nslices, R.sstart[3] + (ub - R.ustart[3] + 31) / 32);
       }

@@ -300,7 +300,7 @@ struct __align__(8) SliceDesc {
   int32_t steps;    // ceil(width / G)
   int16_t count;    // units in the slice (<= H)
   int8_t lg;        // log2 G
-  int8_t uniform;   // lg == 0 and all 32 units of length `width`
+  int8_t pad;
 };
 
 // len entries; ref >= 0: the unit is the whole sorted row `ref`; ref < 0: it

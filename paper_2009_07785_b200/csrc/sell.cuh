@@ -46,23 +46,11 @@ namespace pgb {
 #ifndef PG_SELL_B16
 #define PG_SELL_B16 1  // gather 16 B {lb, ub} from the compact bounds array
 #endif
-#ifndef PG_SELL_ASYNC
-#define PG_SELL_ASYNC 0  // dense chains through a per-lane cp.async ring
-#endif
-#ifndef PG_SELL_DEPTH
-#define PG_SELL_DEPTH 8
-#endif
 #ifndef PG_SELL_GROUP
 #define PG_SELL_GROUP 2  // narrow one-lane slices per work item
 #endif
 #ifndef PG_SELL_B16
 #define PG_SELL_B16 1  // gather 16 B {lb, ub} from the compact bounds array
-#endif
-#ifndef PG_SELL_ASYNC
-#define PG_SELL_ASYNC 0  // dense chains through a per-lane cp.async ring
-#endif
-#ifndef PG_SELL_DEPTH
-#define PG_SELL_DEPTH 8
 #endif
 #ifndef PG_SELL_GROUPW
 #define PG_SELL_GROUPW 16  // slices at most this wide are grouped
@@ -197,12 +185,6 @@ struct SellWarpSmem {
   uint8_t qu[64];
   double2 wbuf[256];  // worklist rounds: {min, max} contributions of a wide unit's block
   double2 wbuf2[256];
-#if PG_SELL_ASYNC
-  // per lane, PG_SELL_DEPTH steps in flight: the {lb, ub} record and the
-  // value of each step land here by cp.async (no registers held)
-  double2 rrec[PG_SELL_DEPTH][32];
-  double ra[PG_SELL_DEPTH][32];
-#endif
 };
 
 constexpr size_t kSellSmem = sizeof(SellWarpSmem) * kSellWarps;
@@ -366,72 +348,6 @@ __device__ __forceinline__ void slice_tail(const RoundArgs& A, SellWarpSmem& W, 
   __syncwarp();
 }
 
-// ---- dense chains through a per-lane cp.async ring --------------------------------
-__device__ __forceinline__ void cp_async16(void* dst, const void* src) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src)
-               : "memory");
-}
-__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-
-#if PG_SELL_ASYNC
-// Every lane keeps PG_SELL_DEPTH steps of its chain in flight: the column
-// index of a step is loaded a block ahead into registers, the 16 B {lb, ub}
-// gather and the value go to shared memory by cp.async (per-lane groups, no
-// barrier), and a step is consumed in entry order once its group landed.
-template <int LG>
-__device__ __forceinline__ void sell_chain_async(const double* sv, const int32_t* sc, uint32_t* sw,
-                                                 int steps, int u, int lane, const double2* bnd,
-                                                 SellWarpSmem& W, bool frac_any, const DevCfg& cfg,
-                                                 Act& act, double& xmax) {
-  constexpr int D = PG_SELL_DEPTH;
-  int32_t cc[D], cn[D];
-#pragma unroll
-  for (int d = 0; d < D; ++d) {
-    cc[d] = 0;
-    if (d < steps) {
-      cc[d] = __ldg(sc + 32 * d);
-      cp_async16(&W.rrec[d][lane], bnd + (cc[d] & 0x7fffffff));
-      cp_async8(&W.ra[d][lane], sv + 32 * d);
-    }
-    cp_async_commit();
-  }
-#pragma unroll
-  for (int d = 0; d < D; ++d) cn[d] = D + d < steps ? __ldg(sc + 32 * (D + d)) : 0;
-  for (int t0 = 0; t0 < steps; t0 += D) {
-#pragma unroll
-    for (int d = 0; d < D; ++d) {
-      const int t = t0 + d;
-      cp_async_wait<D - 1>();
-      if (t < steps) {
-        const double2 b = W.rrec[d][lane];
-        const double a = W.ra[d][lane];
-        const double q = column_q_inline(b.x, b.y, cc[d] < 0, frac_any, cfg);
-        sell_step<LG>(a, b.x, b.y, q, u, act, xmax, sw + 32 * t);
-      }
-      if (t + D < steps) {
-        cp_async16(&W.rrec[d][lane], bnd + (cn[d] & 0x7fffffff));
-        cp_async8(&W.ra[d][lane], sv + 32 * (t + D));
-      }
-      cp_async_commit();
-      cc[d] = cn[d];
-      cn[d] = t + 2 * D < steps ? __ldg(sc + 32 * (t + 2 * D)) : 0;
-    }
-  }
-  cp_async_wait<0>();
-}
-#endif
-
 // One slice by one warp.  LG = log2(lanes per unit); kDense: a full sweep
 // (no worklist), every lane walks every step of the slice.
 template <bool kRowCheck, int LG, bool kDense>
@@ -462,12 +378,7 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
   // ---- phase 1: the chains ------------------------------------------------------
   Act act = {0.0, 0.0, 0, 0};
   double xmax = -CUDART_INF;
-  if (kDense && PG_SELL_ASYNC) {
-#if PG_SELL_ASYNC
-    sell_chain_async<LG>(sv, sc, sw, steps, u, lane, A.bnd, W,
-                         ld_gpu(&A.st->frac_any) != 0, cfg, act, xmax);
-#endif
-  } else if (kDense) {
+  if (kDense) {
     constexpr int UL = LG >= PG_SELL_LGU ? PG_SELL_ULONG : kSellUnroll;
     // every lane walks all `steps` of the slice: entries past a unit's end are
     // padding (value 0, the padding column with bounds [0, 0]) and add +0.0
@@ -1041,8 +952,7 @@ __global__ void k_slice_desc(const UnitDesc* __restrict__ units, const SellRegio
     const int count = min(H, R.ustart[k + 1] - first);
     const int width = units[first].len;  // sorted descending
     const int steps = (width + (1 << lg) - 1) >> lg;
-    const bool uniform = lg == 0 && count == H && units[first + count - 1].len == width;
-    slices[s] = SliceDesc{0, first, width, steps, (int16_t)count, (int8_t)lg, (int8_t)uniform};
+    slices[s] = SliceDesc{0, first, width, steps, (int16_t)count, (int8_t)lg, 0};
     elems[s] = 32LL * steps;
   }
 }
