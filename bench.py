@@ -246,7 +246,14 @@ def bench_single(args, inst, world, rank, local):
     for _ in range(args.warmup):
         r = sess.run()
     # k_sell + k_cand + k_commit (+ k_mark with the worklist)
-    launches_per_round = (2 if info["slices"] else 0) + 1 + (1 if args.worklist else 0)
+    # our kernels per round: k_sell (full sweep) + k_cand + k_commit, k_split_finish
+    # with split rows, and with the worklist the worklist k_sell + k_commit_list
+    # + k_mark; k_reset (+ k_mark_vars) per solve.  The persistent loop is one
+    # kernel per solve (+ k_reset).
+    launches_per_round = ((2 if info["slices"] else 0) + 1 + (1 if info["split_rows"] else 0) +
+                          (3 if args.worklist else 0))
+    if info["persistent"]:
+        launches_per_round = 0
 
     def barrier():
         torch.cuda.synchronize()
@@ -268,7 +275,8 @@ def bench_single(args, inst, world, rank, local):
         wall_ms = (time.perf_counter() - t0) * 1e3
     ms = _max_over_ranks(torch, dist, world, local, float(np.sum(step_ms))) / args.steps
     R = rounds[-1]
-    gpu_launches = sum(1 + rr * launches_per_round for rr in rounds)
+    per_solve = (1 + (1 if args.worklist else 0)) + (1 if info["persistent"] else 0)
+    gpu_launches = sum(per_solve + rr * launches_per_round for rr in rounds)
 
     # dominant kernels alone (roofline), first-round snapshot
     k_ns, k_bytes = sess.time_round_kernel(reps=20)

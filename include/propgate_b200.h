@@ -208,7 +208,8 @@ int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank,
 /* Session statistics, in this order: m, n, nnz, slices (sliced-ELL, 32
  * chains each), split-candidate rows (> 16 entries), segments (chains of
  * those rows), short rows, short-row entries, segment entries, chains,
- * sliced-ELL elements (entries + padding). */
+ * sliced-ELL elements (entries + padding), split rows (> nnz_budget),
+ * persistent loop (1: the whole solve is one cooperative kernel). */
 int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info);
 
 /* Thread-local message of the last failed call on this thread. */

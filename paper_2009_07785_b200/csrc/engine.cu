@@ -1524,7 +1524,8 @@ int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info) {
     return PG_EINVAL;
   }
   const int64_t v[] = {s->m, s->n, s->nnz, s->nslices, s->nsrow, s->nseg,
-                       s->short_rows, s->short_nnz, s->seg_nnz, s->nunits, s->sell_elems};
+                       s->short_rows, s->short_nnz, s->seg_nnz, s->nunits, s->sell_elems,
+                       s->nsplit, s->use_persistent() ? 1 : 0};
   for (int i = 0; i < n_info && i < (int)(sizeof(v) / sizeof(v[0])); ++i) info[i] = v[i];
   return PG_OK;
 }
