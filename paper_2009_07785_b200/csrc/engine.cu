@@ -421,17 +421,16 @@ struct pg_session {
     d_col_item = dalloc<int32_t>(nnz);
     int32_t* cnt = dalloc<int32_t>((size_t)n + 1);
     PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)n + 1), st));
-    if (m) k_csc_count<<<grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(d_row_ptr, d_colx, m, cnt);
+    if (nnz) k_csc_count<<<grid_for(nnz, 256, 16), 256, 0, st>>>(d_colx, nnz, cnt);
     size_t tmp_bytes = 0;
     PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, d_col_ptr, n + 1, st));
     void* tmp = dalloc<unsigned char>(tmp_bytes);
     PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, d_col_ptr, n + 1, st));
     PG_CUDA(cudaMemcpyAsync(cnt, d_col_ptr, sizeof(int32_t) * ((size_t)n + 1),
                             cudaMemcpyDeviceToDevice, st));
-    if (m) k_csc_fill<<<grid_for((int64_t)m * 32, 256, 16), 256, 0, st>>>(d_row_ptr, d_colx, m, cnt,
+    if (m) k_csc_fill<<<grid_for(nnz * 32 / kWalkChunk + 1, 256, 16), 256, 0, st>>>(d_row_ptr, d_colx, m, cnt,
                                                                          d_col_item);
     PG_CUDA(cudaGetLastError());
-    PG_CUDA(cudaStreamSynchronize(st));
     dfree(tmp);
     dfree(cnt);
     dirty.col_ptr = d_col_ptr;
@@ -522,11 +521,32 @@ struct pg_session {
   }
 
   // Runs one full solve from lo0/up0.  Returns elapsed device ns.
-  int64_t run_solve(bool check_crossed = true) {
+  // res: download the bounds in the same pass (graph loop): the decode and
+  // the copies are queued behind the solve and the host faults in the
+  // result pages while the GPU works (a fresh pageable array costs a page
+  // fault per 4 KB inside the copy otherwise)
+  int64_t run_solve(bool check_crossed = true, pg_result* res = nullptr) {
+    bounds_done = false;
     if (cfg.loop_mode == PG_LOOP_GRAPH && check_crossed) {
       PG_CUDA(cudaEventRecord(ev0, stream));
       PG_CUDA(cudaGraphLaunch(exec, stream));
       PG_CUDA(cudaEventRecord(ev1, stream));
+      if (res && (res->lower || res->upper)) {
+        k_decode<<<grid_for(n, 256), 256, 0, stream>>>(d_key_out, d_lo_res, d_up_res, n);
+        PG_CUDA(cudaGetLastError());
+        for (double* out : {res->lower, res->upper})
+          if (out) {
+            volatile char* b = reinterpret_cast<volatile char*>(out);
+            for (size_t off = 0; off < sizeof(double) * n; off += 4096) b[off] = 0;
+          }
+        if (res->lower)
+          PG_CUDA(cudaMemcpyAsync(res->lower, d_lo_res, sizeof(double) * n,
+                                  cudaMemcpyDeviceToHost, stream));
+        if (res->upper)
+          PG_CUDA(cudaMemcpyAsync(res->upper, d_up_res, sizeof(double) * n,
+                                  cudaMemcpyDeviceToHost, stream));
+        bounds_done = true;
+      }
     } else {
       // host-driven loop: one sync per round (the paper's cpu_loop)
       PG_CUDA(cudaEventRecord(ev0, stream));
@@ -552,6 +572,8 @@ struct pg_session {
     return (int64_t)((double)ms * 1e6);
   }
 
+  bool bounds_done = false;  // run_solve already downloaded the bounds
+
   void fill_result(pg_result* res, int64_t elapsed) {
     res->status = h_st->status < 0 ? PG_ROUNDLIMIT : h_st->status;
     res->rounds_executed = h_st->round;
@@ -563,7 +585,7 @@ struct pg_session {
       PG_CUDA(cudaMemcpyAsync(res->per_round_changes, d_per_round, sizeof(long long) * cnt,
                               cudaMemcpyDeviceToHost, stream));
     }
-    if (res->lower || res->upper) {
+    if ((res->lower || res->upper) && !bounds_done) {
       // returned bounds = last round's output (par_engine.cpp:271); after
       // the commit key_in == key_out; with 0 rounds they are the start bounds
       k_decode<<<grid_for(n, 256), 256, 0, stream>>>(d_key_out, d_lo_res, d_up_res, n);
@@ -837,7 +859,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     PG_CUDA(cudaEventRecord(s->ev_join, s2));
     PG_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
     if (m) {
-      k_permute_rows<<<s->grid_for((int64_t)m, 256, 16), 256, 0, st>>>(
+      k_permute_rows<<<s->grid_for(std::max<int64_t>(m, nnz * 32 / kWalkChunk + 1), 256, 16), 256, 0, st>>>(
           t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, s->d_integral, s->d_colx,
           s->d_vals, s->d_lhs, s->d_rhs, m, cfg->infinity_threshold);
       PG_CUDA(cudaGetLastError());
@@ -935,8 +957,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
                     (void*)segs_in, (void*)skey, (void*)skey2, (void*)sidx, (void*)sorder,
                     tmp})
       dfree(q);
-    PG_CUDA(cudaStreamSynchronize(st));
-    tm.lap("H2D + permute");
+    tm.lap("H2D + permute (queued)");
     // worklist index: column -> work items (device counting sort by column)
     {
       Dirty& D = s->dirty;
@@ -985,11 +1006,12 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     }
     s->upload_bounds(p->lower, p->upper);
     PG_CUDA(cudaGetLastError());
-    PG_CUDA(cudaStreamSynchronize(st));
+    // everything after this point is ordered on the session stream: no host
+    // sync (the graph is instantiated while the GPU finishes the setup)
     for (void* q : {(void*)t_rp, (void*)t_cols, (void*)t_vals, (void*)t_lhs, (void*)t_rhs,
                     (void*)t_perm})
       dfree(q);
-    tm.lap("worklist/bounds/free");
+    tm.lap("worklist/bounds (queued)");
     // keep the snapshot records (the per-entry random gathers) resident in a
     // persisting L2 carve-out while the matrix streams through
     if (const char* e = getenv("PG_L2_PERSIST_MB")) {
@@ -1080,7 +1102,7 @@ int pg_session_run(pg_session* s, pg_result* res) {
   }
   return guarded([&] {
     PG_CUDA(cudaSetDevice(s->dev));
-    const int64_t ns = s->run_solve(true);
+    const int64_t ns = s->run_solve(true, res);
     s->fill_result(res, ns);
     return PG_OK;
   });
@@ -1097,7 +1119,7 @@ int pg_session_propagate(pg_session* s, const double* lower, const double* upper
       if (!lower || !upper) throw Error{PG_EINVAL, "lower and upper must both be given"};
       s->upload_bounds(lower, upper);
     }
-    const int64_t ns = s->run_solve(true);
+    const int64_t ns = s->run_solve(true, res);
     s->fill_result(res, ns);
     return PG_OK;
   });
@@ -1224,7 +1246,7 @@ int pg_session_set_root(pg_session* s, pg_result* res) {
   }
   return guarded([&] {
     PG_CUDA(cudaSetDevice(s->dev));
-    const int64_t ns = s->run_solve(true);
+    const int64_t ns = s->run_solve(true, res);
     s->fill_result(res, ns);
     s->has_root = res->status == PG_CONVERGED;
     if (s->has_root) {

@@ -683,9 +683,67 @@ __global__ void k_normalize(double* __restrict__ v, int n, double thr) {
   }
 }
 
+// Entry-balanced walk over a CSR: warp-cooperative, each warp takes chunks
+// of kWalkChunk consecutive entries, so a 100k-entry row costs the same as
+// 100k entries of short rows (a warp per row would leave one warp walking
+// the longest row while the rest of the GPU idles).  f(valid, k, r) is called
+// by every lane for entry k of row r.
+constexpr int kWalkChunk = 512;
+
+// last r in [0, m) with rp[r] <= k (same k on all lanes, rp[0] <= k):
+// 32-ary search, four dependent probes for a million rows
+__device__ __forceinline__ int warp_row_search(const int32_t* __restrict__ rp, int m, int64_t k) {
+  const int lane = threadIdx.x & 31;
+  int lo = 0, hi = m;
+  while (hi - lo > 1) {
+    const int step = (hi - lo + 31) >> 5;
+    const int p = lo + lane * step;
+    const bool ok = p < hi && rp[p] <= k;
+    const int cnt = __popc(__ballot_sync(0xffffffffu, ok));
+    lo += (cnt - 1) * step;
+    hi = min(hi, lo + step);
+  }
+  return lo;
+}
+
+template <class F>
+__device__ __forceinline__ void walk_entries(const int32_t* __restrict__ rp, int m, int64_t nnz,
+                                             F&& f) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t c = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; c * kWalkChunk < nnz;
+       c += nwarps) {
+    const int64_t kb = c * kWalkChunk, ke = min(kb + kWalkChunk, nnz);
+    int r = warp_row_search(rp, m, kb);
+    for (int64_t k0 = kb; k0 < ke;) {
+      // rows r .. r+31 and where row r+32 starts: the window covers entries
+      // [k0, wend) -- all of the next 32 unless empty rows sit in between
+      const int rr = r + lane;
+      const int64_t s = rr < m ? rp[rr] : INT64_MAX;
+      const int64_t s_end = rr < m ? rp[rr + 1] : INT64_MAX;
+      const int64_t wend = min(min(k0 + 32, ke), __shfl_sync(0xffffffffu, s_end, 31));
+      const int64_t k = k0 + lane;
+      int j = 0;
+#pragma unroll
+      for (int step = 16; step; step >>= 1) {
+        const int64_t v = __shfl_sync(0xffffffffu, s, j + step);
+        if (v <= k) j += step;
+      }
+      f(k < wend, k, r + j);
+      // row of entry wend
+      k0 = wend;
+      const int cnt = __popc(__ballot_sync(0xffffffffu, s <= k0));
+      r += cnt - 1;
+      if (cnt == 32)
+        while (r + 1 < m && rp[r + 1] <= k0) ++r;
+    }
+  }
+}
+
 // Session init: rows into length-sorted order (perm[new] = old), lhs/rhs
 // normalised (model.hpp:147-151), integrality packed into bit 31 of the
-// column index (no per-entry byte gather).  One warp per row.
+// column index (no per-entry byte gather).  Entries walked in the new order
+// (coalesced stores, entry-balanced), each gathered from its old position.
 __global__ void k_permute_rows(const int32_t* __restrict__ rp, const int32_t* __restrict__ cols,
                                const double* __restrict__ vals, const double* __restrict__ lhs,
                                const double* __restrict__ rhs, const int32_t* __restrict__ perm,
@@ -693,42 +751,19 @@ __global__ void k_permute_rows(const int32_t* __restrict__ rp, const int32_t* __
                                const uint8_t* __restrict__ integral, int32_t* __restrict__ colx,
                                double* __restrict__ new_vals, double* __restrict__ new_lhs,
                                double* __restrict__ new_rhs, int m, double thr) {
-  // a warp per 32 consecutive new rows: their entries are contiguous in the
-  // new order, so the lanes walk them flat (coalesced stores) and find each
-  // entry's row by a binary search over the batch's starts (shuffles)
-  const int lane = threadIdx.x & 31;
-  for (int i0 = ((blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; i0 < m;
-       i0 += ((gridDim.x * blockDim.x) >> 5) * 32) {
-    const int cnt = min(32, m - i0);
-    const int i = i0 + lane;
-    int nb = 0, ob = 0;
-    if (lane < cnt) {
-      const int old = perm[i];
-      nb = new_rp[i];
-      ob = rp[old];
-      const double l = lhs[old], h = rhs[old];
-      new_lhs[i] = l >= thr ? CUDART_INF : (l <= -thr ? -CUDART_INF : l);
-      new_rhs[i] = h >= thr ? CUDART_INF : (h <= -thr ? -CUDART_INF : h);
-    }
-    const int start = __shfl_sync(0xffffffffu, nb, 0);
-    const int end = new_rp[i0 + cnt];
-    for (int k0 = start; k0 < end; k0 += 32) {
-      const int k = k0 + lane;
-      int r = 0;
-#pragma unroll
-      for (int step = 16; step; step >>= 1) {
-        const int cand = r + step;
-        const int v = __shfl_sync(0xffffffffu, nb, cand & 31);
-        if (cand < cnt && v <= k) r = cand;
-      }
-      const int src = __shfl_sync(0xffffffffu, ob, r) + (k - __shfl_sync(0xffffffffu, nb, r));
-      if (k < end) {
-        const int32_t c = cols[src];
-        colx[k] = integral[c] ? (int32_t)(c | 0x80000000u) : c;
-        new_vals[k] = vals[src];
-      }
-    }
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const int old = perm[i];
+    const double l = lhs[old], h = rhs[old];
+    new_lhs[i] = l >= thr ? CUDART_INF : (l <= -thr ? -CUDART_INF : l);
+    new_rhs[i] = h >= thr ? CUDART_INF : (h <= -thr ? -CUDART_INF : h);
   }
+  walk_entries(new_rp, m, new_rp[m], [&](bool valid, int64_t k, int r) {
+    if (!valid) return;
+    const int64_t src = rp[perm[r]] + (k - new_rp[r]);
+    const int32_t c = cols[src];
+    colx[k] = integral[c] ? (int32_t)(c | 0x80000000u) : c;
+    new_vals[k] = vals[src];
+  });
 }
 
 // Warm start of a branch-and-bound node (config C4): the start bounds are a
@@ -819,23 +854,20 @@ __global__ void k_max_row_len(const int32_t* __restrict__ rp, int m, int32_t* __
 
 // ---- worklist index (session init) -----------------------------------------------
 
-// column counts (one warp per row)
-__global__ void k_csc_count(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ colx,
-                            int m, int32_t* __restrict__ cnt) {
-  const int lane = threadIdx.x & 31;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m;
-       i += (gridDim.x * blockDim.x) >> 5)
-    for (int k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32)
-      atomicAdd(&cnt[colx[k] & 0x7fffffff], 1);
+// column counts (flat over the entries)
+__global__ void k_csc_count(const int32_t* __restrict__ colx, int64_t nnz,
+                            int32_t* __restrict__ cnt) {
+  for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[colx[k] & 0x7fffffff], 1);
 }
 
+// rows into their columns' ranges (entry-balanced walk)
 __global__ void k_csc_fill(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ colx,
                            int m, int32_t* __restrict__ cursor, int32_t* __restrict__ col_row) {
-  const int lane = threadIdx.x & 31;
-  for (int i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < m;
-       i += (gridDim.x * blockDim.x) >> 5)
-    for (int k = row_ptr[i] + lane; k < row_ptr[i + 1]; k += 32)
-      col_row[atomicAdd(&cursor[colx[k] & 0x7fffffff], 1)] = i;
+  walk_entries(row_ptr, m, row_ptr[m], [&](bool valid, int64_t k, int r) {
+    if (valid) col_row[atomicAdd(&cursor[colx[k] & 0x7fffffff], 1)] = r;
+  });
 }
 
 }  // namespace pgb
