@@ -36,6 +36,7 @@ extern "C" {
 #define PG_ECUDA (-3)   /* CUDA runtime error */
 #define PG_ENCCL (-4)   /* NCCL error (row-sharded multi-GPU path) */
 #define PG_ENODEV (-5)  /* no usable sm_100 device */
+#define PG_ERANGE (-6)  /* index out of range; reference throws std::out_of_range (core/src/model.cpp:40-45) */
 
 /* ---- statuses: same order as propgate::PropagationStatus (model.hpp:112) */
 #define PG_CONVERGED 0
@@ -142,6 +143,18 @@ int pg_round(const pg_problem* prob, const pg_config* cfg, const double* lb_in,
 int pg_partition_row_blocks(const pg_problem* prob, const pg_config* cfg,
                             int32_t* block_starts, int32_t* kinds,
                             int32_t* num_blocks);
+
+/* Replaces csr_from_triplets (core/include/propgate/model.hpp, core/src/model.cpp:37-80)
+ * with an on-device build (on-device ingest): triplets
+ * (row, col, value) stable-sorted by (row, col), duplicates summed in input
+ * order, zero sums dropped.  PG_ERANGE with the reference's message
+ * ("triplet row index out of range" / "triplet column index out of range")
+ * for the first bad triplet.  row_ptr is caller-allocated [num_rows + 1],
+ * col_idx / values_out [count] (the result has *nnz <= count entries). */
+int pg_csr_from_triplets(int32_t num_rows, int32_t num_cols, int64_t count,
+                         const int32_t* rows, const int32_t* cols, const double* values,
+                         int32_t device, int32_t* row_ptr, int32_t* col_idx,
+                         double* values_out, int64_t* nnz);
 
 /* ---- sessions: matrix resident on the device ---------------------------
  * New capability (B&B warm start, SURVEY.md 5 "Checkpoint / resume"): the

@@ -10,6 +10,8 @@
 //   propgate::propagate_round_gpu(instance, snap, partition, cfg)
 //                                                     ~ propagate_round_parallel
 //                                                     (par_engine.hpp:33-36)
+//   propgate::csr_from_triplets_gpu(entries, m, n)     ~ csr_from_triplets
+//                                                     (model.cpp:37-80), built on the GPU
 //
 // with the reference's own ProblemInstance / EngineConfig / PropagationResult
 // (model.hpp:68-144).  Semantics follow the reference: EngineConfig::validate
@@ -21,7 +23,9 @@
 
 #include <chrono>
 #include <stdexcept>
+#include <span>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "propgate/model.hpp"
@@ -78,6 +82,7 @@ inline void check(int rc, const char* what) {
   if (rc == PG_OK) return;
   const std::string msg = std::string(what) + ": " + pg_last_error();
   if (rc == PG_EINVAL) throw std::invalid_argument(pg_last_error());
+  if (rc == PG_ERANGE) throw std::out_of_range(pg_last_error());
   throw std::runtime_error(msg);
 }
 
@@ -134,6 +139,35 @@ inline RoundOutcome propagate_round_gpu(const ProblemInstance& instance, RoundSn
   o.infeasible = infeasible != 0;
   o.changes = changes;
   return o;
+}
+
+// csr_from_triplets (model.cpp:37-80) with the CSR built on the device:
+// same order, duplicate sums and dropped zeros; std::out_of_range with the
+// reference's messages
+inline SparseMatrix csr_from_triplets_gpu(std::span<const std::tuple<int, int, double>> entries,
+                                          int num_rows, int num_cols, int device = 0) {
+  const size_t k = entries.size();
+  std::vector<int32_t> rows(k), cols(k);
+  std::vector<double> vals(k);
+  for (size_t i = 0; i < k; ++i) {
+    rows[i] = std::get<0>(entries[i]);
+    cols[i] = std::get<1>(entries[i]);
+    vals[i] = std::get<2>(entries[i]);
+  }
+  SparseMatrix m;
+  m.num_rows = num_rows;
+  m.num_cols = num_cols;
+  m.row_ptr.assign(static_cast<size_t>(num_rows) + 1, 0);
+  m.col_idx.resize(k);
+  m.values.resize(k);
+  int64_t nnz = 0;
+  b200_detail::check(pg_csr_from_triplets(num_rows, num_cols, (int64_t)k, rows.data(),
+                                          cols.data(), vals.data(), device, m.row_ptr.data(),
+                                          m.col_idx.data(), m.values.data(), &nnz),
+                     "pg_csr_from_triplets");
+  m.col_idx.resize(static_cast<size_t>(nnz));
+  m.values.resize(static_cast<size_t>(nnz));
+  return m;
 }
 
 }  // namespace propgate

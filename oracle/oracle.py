@@ -80,6 +80,9 @@ def oracle_lib():
         lib.orc_propcore_rows.argtypes = [C.c_int32, _ip, _dp, _dp, _dp, _dp, _G, _dp, _ip, _dp, _dp,
                                           _dp, _ip]
         lib.orc_propcore_rows.restype = None
+        lib.orc_csr_from_triplets.argtypes = [C.c_int32, C.c_int32, C.c_int64, _ip, _ip, _dp, _ip,
+                                              _ip, _dp, _lp]
+        lib.orc_csr_from_triplets.restype = C.c_int
         _orc = lib
     return _orc
 
@@ -123,6 +126,9 @@ def ref_lib():
         lib.ref_classify.restype = C.c_int32
         lib.ref_tighten.argtypes = [C.c_double] * 4 + [_G, _dp]
         lib.ref_tighten.restype = C.c_int32
+        lib.ref_csr_from_triplets.argtypes = [C.c_int32, C.c_int32, C.c_int64, _ip, _ip, _dp, _ip,
+                                              _ip, _dp, _lp]
+        lib.ref_csr_from_triplets.restype = C.c_int
         _ref = lib
     return _ref
 
@@ -253,3 +259,36 @@ def bounds_equal(a, b, t_abs=1e-8, t_rel=1e-5):
     with np.errstate(invalid="ignore"):
         close = np.abs(a - b) <= t_abs + t_rel * np.abs(b)
     return np.where(inf, a == b, close)
+
+
+_TRIP_MSG = {1: "triplet row index out of range", 2: "triplet column index out of range"}
+
+
+def csr_from_triplets(rows, cols, values, num_rows: int, num_cols: int, impl: str = "port"):
+    """csr_from_triplets (core/src/model.cpp:37-80): the C restatement ("port")
+    or the reference itself ("reference").  Returns (row_ptr, col_idx, values);
+    IndexError for an out-of-range triplet (std::out_of_range)."""
+    r = np.ascontiguousarray(rows, dtype=np.int32)
+    c = np.ascontiguousarray(cols, dtype=np.int32)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    cnt = r.shape[0]
+    rp = np.zeros(num_rows + 1, dtype=np.int32)
+    ci = np.empty(max(cnt, 1), dtype=np.int32)
+    vo = np.empty(max(cnt, 1), dtype=np.float64)
+    nnz = C.c_int64()
+    args = (num_rows, num_cols, cnt, abi.ptr(r, C.c_int32), abi.ptr(c, C.c_int32),
+            abi.ptr(v, C.c_double), abi.ptr(rp, C.c_int32), abi.ptr(ci, C.c_int32),
+            abi.ptr(vo, C.c_double), C.byref(nnz))
+    if impl == "reference":
+        lib = ref_lib()
+        rc = lib.ref_csr_from_triplets(*args)
+        if rc == 1:
+            raise IndexError(lib.ref_last_error().decode())
+    else:
+        rc = oracle_lib().orc_csr_from_triplets(*args)
+        if rc in _TRIP_MSG:
+            raise IndexError(_TRIP_MSG[rc])
+    if rc != 0:
+        raise RuntimeError(f"csr_from_triplets ({impl}) failed: {rc}")
+    k = int(nnz.value)
+    return rp, ci[:k].copy(), vo[:k].copy()

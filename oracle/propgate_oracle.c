@@ -234,3 +234,58 @@ void orc_propcore_rows(int32_t nrows, const int32_t* row_len, const double* coef
     off += L;
   }
 }
+
+/* ---- csr_from_triplets (core/src/model.cpp:37-80) -------------------------
+ * Range check over the triplets in input order (row before column, the first
+ * bad triplet decides: returns 1 for a bad row, 2 for a bad column), then a
+ * stable order by (row, col) -- here an LSD counting sort, columns first,
+ * then rows -- and a sequential `sum += value` from 0.0 over each run of equal
+ * (row, col); runs summing to 0.0 are dropped.  row_ptr [m + 1], col_idx /
+ * values_out [count]; *nnz receives the entries kept.  -1 on allocation
+ * failure. */
+int orc_csr_from_triplets(int32_t m, int32_t n, int64_t count, const int32_t* rows,
+                          const int32_t* cols, const double* vals, int32_t* row_ptr,
+                          int32_t* col_idx, double* values_out, int64_t* nnz) {
+  for (int64_t i = 0; i < count; ++i) {
+    if (rows[i] < 0 || rows[i] >= m) return 1;
+    if (cols[i] < 0 || cols[i] >= n) return 2;
+  }
+  int64_t* a = malloc(sizeof(int64_t) * (size_t)(count ? count : 1));
+  int64_t* b = malloc(sizeof(int64_t) * (size_t)(count ? count : 1));
+  int64_t* cnt = malloc(sizeof(int64_t) * ((size_t)(m > n ? m : n) + 1));
+  if (!a || !b || !cnt) {
+    free(a);
+    free(b);
+    free(cnt);
+    return -1;
+  }
+  /* pass 1: stable by column */
+  memset(cnt, 0, sizeof(int64_t) * ((size_t)n + 1));
+  for (int64_t i = 0; i < count; ++i) ++cnt[cols[i] + 1];
+  for (int32_t j = 0; j < n; ++j) cnt[j + 1] += cnt[j];
+  for (int64_t i = 0; i < count; ++i) a[cnt[cols[i]]++] = i;
+  /* pass 2: stable by row */
+  memset(cnt, 0, sizeof(int64_t) * ((size_t)m + 1));
+  for (int64_t i = 0; i < count; ++i) ++cnt[rows[i] + 1];
+  for (int32_t r = 0; r < m; ++r) cnt[r + 1] += cnt[r];
+  for (int64_t t = 0; t < count; ++t) b[cnt[rows[a[t]]]++] = a[t];
+  int64_t out = 0, t = 0;
+  row_ptr[0] = 0;
+  for (int32_t r = 0; r < m; ++r) {
+    while (t < count && rows[b[t]] == r) {
+      const int32_t c = cols[b[t]];
+      double sum = 0.0;
+      while (t < count && rows[b[t]] == r && cols[b[t]] == c) sum += vals[b[t++]];
+      if (sum != 0.0) {
+        col_idx[out] = c;
+        values_out[out++] = sum;
+      }
+    }
+    row_ptr[r + 1] = (int32_t)out;
+  }
+  *nnz = out;
+  free(a);
+  free(b);
+  free(cnt);
+  return 0;
+}

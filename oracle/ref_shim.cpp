@@ -200,6 +200,29 @@ void ref_inst_view(void* h, pg_problem* out) {
 
 void ref_inst_free(void* h) { delete static_cast<ProblemInstance*>(h); }
 
+// ---- csr_from_triplets (model.cpp:37-80) ----------------------------------
+// 0 ok, 1 std::out_of_range (message in ref_last_error), -1 other error
+int ref_csr_from_triplets(int32_t m, int32_t n, int64_t count, const int32_t* rows,
+                          const int32_t* cols, const double* vals, int32_t* row_ptr,
+                          int32_t* col_idx, double* values_out, int64_t* nnz) {
+  try {
+    std::vector<std::tuple<int, int, double>> t((size_t)count);
+    for (int64_t i = 0; i < count; ++i) t[(size_t)i] = {rows[i], cols[i], vals[i]};
+    const SparseMatrix mat = csr_from_triplets(t, m, n);
+    std::copy(mat.row_ptr.begin(), mat.row_ptr.end(), row_ptr);
+    std::copy(mat.col_idx.begin(), mat.col_idx.end(), col_idx);
+    std::copy(mat.values.begin(), mat.values.end(), values_out);
+    *nnz = (int64_t)mat.col_idx.size();
+    return 0;
+  } catch (const std::out_of_range& e) {
+    g_err = e.what();
+    return 1;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return -1;
+  }
+}
+
 // ---- propcore (for golden vectors of the unit KATs) ----------------------
 
 void ref_row_activities(const int32_t* cols, const double* coefs, int64_t len,

@@ -17,7 +17,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.path.join(PKG_DIR, "libpropgate_b200.so")
 GEN_PATH = os.path.join(PKG_DIR, "libpgen.so")
 
-PG_OK, PG_EINVAL, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_ENODEV = 0, -1, -2, -3, -4, -5
+PG_OK, PG_EINVAL, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_ENODEV, PG_ERANGE = 0, -1, -2, -3, -4, -5, -6
 PG_CONVERGED, PG_ROUNDLIMIT, PG_INFEASIBLE = 0, 1, 2
 PG_WIDE64, PG_NARROW32 = 0, 1
 PG_LOOP_GRAPH, PG_LOOP_HOST = 0, 1
@@ -123,6 +123,8 @@ PROTOTYPES = {
                                              _dp, _dp, _lp]),
     "pg_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "pg_session_attach_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32]),
+    "pg_csr_from_triplets": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, _ip, _ip, _dp, C.c_int32,
+                                       _ip, _ip, _dp, _lp]),
     "pg_last_error": (C.c_char_p, []),
     "pg_abi_version": (C.c_int32, []),
 }
@@ -162,6 +164,8 @@ def check(rc: int, what: str):
         msg = msg.decode() if msg else ""
         if rc == PG_EINVAL:
             raise ValueError(f"{what}: {msg}")
+        if rc == PG_ERANGE:  # std::out_of_range in the reference
+            raise IndexError(f"{what}: {msg}")
         raise EngineError(f"{what} failed ({rc}): {msg}")
 
 

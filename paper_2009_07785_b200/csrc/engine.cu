@@ -46,6 +46,7 @@
 #include "loop.cuh"
 #include "nodes.cuh"
 #include "narrow.cuh"
+#include "ingest.cuh"
 
 using namespace pgb;
 
@@ -1179,6 +1180,123 @@ int pg_round(const pg_problem* p, const pg_config* cfg, const double* lb_in, con
   });
   pg_session_destroy(s);
   return rc;
+}
+
+int pg_csr_from_triplets(int32_t num_rows, int32_t num_cols, int64_t count, const int32_t* rows,
+                         const int32_t* cols, const double* values, int32_t device,
+                         int32_t* row_ptr, int32_t* col_idx, double* values_out, int64_t* nnz) {
+  // csr_from_triplets (core/src/model.cpp:37-80) on the device (ingest.cuh)
+  if (!row_ptr || !nnz || (count > 0 && (!rows || !cols || !values || !col_idx || !values_out))) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  if (num_rows < 0 || num_cols < 0 || count < 0 || count > 0x7fffffffLL) {
+    g_err = "triplet count or dimensions out of the int32 range";
+    return PG_EINVAL;
+  }
+  return guarded([&] {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+      throw Error{PG_ENODEV, "no CUDA device visible (the B200 engine has no CPU fallback)"};
+    if (device < 0 || device >= ndev) throw Error{PG_EINVAL, "device ordinal out of range"};
+    const DevInfo prop = device_info(device);
+    PG_CUDA(cudaSetDevice(device));
+    cudaStream_t st;
+    PG_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    t_alloc_stream = st;
+    std::vector<void*> owned;
+    auto cleanup = [&] {
+      for (void* q : owned) dfree(q);
+      cudaStreamSynchronize(st);
+      cudaStreamDestroy(st);
+    };
+    try {
+      const int64_t m = num_rows;
+      auto grid = [&](int64_t items) {
+        return (int)std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, (int64_t)prop.sms * 8));
+      };
+      auto alloc = [&](size_t bytes) {
+        void* q = dalloc<unsigned char>(bytes);
+        owned.push_back(q);
+        return q;
+      };
+      int32_t* d_rows = (int32_t*)alloc(4 * (size_t)count);
+      int32_t* d_cols = (int32_t*)alloc(4 * (size_t)count);
+      double* d_vals = (double*)alloc(8 * (size_t)count);
+      auto* d_bad = (unsigned long long*)alloc(8);
+      int32_t* d_rcnt = (int32_t*)alloc(4 * ((size_t)m + 1));
+      if (count) {
+        PG_CUDA(cudaMemcpyAsync(d_rows, rows, 4 * (size_t)count, cudaMemcpyHostToDevice, st));
+        PG_CUDA(cudaMemcpyAsync(d_cols, cols, 4 * (size_t)count, cudaMemcpyHostToDevice, st));
+        PG_CUDA(cudaMemcpyAsync(d_vals, values, 8 * (size_t)count, cudaMemcpyHostToDevice, st));
+      }
+      PG_CUDA(cudaMemsetAsync(d_bad, 0xff, 8, st));
+      PG_CUDA(cudaMemsetAsync(d_rcnt, 0, 4 * ((size_t)m + 1), st));
+      unsigned long long bad = ~0ull;
+      if (count) {
+        k_trip_check<<<grid(count), 256, 0, st>>>(d_rows, d_cols, count, num_rows, num_cols, d_bad);
+        PG_CUDA(cudaGetLastError());
+        PG_CUDA(cudaMemcpyAsync(&bad, d_bad, 8, cudaMemcpyDeviceToHost, st));
+        PG_CUDA(cudaStreamSynchronize(st));
+      }
+      if (bad != ~0ull) {
+        // the reference checks the row of a triplet before its column
+        const int32_t r = rows[bad];
+        throw Error{PG_ERANGE, r < 0 || r >= num_rows ? "triplet row index out of range"
+                                                      : "triplet column index out of range"};
+      }
+      int colbits = 1, rowbits = 1;
+      while (colbits < 31 && (1ll << colbits) < num_cols) ++colbits;
+      while (rowbits < 31 && (1ll << rowbits) < num_rows) ++rowbits;
+      int64_t kept = 0;
+      if (count) {
+        auto* key = (unsigned long long*)alloc(8 * (size_t)count);
+        auto* key2 = (unsigned long long*)alloc(8 * (size_t)count);
+        double* val2 = (double*)alloc(8 * (size_t)count);
+        double* sum = (double*)alloc(8 * (size_t)count);
+        int32_t* keep = (int32_t*)alloc(4 * (size_t)count + 4);
+        int32_t* pos = (int32_t*)alloc(4 * (size_t)count + 4);
+        k_trip_keys<<<grid(count), 256, 0, st>>>(d_rows, d_cols, count, colbits, key);
+        size_t need = 0;
+        PG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, d_vals, val2, count, 0,
+                                                colbits + rowbits, st));
+        void* tmp = alloc(need);
+        PG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, key, key2, d_vals, val2, count, 0,
+                                                colbits + rowbits, st));
+        k_trip_runs<<<grid(count), 256, 0, st>>>(key2, val2, count, colbits, sum, keep, d_rcnt);
+        need = 0;
+        PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, keep, pos, count + 1, st));
+        void* tmp2 = alloc(need);
+        PG_CUDA(cudaMemsetAsync(keep + count, 0, 4, st));
+        PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp2, need, keep, pos, count + 1, st));
+        int32_t* d_ci = (int32_t*)alloc(4 * (size_t)count);
+        double* d_v = (double*)alloc(8 * (size_t)count);
+        k_trip_emit<<<grid(count), 256, 0, st>>>(key2, sum, keep, pos, count, colbits, d_ci, d_v);
+        PG_CUDA(cudaGetLastError());
+        int32_t k32 = 0;
+        PG_CUDA(cudaMemcpyAsync(&k32, pos + count, 4, cudaMemcpyDeviceToHost, st));
+        PG_CUDA(cudaStreamSynchronize(st));
+        kept = k32;
+        if (kept) {
+          PG_CUDA(cudaMemcpyAsync(col_idx, d_ci, 4 * (size_t)kept, cudaMemcpyDeviceToHost, st));
+          PG_CUDA(cudaMemcpyAsync(values_out, d_v, 8 * (size_t)kept, cudaMemcpyDeviceToHost, st));
+        }
+      }
+      int32_t* d_rp = (int32_t*)alloc(4 * ((size_t)m + 1));
+      size_t need = 0;
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, d_rcnt, d_rp, m + 1, st));
+      void* tmp3 = alloc(need);
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp3, need, d_rcnt, d_rp, m + 1, st));
+      PG_CUDA(cudaMemcpyAsync(row_ptr, d_rp, 4 * ((size_t)m + 1), cudaMemcpyDeviceToHost, st));
+      PG_CUDA(cudaStreamSynchronize(st));
+      *nnz = kept;
+    } catch (...) {
+      cleanup();
+      throw;
+    }
+    cleanup();
+    return PG_OK;
+  });
 }
 
 int pg_partition_row_blocks(const pg_problem* p, const pg_config* cfg, int32_t* starts,

@@ -4,6 +4,8 @@
                                           with cpu_seq verdicts when cfg.row_check
   propagate_round_gpu(instance, snap)   ~ propagate_round_parallel (par_engine.hpp:33-36)
   partition_row_blocks(matrix, cfg)     ~ partition_row_blocks (par_engine.hpp:12-13)
+  csr_from_triplets_gpu(rows, cols, ...) ~ csr_from_triplets (model.cpp:37-80), built on
+                                          the device (IndexError ~ std::out_of_range)
   Session(instance, cfg)                matrix resident in HBM; re-propagate new
                                         start bounds (B&B warm start) and node batches
 
@@ -20,8 +22,8 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import abi
-from .model import (EngineConfig, PropagationResult, ProblemInstance, VariableBounds,
-                    new_c_result, result_from_c)
+from .model import (EngineConfig, PropagationResult, ProblemInstance, SparseMatrix,
+                    VariableBounds, new_c_result, result_from_c)
 
 
 def _lib():
@@ -31,6 +33,30 @@ def _lib():
 def validate(cfg: EngineConfig) -> None:
     c = cfg.to_c()
     abi.check(_lib().pg_config_validate(C.byref(c)), "EngineConfig.validate")
+
+
+def csr_from_triplets_gpu(rows, cols, values, num_rows: int, num_cols: int,
+                          device: int = 0) -> SparseMatrix:
+    """csr_from_triplets (core/src/model.cpp:37-80) on the GPU: stable (row, col)
+    order, duplicates summed in input order, zero sums dropped; IndexError with
+    the reference's message for the first out-of-range triplet."""
+    r = np.ascontiguousarray(rows, dtype=np.int32)
+    c = np.ascontiguousarray(cols, dtype=np.int32)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    if not (r.shape == c.shape == v.shape) or r.ndim != 1:
+        raise ValueError("rows, cols and values must be 1-D arrays of one length")
+    cnt = r.shape[0]
+    rp = np.zeros(num_rows + 1, dtype=np.int32)
+    ci = np.empty(max(cnt, 1), dtype=np.int32)
+    vo = np.empty(max(cnt, 1), dtype=np.float64)
+    nnz = C.c_int64()
+    abi.check(_lib().pg_csr_from_triplets(num_rows, num_cols, cnt, abi.ptr(r, C.c_int32),
+                                          abi.ptr(c, C.c_int32), abi.ptr(v, C.c_double), device,
+                                          abi.ptr(rp, C.c_int32), abi.ptr(ci, C.c_int32),
+                                          abi.ptr(vo, C.c_double), C.byref(nnz)),
+              "csr_from_triplets")
+    k = int(nnz.value)
+    return SparseMatrix(num_rows, num_cols, rp, ci[:k], vo[:k])
 
 
 def propagate_gpu(instance: ProblemInstance, cfg: EngineConfig | None = None) -> PropagationResult:

@@ -3,11 +3,13 @@
 // -- what EngineId::Gpu in the reference harness would run.
 // Built by oracle/build_ref.sh against the unmodified reference sources.
 // Exit code = number of failed checks.
+#include <cstring>
 #include <cmath>
 #include <cstdio>
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "propgate/generators.hpp"
@@ -88,6 +90,38 @@ int main() {
   report("one round (test_par_engine.cpp:102-116)",
          o.changed && !o.infeasible && o.changes == 1 && snap.bounds_out.upper[1] == 0.0,
          "1 change, ub[1] = 0");
+  // csr_from_triplets (model.cpp:37-80): the reference's own builder vs the
+  // device build on shuffled triplets with duplicates and cancelling pairs
+  {
+    RandomInstanceOptions ro;
+    ro.num_rows = ro.num_cols = 20000;
+    ro.seed = 7;
+    ro.mean_row_nnz = 12.0;
+    const ProblemInstance big = gen_random(ro);
+    std::vector<std::tuple<int, int, double>> trip;
+    for (int r = 0; r < big.matrix.num_rows; ++r)
+      for (int k = big.matrix.row_ptr[r]; k < big.matrix.row_ptr[r + 1]; ++k) {
+        trip.emplace_back(r, big.matrix.col_idx[k], big.matrix.values[k]);
+        if (k % 5 == 0) trip.emplace_back(r, big.matrix.col_idx[k], 0.5);
+        if (k % 11 == 0) trip.emplace_back(r, big.matrix.col_idx[k], -big.matrix.values[k]);
+      }
+    for (size_t i = trip.size() - 1; i > 0; --i) std::swap(trip[i], trip[(i * 2654435761u) % (i + 1)]);
+    const SparseMatrix a = csr_from_triplets(trip, big.matrix.num_rows, big.matrix.num_cols);
+    const SparseMatrix b = csr_from_triplets_gpu(trip, big.matrix.num_rows, big.matrix.num_cols);
+    const bool same = a.row_ptr == b.row_ptr && a.col_idx == b.col_idx &&
+                      a.values.size() == b.values.size() &&
+                      std::memcmp(a.values.data(), b.values.data(), 8 * a.values.size()) == 0;
+    report("csr_from_triplets on the device (model.cpp:37-80)", same,
+           std::to_string(trip.size()) + " triplets -> " + std::to_string(a.values.size()) + " entries");
+    bool oor = false;
+    try {
+      const std::vector<std::tuple<int, int, double>> bad = {{0, 0, 1.0}, {0, 5, 1.0}};
+      csr_from_triplets_gpu(bad, 2, 2);
+    } catch (const std::out_of_range& e) {
+      oor = std::string(e.what()) == "triplet column index out of range";
+    }
+    report("bad triplet throws std::out_of_range", oor, "column 5 of 2");
+  }
   std::printf("%d check(s) failed\n", failures);
   return failures;
 }

@@ -19,8 +19,11 @@ restatement (oracle/liboracle.so) and the generator restatement
   c1.npz          config C1 (gen_random 10k x 10k, mean 8, 50% int), seeds 1-5
   partition.npz   partition_row_blocks on random row-length patterns
   rounds.npz      propagate_round_parallel on random snapshots
+  triplets.npz    csr_from_triplets (model.cpp:37-80): duplicates, cancelling
+                  sums, summation-order-sensitive runs, empty rows, range errors
 
-usage: python tests/golden/make_golden.py   (needs oracle/_ref built)
+usage: python tests/golden/make_golden.py [triplets]   (needs oracle/_ref built;
+       `triplets` regenerates triplets.npz only)
 """
 from __future__ import annotations
 
@@ -146,8 +149,60 @@ def save_result(prefix, r, out):
     out[prefix + "up"] = r.bounds.upper
 
 
+def triplet_cases():
+    """(name, m, n, rows, cols, vals) inputs of the csr_from_triplets vectors"""
+    rng = np.random.default_rng(37)
+    cases = []
+    k = 600
+    v = rng.integers(-3, 4, k).astype(np.float64)  # small integers: many sums cancel to 0
+    cases.append(("dups", 50, 40, rng.integers(0, 50, k), rng.integers(0, 6, k), v))
+    cases.append(("empty", 5, 3, np.zeros(0, int), np.zeros(0, int), np.zeros(0)))
+    cases.append(("sparse_rows", 100, 10, np.array([7, 7, 93, 3, 93]), np.array([2, 1, 9, 0, 9]),
+                  np.array([1.5, -2.0, 0.25, 4.0, -0.25])))
+    cases.append(("signed_zero", 3, 3, np.array([0, 0, 1, 2, 2]), np.array([1, 1, 2, 0, 0]),
+                  np.array([-0.0, 0.0, -0.0, 1e-300, -1e-300])))
+    # input order decides the rounding of a run: (1e16 + 1) - 1e16 vs (1e16 - 1e16) + 1
+    cases.append(("order", 2, 2, np.array([0, 1, 0, 1, 0, 1]), np.array([1, 1, 1, 1, 1, 1]),
+                  np.array([1e16, 1e16, 1.0, -1e16, -1e16, 1.0])))
+    k = 50000
+    rows = rng.integers(0, 2000, k)
+    cols = rng.integers(0, 3000, k)
+    dup = rng.integers(0, k, k // 10)
+    rows = np.concatenate([rows, rows[dup]])
+    cols = np.concatenate([cols, cols[dup]])
+    vals = rng.uniform(-10, 10, rows.shape[0])
+    vals[k:] = np.where(rng.random(dup.shape[0]) < 0.3, -vals[dup], vals[k:])
+    cases.append(("medium", 2000, 3000, rows, cols, vals))
+    cases.append(("bad_row", 4, 4, np.array([0, 1, 2, 3, 4, 0]), np.array([0, 1, 2, 3, 0, 9]),
+                  np.ones(6)))
+    cases.append(("bad_col_first", 4, 4, np.array([0, 1, 2, 0, 9]), np.array([0, 1, 2, -1, 0]),
+                  np.ones(5)))
+    cases.append(("bad_both", 4, 4, np.array([0, -1]), np.array([0, 7]), np.ones(2)))
+    return cases
+
+
+def triplet_vectors():
+    out = {}
+    for name, m, n, r, c, v in triplet_cases():
+        out[f"{name}/in"] = np.array([m, n], dtype=np.int64)
+        out[f"{name}/rows"] = np.asarray(r, dtype=np.int32)
+        out[f"{name}/cols"] = np.asarray(c, dtype=np.int32)
+        out[f"{name}/vals"] = np.asarray(v, dtype=np.float64)
+        try:
+            rp, ci, vo = O.csr_from_triplets(r, c, v, m, n, impl="reference")
+            out[f"{name}/row_ptr"] = rp
+            out[f"{name}/col_idx"] = ci
+            out[f"{name}/values"] = vo
+        except IndexError as e:
+            out[f"{name}/error"] = np.array(str(e))
+    return out
+
+
 def main():
     assert O.ref_available(), "build oracle/_ref first (oracle/build_ref.sh)"
+    if sys.argv[1:] == ["triplets"]:
+        np.savez_compressed(os.path.join(HERE, "triplets.npz"), **triplet_vectors())
+        return
     rng = np.random.default_rng(20090778)
     np.savez_compressed(os.path.join(HERE, "propcore.npz"), **propcore_vectors(rng))
 
@@ -259,6 +314,7 @@ def main():
         out[f"{t}/ub_out"] = r["upper"]
         out[f"{t}/outcome"] = np.array([r["changed"], r["infeasible"], r["changes"]], dtype=np.int64)
     np.savez_compressed(os.path.join(HERE, "rounds.npz"), **out)
+    np.savez_compressed(os.path.join(HERE, "triplets.npz"), **triplet_vectors())
     for f in sorted(os.listdir(HERE)):
         print(f, os.path.getsize(os.path.join(HERE, f)))
 

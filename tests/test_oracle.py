@@ -273,3 +273,42 @@ def test_f32_mode_matches_reference():
         assert same(a.bounds.lower, b.bounds.lower) and same(a.bounds.upper, b.bounds.upper)
         a, b = O.propagate_sequential(inst, cfg), O.ref_propagate_sequential(inst, cfg)
         assert same(a.bounds.lower, b.bounds.lower) and same(a.bounds.upper, b.bounds.upper)
+
+
+def _triplet_cases():
+    d = load("triplets.npz")
+    names = sorted({k.split("/")[0] for k in d.files})
+    return d, names
+
+
+def test_csr_from_triplets_golden():
+    """csr_from_triplets (model.cpp:37-80): the C restatement reproduces the
+    reference's CSR (order, duplicate sums, dropped zeros) and its
+    out_of_range messages on every golden case"""
+    d, names = _triplet_cases()
+    assert len(names) >= 9
+    for name in names:
+        m, n = (int(x) for x in d[f"{name}/in"])
+        args = (d[f"{name}/rows"], d[f"{name}/cols"], d[f"{name}/vals"], m, n)
+        if f"{name}/error" in d.files:
+            with pytest.raises(IndexError, match=str(d[f"{name}/error"])):
+                O.csr_from_triplets(*args)
+            continue
+        rp, ci, v = O.csr_from_triplets(*args)
+        np.testing.assert_array_equal(rp, d[f"{name}/row_ptr"])
+        np.testing.assert_array_equal(ci, d[f"{name}/col_idx"])
+        assert v.tobytes() == d[f"{name}/values"].tobytes(), name
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_csr_from_triplets_vs_reference_live():
+    rng = np.random.default_rng(5)
+    for trial in range(5):
+        m, n, k = 300, 200, 20000
+        r = rng.integers(0, m, k)
+        c = rng.integers(0, 8 if trial % 2 else n, k)
+        v = rng.integers(-2, 3, k).astype(np.float64) if trial < 3 else rng.normal(size=k)
+        a = O.csr_from_triplets(r, c, v, m, n)
+        b = O.csr_from_triplets(r, c, v, m, n, impl="reference")
+        for x, y in zip(a, b):
+            assert x.tobytes() == y.tobytes()
