@@ -401,7 +401,8 @@ def bench_rowshard(args, inst, world, rank, local):
     from paper_2009_07785_b200.model import EngineConfig
     from paper_2009_07785_b200.multi import RowShardedSession
 
-    cfg = EngineConfig(device=local, worklist=args.worklist)
+    delta = bool(args.delta if args.delta is not None else world > 1)
+    cfg = EngineConfig(device=local, worklist=args.worklist, delta_exchange=delta)
     rs = RowShardedSession(inst, cfg, rank, world)
     for _ in range(args.warmup):
         r = rs.run()
@@ -421,8 +422,11 @@ def bench_rowshard(args, inst, world, rank, local):
     R = r.rounds_executed
     line = _common_line(args, world, ms, "strong", "c5", {
         "instance": inst.name, "m": m, "n": n, "nnz": nnz,
-        "parallelism": f"row-sharded x{world} (NCCL max all-reduce of bound keys)",
-        "worklist": args.worklist})
+        "parallelism": f"row-sharded x{world} (NCCL max all-reduce of bound keys"
+                       + (", sparse delta all-gather when every rank changed <= n/16 columns)"
+                          if delta else ")"),
+        "worklist": args.worklist, "delta_exchange": delta})
+    line["delta_rounds"] = rs.session.info()["delta_rounds"]
     line.update({"rounds": R, "status": r.status.name, "rounds_per_s": round(R / (ms / 1e3), 1),
                  "gbs_per_round": round(b_round(m, n, nnz) * R / (ms / 1e3) / 1e9, 1),
                  "clocks": clk.summary(), "gpu_launches": None,
@@ -448,6 +452,8 @@ def main():
     ap.add_argument("--worklist", type=int, default=None,
                     help="device-side worklist (exact); default: on for c2 and c5 (few rows "
                          "change after the first rounds), off for c1/c3 (faster as full sweeps)")
+    ap.add_argument("--delta", type=int, default=None,
+                    help="c5: sparse delta exchange rounds (default: on when world > 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--loop", default="graph", choices=["graph", "host"],
                     help="host: one launch per kernel per round (for ncu launch lists: ncu "

@@ -60,6 +60,13 @@ extern "C" {
  * whose bound changed in the previous round (exact under snapshot
  * semantics). */
 #define PG_FLAG_WORKLIST 0x2u
+/* Row-sharded sessions (pg_session_attach_comm): a round in which every rank
+ * changed at most num_cols / 16 columns exchanges only those columns (NCCL
+ * all-gather of (column, keys) items, max-merged on every rank) instead of
+ * the dense all-reduce of every bound.  Results
+ * are identical either way; the solve runs the host-driven loop (the choice
+ * reads the gathered counts on the host each round). */
+#define PG_FLAG_DELTA_EXCHANGE 0x4u
 
 /* Problem in CSR form: the fields of propgate::ProblemInstance
  * (core/include/propgate/model.hpp:20-37, 68-79).  int32 row_ptr/col_idx,
@@ -222,7 +229,8 @@ int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank,
  * chains each), split-candidate rows (> 16 entries), segments (chains of
  * those rows), short rows, short-row entries, segment entries, chains,
  * sliced-ELL elements (entries + padding), split rows (> nnz_budget),
- * persistent loop (1: the whole solve is one cooperative kernel). */
+ * persistent loop (1: the whole solve is one cooperative kernel), rounds of
+ * the last solve that used the sparse delta exchange. */
 int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info);
 
 /* Thread-local message of the last failed call on this thread. */

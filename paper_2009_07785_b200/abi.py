@@ -21,7 +21,7 @@ PG_OK, PG_EINVAL, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_ENODEV, PG_ERANGE = 0, -1, -
 PG_CONVERGED, PG_ROUNDLIMIT, PG_INFEASIBLE = 0, 1, 2
 PG_WIDE64, PG_NARROW32 = 0, 1
 PG_LOOP_GRAPH, PG_LOOP_HOST = 0, 1
-PG_FLAG_ROWCHECK, PG_FLAG_WORKLIST = 0x1, 0x2
+PG_FLAG_ROWCHECK, PG_FLAG_WORKLIST, PG_FLAG_DELTA_EXCHANGE = 0x1, 0x2, 0x4
 
 STATUS_NAMES = {PG_CONVERGED: "Converged", PG_ROUNDLIMIT: "RoundLimit", PG_INFEASIBLE: "Infeasible"}
 

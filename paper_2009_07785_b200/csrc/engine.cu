@@ -157,6 +157,7 @@ struct PhaseTimer {
 // Values from nccl.h: ncclInt64 = 4, ncclMax = 2; ncclUniqueId = 128 bytes.
 constexpr int kNcclInt64 = 4;
 constexpr int kNcclMax = 2;
+constexpr int kNcclInt32 = 2;
 struct NcclUid {
   char internal[128];
 };
@@ -166,6 +167,7 @@ struct Nccl {
   int (*comm_init_rank)(void**, int, NcclUid, int) = nullptr;
   int (*comm_destroy)(void*) = nullptr;
   int (*all_reduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*all_gather_fn)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
   const char* (*error_string)(int) = nullptr;
   bool load() {
     if (h) return true;
@@ -179,8 +181,10 @@ struct Nccl {
     comm_destroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
     all_reduce_fn = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
         h, "ncclAllReduce");
+    all_gather_fn = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(
+        h, "ncclAllGather");
     error_string = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
-    return get_unique_id && comm_init_rank && comm_destroy && all_reduce_fn;
+    return get_unique_id && comm_init_rank && comm_destroy && all_reduce_fn && all_gather_fn;
   }
   int all_reduce(const void* s, void* r, size_t count, int dt, int op, void* comm,
                  cudaStream_t st) const {
@@ -267,6 +271,16 @@ struct pg_session {
   cudaStream_t stream2 = nullptr;  // session setup: ordering overlapped with the upload
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* comm = nullptr;  // NCCL communicator of the row-sharded mode
+  int32_t rank = 0, world = 1;
+  // sparse delta exchange (PG_FLAG_DELTA_EXCHANGE): this rank's items, every
+  // rank's items, counts; rounds of the last solve that used it
+  DeltaItem* d_delta = nullptr;
+  DeltaItem* d_delta_all = nullptr;
+  int* d_dcnt = nullptr;
+  int* d_dcnt_all = nullptr;
+  int* h_dcnt = nullptr;
+  int32_t delta_cap = 0, delta_rounds = 0;
+  bool delta_mode() const { return comm && (cfg.flags & PG_FLAG_DELTA_EXCHANGE); }
   // branch-and-bound: the root fixpoint and the next solve's start control
   NodeCtl* d_ctl = nullptr;
   double* d_root_lo = nullptr;
@@ -284,7 +298,10 @@ struct pg_session {
     if (ev_join) cudaEventDestroy(ev_join);
     if (stream2) cudaStreamDestroy(stream2);
     if (comm) g_nccl.comm_destroy(comm);
-    for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up}) dfree(p);
+    for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up, (void*)d_delta,
+                    (void*)d_delta_all, (void*)d_dcnt, (void*)d_dcnt_all})
+      dfree(p);
+    if (h_dcnt) cudaFreeHost(h_dcnt);
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
                     d_lo_res, d_up_res, d_segs, d_srow, d_sfirst, d_partial,
                     d_ract, d_wl_short, d_wl_long, d_f32_part, d_split, d_bnd, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
@@ -372,7 +389,36 @@ struct pg_session {
       k_cand<<<num_sms * cand_per_sm, kCandThreads, 0, stream>>>(A, dcfg);
     }
     if (k1_end) PG_CUDA(cudaEventRecord(k1_end, stream));
-    if (comm) {
+    bool dense_exchange = comm != nullptr;
+    if (comm && delta_mode() && !use_graph) {
+      // sparse delta exchange: all-gather the
+      // counts; when every rank changed at most delta_cap columns, all-gather
+      // the (column, keys) items and max-merge them, else the dense all-reduce.
+      // The choice reads the gathered counts, so every rank makes the same one.
+      PG_CUDA(cudaMemsetAsync(d_dcnt, 0, 2 * sizeof(int), stream));
+      k_delta_compact<<<grid_for(n, 256, 8), 256, 0, stream>>>(d_bnd, d_key_out, n, d_st, d_delta,
+                                                                delta_cap, d_dcnt);
+      PG_CUDA(cudaGetLastError());
+      int rc = g_nccl.all_gather_fn(d_dcnt, d_dcnt_all, 2, kNcclInt32, comm, stream);
+      if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllGather: ") + g_nccl.error(rc)};
+      PG_CUDA(cudaMemcpyAsync(h_dcnt, d_dcnt_all, 2 * sizeof(int) * world, cudaMemcpyDeviceToHost,
+                              stream));
+      PG_CUDA(cudaStreamSynchronize(stream));
+      int maxc = 0;
+      for (int r = 0; r < world; ++r) maxc = std::max(maxc, h_dcnt[2 * r]);
+      if (maxc <= delta_cap) {
+        dense_exchange = false;
+        ++delta_rounds;
+        if (maxc > 0) {
+          rc = g_nccl.all_gather_fn(d_delta, d_delta_all, 3 * (size_t)maxc, kNcclInt64, comm, stream);
+          if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllGather: ") + g_nccl.error(rc)};
+        }
+        k_delta_apply<<<grid_for(std::max(maxc, 1), 256, 8), 256, 0, stream>>>(
+            d_delta_all, d_dcnt_all, world, maxc, d_key_out, d_st);
+        PG_CUDA(cudaGetLastError());
+      }
+    }
+    if (dense_exchange) {
       // row shards: merge every rank's bound keys (lb keys and negated ub keys)
       // and infeasibility with one max all-reduce; each rank then commits the
       // same merged bounds, so counts and decisions need no further exchange
@@ -528,7 +574,8 @@ struct pg_session {
   // fault per 4 KB inside the copy otherwise)
   int64_t run_solve(bool check_crossed = true, pg_result* res = nullptr) {
     bounds_done = false;
-    if (cfg.loop_mode == PG_LOOP_GRAPH && check_crossed) {
+    delta_rounds = 0;
+    if (cfg.loop_mode == PG_LOOP_GRAPH && check_crossed && !delta_mode()) {
       PG_CUDA(cudaEventRecord(ev0, stream));
       PG_CUDA(cudaGraphLaunch(exec, stream));
       PG_CUDA(cudaEventRecord(ev1, stream));
@@ -1644,6 +1691,20 @@ int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank, i
     if (rc != 0) throw Error{PG_ENCCL, std::string("ncclCommInitRank: ") + g_nccl.error(rc)};
     if (s->comm) g_nccl.comm_destroy(s->comm);
     s->comm = comm;
+    s->rank = rank;
+    s->world = world;
+    t_alloc_stream = s->stream;
+    for (void* p : {(void*)s->d_delta, (void*)s->d_delta_all, (void*)s->d_dcnt, (void*)s->d_dcnt_all})
+      dfree(p);
+    if (s->h_dcnt) cudaFreeHost(s->h_dcnt);
+    // a round whose every rank changed at most n/16 columns goes sparse
+    // (C5 changes <= 253k of 10M sides after round 1)
+    s->delta_cap = std::max(1024, s->n / 16);
+    s->d_delta = dalloc<DeltaItem>(s->delta_cap);
+    s->d_delta_all = dalloc<DeltaItem>((size_t)s->delta_cap * world);
+    s->d_dcnt = dalloc<int>(2);
+    s->d_dcnt_all = dalloc<int>(2 * (size_t)world);
+    PG_CUDA(cudaMallocHost(&s->h_dcnt, 2 * sizeof(int) * world));
     // the device-resident loop now carries the all-reduce: rebuild the graph
     if (s->exec) {
       cudaGraphExecDestroy(s->exec);
@@ -1665,7 +1726,7 @@ int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info) {
   }
   const int64_t v[] = {s->m, s->n, s->nnz, s->nslices, s->nsrow, s->nseg,
                        s->short_rows, s->short_nnz, s->seg_nnz, s->nunits, s->sell_elems,
-                       s->nsplit, s->use_persistent() ? 1 : 0};
+                       s->nsplit, s->use_persistent() ? 1 : 0, s->delta_rounds};
   for (int i = 0; i < n_info && i < (int)(sizeof(v) / sizeof(v[0])); ++i) info[i] = v[i];
   return PG_OK;
 }

@@ -665,6 +665,57 @@ __global__ void k_flag_to_slot(const DevState* __restrict__ st, longlong2* __res
   if (threadIdx.x == 0) slot->x = ld_gpu(&st->infeasible) ? 1 : 0;
 }
 
+// ---- row shards: sparse delta exchange ---------------
+// A round's local merges as (column, lb key, negated ub key) items; the ranks
+// all-gather them and apply them with the same max merges as the dense
+// all-reduce, so key_out ends identical on every rank either way.
+struct DeltaItem {
+  long long col, lo, nup;
+};
+
+// cnt[0] = this rank's changed columns (items past `cap` are not written),
+// cnt[1] = its infeasibility flag; cnt zeroed before the launch
+__global__ void __launch_bounds__(256)
+    k_delta_compact(const double2* __restrict__ bnd, const longlong2* __restrict__ key_out, int n,
+                    const DevState* __restrict__ st, DeltaItem* __restrict__ out, int cap,
+                    int* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  if (blockIdx.x == 0 && threadIdx.x == 0) cnt[1] = ld_gpu(&st->infeasible) ? 1 : 0;
+  for (int j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; j0 < n; j0 += gridDim.x * blockDim.x) {
+    const int j = j0 + lane;
+    bool ch = false;
+    longlong2 k = make_longlong2(0, 0);
+    if (j < n) {
+      const double2 b = bnd[j];
+      k = key_out[j];
+      ch = k.x != key_enc(b.x) || k.y != -key_enc(b.y);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, ch);
+    if (!m) continue;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(cnt, __popc(m));
+    base = __shfl_sync(0xffffffffu, base, 0) + __popc(m & ((1u << lane) - 1u));
+    if (ch && base < cap) out[base] = DeltaItem{j, k.x, k.y};
+  }
+}
+
+// every rank's items (rank r: all[r * stride .. + cnt_all[2r]]) merged by max
+__global__ void __launch_bounds__(256)
+    k_delta_apply(const DeltaItem* __restrict__ all, const int* __restrict__ cnt_all, int world,
+                  int stride, longlong2* __restrict__ key_out, DevState* __restrict__ st) {
+  if (blockIdx.x == 0 && threadIdx.x < world && cnt_all[2 * threadIdx.x + 1]) st->infeasible = 1;
+  for (int r = 0; r < world; ++r) {
+    const int c = min(cnt_all[2 * r], stride);
+    const DeltaItem* a = all + (size_t)r * stride;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < c; i += gridDim.x * blockDim.x) {
+      const DeltaItem d = a[i];
+      long long* k = reinterpret_cast<long long*>(key_out + d.col);
+      red_max(k, d.lo);
+      red_max(k + 1, d.nup);
+    }
+  }
+}
+
 // keys -> doubles (result download)
 __global__ void k_decode(const longlong2* __restrict__ key, double* __restrict__ lo,
                          double* __restrict__ up, int n) {

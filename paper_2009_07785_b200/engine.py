@@ -120,7 +120,8 @@ class Session:
     """One problem resident on the device (pg_session_*)."""
 
     INFO_FIELDS = ("m", "n", "nnz", "slices", "seg_rows", "segments", "short_rows", "short_nnz",
-                   "seg_nnz", "chains", "sell_elems", "split_rows", "persistent")
+                   "seg_nnz", "chains", "sell_elems", "split_rows", "persistent",
+                   "delta_rounds")
 
     def __init__(self, instance: ProblemInstance, cfg: EngineConfig | None = None):
         self.cfg = cfg or EngineConfig()

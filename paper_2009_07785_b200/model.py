@@ -154,6 +154,7 @@ class EngineConfig:
     loop_mode: LoopMode = LoopMode.Graph
     row_check: bool = True
     worklist: bool = False
+    delta_exchange: bool = False  # row shards: sparse delta rounds (PG_FLAG_DELTA_EXCHANGE)
 
     def to_c(self) -> abi.PgConfig:
         c = abi.PgConfig()
@@ -168,8 +169,9 @@ class EngineConfig:
         c.scalar_mode = int(self.scalar_mode)
         c.device = self.device
         c.loop_mode = int(self.loop_mode)
-        c.flags = (abi.PG_FLAG_ROWCHECK if self.row_check else 0) | (
-            abi.PG_FLAG_WORKLIST if self.worklist else 0)
+        c.flags = ((abi.PG_FLAG_ROWCHECK if self.row_check else 0) |
+                   (abi.PG_FLAG_WORKLIST if self.worklist else 0) |
+                   (abi.PG_FLAG_DELTA_EXCHANGE if self.delta_exchange else 0))
         return c
 
 

@@ -79,6 +79,33 @@ def test_row_sharded_nccl_world1(loop, worklist):
     rs.close()
 
 
+@pytest.mark.parametrize("worklist", [False, True])
+def test_row_sharded_delta_exchange_world1(worklist):
+    """Sparse delta rounds (compaction, NCCL all-gather of counts and items,
+    max-merge) in place of the dense all-reduce: identical results, and the
+    rounds after the first dense one actually go sparse."""
+    try:
+        from paper_2009_07785_b200.multi import nccl_unique_id
+        nccl_unique_id()
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    for inst in (G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003),
+                 G.gen_random(4000, 4000, 9, mean_row_nnz=10.0, integral_fraction=0.5)):
+        cfg = EngineConfig(row_check=False, worklist=worklist, delta_exchange=True)
+        rs = RowShardedSession(inst, cfg, rank=0, world=1)
+        try:
+            r = rs.propagate()
+            assert_bit_exact(r, O.propagate_parallel(inst, PAR), inst.name)
+            info = rs.session.info()
+            assert 0 < info["delta_rounds"] <= r.rounds_executed, info
+        finally:
+            rs.close()
+    bad = G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003, infeasible=True)
+    rs = RowShardedSession(bad, EngineConfig(delta_exchange=True), rank=0, world=1)
+    assert rs.propagate().status == PropagationStatus.Infeasible
+    rs.close()
+
+
 @pytest.mark.slow
 def test_c2_full_seeds_properties():
     """C2 full size, two more seeds: bit-exact to the restated cpu_par, and

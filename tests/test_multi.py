@@ -134,6 +134,92 @@ def test_row_sharded_merge_is_bit_identical_gloo():
     assert res[0][1][0] == int(PropagationStatus.Infeasible)  # the infeasible C5 variant
 
 
+def _delta_worker(rank, world, port, insts, cap_div, q):
+    """PG_FLAG_DELTA_EXCHANGE's protocol (engine.cu enqueue_round, kernels.cuh
+    k_delta_compact / k_delta_apply): compact this rank's changed columns as
+    (col, lb key, -ub key), all-gather [count, infeasible]; when every count
+    is <= cap all-gather the items padded to the max count and max-merge
+    them, else fall back to the dense max all-reduce."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    out = []
+    for inst in insts:
+        r0, r1 = row_shards(inst.matrix.row_ptr, world)[rank]
+        n = inst.num_cols()
+        cap = max(1, n // cap_div)
+        lo = np.where(np.abs(inst.bounds.lower) >= 1e20, np.sign(inst.bounds.lower) * np.inf,
+                      inst.bounds.lower)
+        up = np.where(np.abs(inst.bounds.upper) >= 1e20, np.sign(inst.bounds.upper) * np.inf,
+                      inst.bounds.upper)
+        per_round, status, sparse = [], None, 0
+        for rnd in range(1, PAR.round_limit + 1):
+            lo_out, up_out = lo.copy(), up.copy()
+            inf = O.round_rows(inst, PAR, r0, r1, lo, up, lo_out, up_out)
+            klo, knup = _key(lo_out), -_key(up_out)
+            changed = np.nonzero((klo != _key(lo)) | (knup != -_key(up)))[0]
+            cnt = torch.tensor([changed.shape[0], int(inf)], dtype=torch.int64)
+            cnts = [torch.zeros(2, dtype=torch.int64) for _ in range(world)]
+            dist.all_gather(cnts, cnt)
+            maxc = max(int(c[0]) for c in cnts)
+            if maxc <= cap:
+                sparse += 1
+                items = np.zeros((maxc, 3), dtype=np.int64)
+                items[:changed.shape[0]] = np.stack([changed, klo[changed], knup[changed]], 1)
+                got = [torch.zeros((maxc, 3), dtype=torch.int64) for _ in range(world)]
+                dist.all_gather(got, torch.from_numpy(items))
+                mlo, mnup = _key(lo), -_key(up)  # the round's input keys on every rank
+                for r in range(world):
+                    it = got[r].numpy()[: int(cnts[r][0])]
+                    np.maximum.at(mlo, it[:, 0], it[:, 1])
+                    np.maximum.at(mnup, it[:, 0], it[:, 2])
+                lo_out, up_out = _unkey(mlo), _unkey(-mnup)
+                inf = any(int(c[1]) for c in cnts)
+            else:
+                buf = torch.from_numpy(np.concatenate([klo, knup, [int(inf)]]))
+                dist.all_reduce(buf, op=dist.ReduceOp.MAX)
+                b = buf.numpy()
+                lo_out, up_out, inf = _unkey(b[:n]), _unkey(-b[n:2 * n]), bool(b[2 * n])
+            ch, cinf = O.commit(lo, up, lo_out, up_out)
+            per_round.append(ch)
+            if inf or cinf:
+                status = PropagationStatus.Infeasible
+            elif ch == 0:
+                status = PropagationStatus.Converged
+            elif rnd == PAR.round_limit:
+                status = PropagationStatus.RoundLimit
+            lo, up = lo_out, up_out
+            if status is not None:
+                break
+        out.append((int(status), per_round, lo, up, sparse))
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cap_div", [16, 400])
+def test_row_sharded_delta_exchange_gloo(cap_div):
+    """the sparse delta rounds give the unsharded trajectory bit for bit, with
+    the product's cap (n/16) and with a small cap that forces dense fallbacks"""
+    insts = [G.gen_setpart(4000, 20000, 20, f_fixed=0.2, seed=5001),
+             G.gen_setpart(4000, 20000, 20, f_fixed=0.2, seed=5002, infeasible=True),
+             G.gen_random(3000, 2500, 11, mean_row_nnz=9.0, integral_fraction=0.5)]
+    res = _spawn(_delta_worker, 3, insts, cap_div)
+    total_sparse = 0
+    for i, inst in enumerate(insts):
+        ref = O.propagate_parallel(inst, PAR)
+        for rank in (0, 1, 2):
+            status, per_round, lo, up, sparse = res[rank][i]
+            assert status == int(ref.status), (inst.name, rank)
+            assert per_round == ref.per_round_changes, (inst.name, rank)
+            assert np.array_equal(O.canon(lo), O.canon(ref.bounds.lower))
+            assert np.array_equal(O.canon(up), O.canon(ref.bounds.upper))
+            assert sparse <= len(per_round)
+        total_sparse += res[0][i][4]
+        if cap_div == 16 and i == 0:  # C5-like: every round after the first is sparse
+            assert res[0][i][4] >= 1
+    assert total_sparse >= 1
+
+
 def _node_worker(rank, world, port, inst, lo, up, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
