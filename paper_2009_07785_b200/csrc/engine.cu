@@ -272,6 +272,19 @@ struct pg_session {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* comm = nullptr;  // NCCL communicator of the row-sharded mode
   int32_t rank = 0, world = 1;
+  // sum(len^2) / (n nnz): how often consecutive entries of a row hit
+  // neighbouring columns; dense rows gather the 16 B bounds records (two per
+  // sector), sparse ones the 32 B snapshot records (filter coefficient q
+  // precomputed, no per-entry recompute) when those fit in L2 beside the
+  // streamed matrix
+  double row_density = 0.0;
+  bool gather16() const {
+    static const char* e = getenv("PG_SELL_GATHER");
+    if (e) return atoi(e) == 16;
+    // the 32 B records must also stay L2-resident next to the streamed matrix
+    // (C5: 5M columns = 160 MB of snapshot records, 80 MB of bounds)
+    return row_density > 0.05 || (double)n * sizeof(Snap) > 48e6;
+  }
   // sparse delta exchange (PG_FLAG_DELTA_EXCHANGE): this rank's items, every
   // rank's items, counts; rounds of the last solve that used it
   DeltaItem* d_delta = nullptr;
@@ -352,6 +365,22 @@ struct pg_session {
     return A;
   }
 
+  // phase 1 over the sliced-ELL copy: the full sweep, and with the worklist
+  // the worklist sweep (each returns at once when the round is of the other kind)
+  template <bool kB16>
+  void launch_sell(const RoundArgsG<kB16>& G, int grid, bool rowcheck) {
+    if (rowcheck)
+      k_sell<true, true, kB16><<<grid, kSellThreads, kSellSmem, stream>>>(G, dcfg);
+    else
+      k_sell<false, true, kB16><<<grid, kSellThreads, kSellSmem, stream>>>(G, dcfg);
+    if (dirty.enabled) {
+      if (rowcheck)
+        k_sell<true, false, kB16><<<grid, kSellThreads, kSellSmem, stream>>>(G, dcfg);
+      else
+        k_sell<false, false, kB16><<<grid, kSellThreads, kSellSmem, stream>>>(G, dcfg);
+    }
+  }
+
   // One round: phase 1 (k_sell), phase 2 (k_cand), [row shards: all-reduce],
   // commit + decision (k_commit), [worklist: k_mark].  k1_begin/k1_end
   // bracket the two compute phases (bench.py's roofline timing).
@@ -369,16 +398,10 @@ struct pg_session {
       }
     } else if (nslices > 0) {
       const int grid = std::max(1, std::min((nslices + 7) / 8, num_sms * sell_per_sm));
-      if (rowcheck)
-        k_sell<true, true><<<grid, kSellThreads, kSellSmem, stream>>>(A, dcfg);
+      if (gather16())
+        launch_sell(RoundArgsG<true>{A}, grid, rowcheck);
       else
-        k_sell<false, true><<<grid, kSellThreads, kSellSmem, stream>>>(A, dcfg);
-      if (dirty.enabled) {
-        if (rowcheck)
-          k_sell<true, false><<<grid, kSellThreads, kSellSmem, stream>>>(A, dcfg);
-        else
-          k_sell<false, false><<<grid, kSellThreads, kSellSmem, stream>>>(A, dcfg);
-      }
+        launch_sell(RoundArgsG<false>{A}, grid, rowcheck);
       if (nsplit > 0) {
         const int g = std::max(1, std::min((nsplit + kSplitWarps - 1) / kSplitWarps, num_sms * 8));
         if (rowcheck)
@@ -695,14 +718,21 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       std::lock_guard<std::mutex> lock(mu);
       Occ& o = occ[s->dev];
       if (!o.ok) {
-        for (const void* f : {(const void*)k_sell<true, true>, (const void*)k_sell<false, true>,
-                              (const void*)k_sell<true, false>, (const void*)k_sell<false, false>})
+        for (const void* f :
+             {(const void*)k_sell<true, true, true>, (const void*)k_sell<false, true, true>,
+              (const void*)k_sell<true, false, true>, (const void*)k_sell<false, false, true>,
+              (const void*)k_sell<true, true, false>, (const void*)k_sell<false, true, false>,
+              (const void*)k_sell<true, false, false>, (const void*)k_sell<false, false, false>})
           PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem));
         for (const void* f : {(const void*)k_loop<true>, (const void*)k_loop<false>})
           PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(LoopSmem)));
-        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.sell, k_sell<true, true>,
+        int o16 = 0;
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.sell, k_sell<true, true, false>,
                                                               kSellThreads, kSellSmem));
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o16, k_sell<true, true, true>,
+                                                              kSellThreads, kSellSmem));
+        o.sell = std::min(o.sell, o16);
         PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.cand, k_cand, kCandThreads, 0));
         int per = 0, per2 = 0;
         PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_loop<true>, kSellThreads,
@@ -760,7 +790,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     int32_t* idx = dalloc<int32_t>(m);
     int32_t* t_perm = dalloc<int32_t>(m);
     int32_t* slen = dalloc<int32_t>((size_t)m + 1);
-    int32_t* counts = dalloc<int32_t>(kMaxClasses + 4);
+    int32_t* counts = dalloc<int32_t>(kMaxClasses + 4);  // + u64 sum of len^2 at [kMaxClasses + 2]
     PG_CUDA(cudaEventRecord(s->ev_fork, st));
     PG_CUDA(cudaStreamWaitEvent(s2, s->ev_fork, 0));
     // stream 1: the bulk of the upload (asynchronous from pinned memory)
@@ -802,8 +832,14 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, slen, s->d_row_ptr, m + 1, s2));
       PG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (kMaxClasses + 4), s2));
       k_class_counts<<<s->grid_for(m, 256), 256, 0, s2>>>(key2, m, counts);
-      PG_CUDA(cudaMemcpyAsync(cls.data(), counts, sizeof(int32_t) * nb, cudaMemcpyDeviceToHost, s2));
+      auto* len2 = reinterpret_cast<unsigned long long*>(counts + kMaxClasses + 2);
+      k_len2_sum<<<s->grid_for(m, 256), 256, 0, s2>>>(t_rp, m, len2);
+      PG_CUDA(cudaMemcpyAsync(cls.data(), counts, sizeof(int32_t) * (kMaxClasses + 4),
+                              cudaMemcpyDeviceToHost, s2));
       PG_CUDA(cudaStreamSynchronize(s2));
+      unsigned long long l2 = 0;
+      std::memcpy(&l2, cls.data() + kMaxClasses + 2, sizeof(l2));
+      s->row_density = (double)l2 / std::max(1.0, (double)n * (double)nnz);
     }
     TileLayout lay{};
     lay.nclass = short_max + 1;

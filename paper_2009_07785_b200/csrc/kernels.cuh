@@ -356,6 +356,16 @@ struct RoundArgs {
   Touch touch;            // worklist rounds: merged-into columns (kernels.cuh)
 };
 
+// RoundArgs with the gather record fixed at compile time (sell.cuh ld_col):
+// 16 B bounds records for rows dense in the columns, else 32 B snapshot
+// records; plain RoundArgs gathers the snapshot records
+template <bool kB16>
+struct RoundArgsG : RoundArgs {};
+template <class RA>
+constexpr bool gather16_v = false;
+template <>
+constexpr bool gather16_v<RoundArgsG<true>> = true;
+
 // A row's activity is complete: row check (propcore.hpp:147-156, cpu_seq's
 // verdicts), exactness-preserving row filter, and -- if some entry may
 // tighten -- queue the row for phase 2.

@@ -43,14 +43,8 @@ namespace pgb {
 #ifndef PG_SELL_PF
 #define PG_SELL_PF 1
 #endif
-#ifndef PG_SELL_B16
-#define PG_SELL_B16 1  // gather 16 B {lb, ub} from the compact bounds array
-#endif
 #ifndef PG_SELL_GROUP
 #define PG_SELL_GROUP 2  // narrow one-lane slices per work item
-#endif
-#ifndef PG_SELL_B16
-#define PG_SELL_B16 1  // gather 16 B {lb, ub} from the compact bounds array
 #endif
 #ifndef PG_SELL_GROUPW
 #define PG_SELL_GROUPW 16  // slices at most this wide are grouped
@@ -138,21 +132,23 @@ __device__ __forceinline__ double column_q_inline(double lo, double up, bool int
 }
 
 // the gathered record of column c: {lb, ub} and the filter coefficient q --
-// 16 B from the compact bounds array (half the L2 footprint of the snapshot
-// records; q recomputed, column_q) or the 32 B snapshot record
-__device__ __forceinline__ void ld_col(const RoundArgs& A, int32_t c, uint64_t pol, bool frac_any,
+// 16 B from the compact bounds array (two columns per sector: rows dense in
+// the columns, config C3; q recomputed, column_q) or the 32 B snapshot record
+// (q precomputed: sparse rows, one sector per entry either way)
+template <class RA>
+__device__ __forceinline__ void ld_col(const RA& A, int32_t c, uint64_t pol, bool frac_any,
                                        const DevCfg& cfg, double& lo, double& up, double& q) {
-#if PG_SELL_B16
-  double2 b;
-  asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
-               : "=d"(b.x), "=d"(b.y)
-               : "l"(A.bnd + (c & 0x7fffffff)), "l"(pol));
-  lo = b.x;
-  up = b.y;
-  q = column_q_inline(lo, up, c < 0, frac_any, cfg);
-#else
-  ld_snap_keep(A.snap + (c & 0x7fffffff), pol, lo, up, q);
-#endif
+  if constexpr (gather16_v<RA>) {
+    double2 b;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                 : "=d"(b.x), "=d"(b.y)
+                 : "l"(A.bnd + (c & 0x7fffffff)), "l"(pol));
+    lo = b.x;
+    up = b.y;
+    q = column_q_inline(lo, up, c < 0, frac_any, cfg);
+  } else {
+    ld_snap_keep(A.snap + (c & 0x7fffffff), pol, lo, up, q);
+  }
 }
 
 // ---- filter words -----------------------------------------------------------------
@@ -190,7 +186,8 @@ struct SellWarpSmem {
 constexpr size_t kSellSmem = sizeof(SellWarpSmem) * kSellWarps;
 
 // exact pipeline over queue entries [0, cnt), one per lane
-__device__ __forceinline__ bool sell_drain(const RoundArgs& A, const SellWarpSmem& W,
+template <class RA>
+__device__ __forceinline__ bool sell_drain(const RA& A, const SellWarpSmem& W,
                                            long long off, int cnt, int lane, uint64_t pol_keep,
                                            const DevCfg& cfg) {
   bool inf_flag = false;
@@ -260,8 +257,8 @@ __device__ __forceinline__ void chunk_done(const RoundArgs& A, const UnitDesc& u
 // unit's lanes, row finish on the owner lanes (row check, filter; chunks of
 // split rows: partial record, last chunk combines), then phase 2 over the
 // slice's filter words.
-template <bool kRowCheck, int LG>
-__device__ __forceinline__ void slice_tail(const RoundArgs& A, SellWarpSmem& W, const SliceDesc& sd,
+template <bool kRowCheck, int LG, class RA>
+__device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const SliceDesc& sd,
                                            const UnitDesc& ud, bool active, int len, int lane,
                                            Act act, double xmax, double lhs_r, double rhs_r,
                                            uint64_t pol_keep, bool& inf_flag, const DevCfg& cfg) {
@@ -350,8 +347,8 @@ __device__ __forceinline__ void slice_tail(const RoundArgs& A, SellWarpSmem& W, 
 
 // One slice by one warp.  LG = log2(lanes per unit); kDense: a full sweep
 // (no worklist), every lane walks every step of the slice.
-template <bool kRowCheck, int LG, bool kDense>
-__device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, const SliceDesc& sd,
+template <bool kRowCheck, int LG, bool kDense, class RA>
+__device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const SliceDesc& sd,
                                            int lane, bool full, const uint8_t* rflag,
                                            uint64_t pol_keep, uint64_t pol_stream, bool& inf_flag,
                                            const DevCfg& cfg) {
@@ -475,8 +472,8 @@ __device__ __forceinline__ void sell_slice(const RoundArgs& A, SellWarpSmem& W, 
 // independent chains, interleaved, so each step has R entries in flight per
 // lane and the per-slice latencies (descriptors, row sides, the ticket)
 // are paid once per R slices.  Full sweeps only.
-template <bool kRowCheck, int R>
-__device__ __forceinline__ void sell_group(const RoundArgs& A, SellWarpSmem& W, int s0, int nr,
+template <bool kRowCheck, int R, class RA>
+__device__ __forceinline__ void sell_group(const RA& A, SellWarpSmem& W, int s0, int nr,
                                            int lane, uint64_t pol_keep, uint64_t pol_stream,
                                            bool& inf_flag, const DevCfg& cfg) {
   long long off[R];
@@ -563,8 +560,8 @@ __device__ __forceinline__ void sell_group(const RoundArgs& A, SellWarpSmem& W, 
 // entries (coalesced), 256 entries per block; the lanes form the
 // contributions, lane 0 adds them in entry order from shared memory (the
 // reference's chain), then row finish and phase 2 with the exact filter.
-template <bool kRowCheck>
-__device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, int par,
+template <bool kRowCheck, class RA>
+__device__ __forceinline__ void sell_wide(const RA& A, SellWarpSmem& W, int par,
                                           uint64_t pol_keep, bool& inf_flag, const DevCfg& cfg) {
   const int lane = threadIdx.x & 31;
   const int nw = ld_gpu(&A.st->nwide[par]);
@@ -710,8 +707,8 @@ __device__ __forceinline__ void sell_wide(const RoundArgs& A, SellWarpSmem& W, i
 // off + 32 i + position), then row finish and an in-lane phase 2 over the
 // unit's filter words.  Exact like the slice path; used when few rows are
 // marked, so the uncoalesced lane streams do not matter.
-template <bool kRowCheck>
-__device__ __forceinline__ void sell_units(const RoundArgs& A, int par, uint64_t pol_keep,
+template <bool kRowCheck, class RA>
+__device__ __forceinline__ void sell_units(const RA& A, int par, uint64_t pol_keep,
                                            bool& inf_flag, const DevCfg& cfg) {
   const int lane = threadIdx.x & 31;
   const int nu = ld_gpu(&A.st->nunit[par]);
@@ -786,8 +783,8 @@ __device__ __forceinline__ void sell_units(const RoundArgs& A, int par, uint64_t
   }
 }
 
-template <bool kRowCheck, bool kDense>
-__device__ __forceinline__ void sell_sweep(const RoundArgs& A, const DevCfg& cfg,
+template <bool kRowCheck, bool kDense, class RA>
+__device__ __forceinline__ void sell_sweep(const RA& A, const DevCfg& cfg,
                                            SellWarpSmem* smem) {
   const int lane = threadIdx.x & 31;
   SellWarpSmem& W = smem[threadIdx.x >> 5];
@@ -856,8 +853,8 @@ __device__ __forceinline__ bool sell_dense_round(const RoundArgs& A) {
   return !round_is_sparse(A.st, A.dirty);
 }
 
-template <bool kRowCheck, bool kDense>
-__global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const RoundArgs A,
+template <bool kRowCheck, bool kDense, bool kB16>
+__global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const RoundArgsG<kB16> A,
                                                                      const DevCfg cfg) {
   extern __shared__ __align__(16) unsigned char sell_dyn[];  // kSellWarps x SellWarpSmem
   SellWarpSmem* smem = reinterpret_cast<SellWarpSmem*>(sell_dyn);

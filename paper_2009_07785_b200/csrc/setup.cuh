@@ -21,6 +21,18 @@ __global__ void k_row_keys(const int32_t* __restrict__ rp, int m, int short_max,
   }
 }
 
+// sum of squared row lengths (< nnz^2 < 2^62): the entry-weighted row
+// density sum(len^2) / (n nnz) picks the gather record (engine.cu)
+__global__ void k_len2_sum(const int32_t* __restrict__ rp, int m, unsigned long long* __restrict__ out) {
+  unsigned long long acc = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
+    const unsigned long long L = (unsigned long long)(rp[i + 1] - rp[i]);
+    acc += L * L;
+  }
+  for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
 // lengths in the new order (the exclusive scan gives the permuted row_ptr)
 __global__ void k_sorted_len(const int32_t* __restrict__ rp, const int32_t* __restrict__ perm,
                              int m, int32_t* __restrict__ slen) {

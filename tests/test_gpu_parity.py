@@ -365,3 +365,42 @@ def test_modes_on_edge_instances(mode):
     ]
     for k, inst in enumerate(cases):
         assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg), (mode, k))
+
+
+_GATHER_SCRIPT = r"""
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+from oracle import oracle as O
+from paper_2009_07785_b200 import generators as G
+from paper_2009_07785_b200.engine import propagate_gpu
+from paper_2009_07785_b200.model import EngineConfig
+PAR = EngineConfig(row_check=False)
+insts = [G.gen_powerlaw(100000, 100000, 20090778, cap=2000),
+         G.gen_longrows(3000, 6000, 3001, long_every=100, long_min=1500, long_max=4000),
+         G.gen_random(20000, 20000, 5, mean_row_nnz=8.0, integral_fraction=0.5)]
+for inst in insts:
+    for wl in (False, True):
+        g = propagate_gpu(inst, EngineConfig(row_check=False, worklist=wl))
+        r = O.propagate_parallel(inst, PAR)
+        assert int(g.status) == int(r.status) and g.rounds_executed == r.rounds_executed, inst.name
+        assert list(g.per_round_changes) == list(r.per_round_changes), inst.name
+        assert np.array_equal(O.canon(g.bounds.lower), O.canon(r.bounds.lower)), inst.name
+        assert np.array_equal(O.canon(g.bounds.upper), O.canon(r.bounds.upper)), inst.name
+print("ok")
+"""
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("gather", ["16", "32"])
+def test_gather_record_modes(gather):
+    """both gather records (16 B bounds + recomputed q, 32 B snapshot) forced
+    on instances of either kind: bit-exact with the oracle"""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PG_SELL_GATHER=gather)
+    p = subprocess.run([sys.executable, "-c", _GATHER_SCRIPT.format(root=root)], env=env,
+                       capture_output=True, text=True, timeout=600)
+    assert p.returncode == 0 and "ok" in p.stdout, p.stdout + p.stderr
