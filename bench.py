@@ -398,11 +398,12 @@ def bench_rowshard(args, inst, world, rank, local):
     """C5: one 50M-entry set-partitioning instance, row-sharded over the
     GPUs; one NCCL max all-reduce merges the bound keys every round."""
     torch, dist = _gpu_setup(local, world)
-    from paper_2009_07785_b200.model import EngineConfig
+    from paper_2009_07785_b200.model import EngineConfig, LoopMode
     from paper_2009_07785_b200.multi import RowShardedSession
 
     delta = bool(args.delta if args.delta is not None else world > 1)
-    cfg = EngineConfig(device=local, worklist=args.worklist, delta_exchange=delta)
+    cfg = EngineConfig(device=local, worklist=args.worklist, delta_exchange=delta,
+                       loop_mode=LoopMode.Host if args.loop == "host" else LoopMode.Graph)
     rs = RowShardedSession(inst, cfg, rank, world)
     for _ in range(args.warmup):
         r = rs.run()
@@ -422,9 +423,10 @@ def bench_rowshard(args, inst, world, rank, local):
     R = r.rounds_executed
     line = _common_line(args, world, ms, "strong", "c5", {
         "instance": inst.name, "m": m, "n": n, "nnz": nnz,
-        "parallelism": f"row-sharded x{world} (NCCL max all-reduce of bound keys"
-                       + (", sparse delta all-gather when every rank changed <= n/16 columns)"
-                          if delta else ")"),
+        "parallelism": (f"row-sharded x{world} (NCCL max all-reduce of bound keys"
+                        + (", sparse delta all-gather when every rank changed <= n/16 columns)"
+                           if delta else ")")) if world > 1
+                       else "single-gpu (one row shard: no exchange)",
         "worklist": args.worklist, "delta_exchange": delta})
     line["delta_rounds"] = rs.session.info()["delta_rounds"]
     line.update({"rounds": R, "status": r.status.name, "rounds_per_s": round(R / (ms / 1e3), 1),

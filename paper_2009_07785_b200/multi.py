@@ -75,11 +75,16 @@ class RowShardedSession:
     """This rank's row shard of one instance, merged over NCCL every round."""
 
     def __init__(self, inst: ProblemInstance, cfg: EngineConfig, rank: int, world: int,
-                 group=None, uid: bytes | None = None):
+                 group=None, uid: bytes | None = None, force_comm: bool = False):
+        """world == 1 is the plain single-GPU engine (nothing to exchange)
+        unless force_comm attaches a one-rank communicator (tests)."""
         self.rank, self.world = rank, world
         self.r0, self.r1 = row_shards(inst.matrix.row_ptr, world)[rank]
         self.shard = shard_instance(inst, self.r0, self.r1)
         self.session = Session(self.shard, cfg)
+        self.comm = world > 1 or force_comm
+        if not self.comm:
+            return
         if uid is None:
             if world > 1:
                 import torch.distributed as dist

@@ -46,7 +46,7 @@ def test_c4_nodes_match_oracle():
     inst = G.gen_random(20000, 20000, 4, mean_row_nnz=8.0, integral_fraction=0.5)
     root = O.propagate_parallel(inst, PAR)
     lo, up = G.gen_nodes(inst, root.bounds.lower, root.bounds.upper, K=16)
-    k0, k1, blo, bup, st, rd = propagate_nodes_sharded(inst, PAR, lo, up, rank=0, world=1)
+    k0, k1, blo, bup, st, rd = propagate_nodes_sharded(inst, PAR, lo, up, rank=0, world=1, force_comm=True)
     assert (k0, k1) == (0, 16)
     for k in range(16):
         ref = O.propagate_parallel(inst, PAR, lo[k], up[k])
@@ -68,13 +68,13 @@ def test_row_sharded_nccl_world1(loop, worklist):
     for inst in (G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003),
                  G.gen_random(4000, 4000, 9, mean_row_nnz=10.0, integral_fraction=0.5)):
         cfg = EngineConfig(row_check=False, loop_mode=loop, worklist=worklist)
-        rs = RowShardedSession(inst, cfg, rank=0, world=1)
+        rs = RowShardedSession(inst, cfg, rank=0, world=1, force_comm=True)
         try:
             assert_bit_exact(rs.propagate(), O.propagate_parallel(inst, PAR), inst.name)
         finally:
             rs.close()
     bad = G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003, infeasible=True)
-    rs = RowShardedSession(bad, EngineConfig(), rank=0, world=1)
+    rs = RowShardedSession(bad, EngineConfig(), rank=0, world=1, force_comm=True)
     assert rs.propagate().status == PropagationStatus.Infeasible
     rs.close()
 
@@ -92,7 +92,7 @@ def test_row_sharded_delta_exchange_world1(worklist):
     for inst in (G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003),
                  G.gen_random(4000, 4000, 9, mean_row_nnz=10.0, integral_fraction=0.5)):
         cfg = EngineConfig(row_check=False, worklist=worklist, delta_exchange=True)
-        rs = RowShardedSession(inst, cfg, rank=0, world=1)
+        rs = RowShardedSession(inst, cfg, rank=0, world=1, force_comm=True)
         try:
             r = rs.propagate()
             assert_bit_exact(r, O.propagate_parallel(inst, PAR), inst.name)
@@ -101,7 +101,7 @@ def test_row_sharded_delta_exchange_world1(worklist):
         finally:
             rs.close()
     bad = G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003, infeasible=True)
-    rs = RowShardedSession(bad, EngineConfig(delta_exchange=True), rank=0, world=1)
+    rs = RowShardedSession(bad, EngineConfig(delta_exchange=True), rank=0, world=1, force_comm=True)
     assert rs.propagate().status == PropagationStatus.Infeasible
     rs.close()
 
