@@ -46,7 +46,7 @@ def test_c4_nodes_match_oracle():
     inst = G.gen_random(20000, 20000, 4, mean_row_nnz=8.0, integral_fraction=0.5)
     root = O.propagate_parallel(inst, PAR)
     lo, up = G.gen_nodes(inst, root.bounds.lower, root.bounds.upper, K=16)
-    k0, k1, blo, bup, st, rd = propagate_nodes_sharded(inst, PAR, lo, up, rank=0, world=1, force_comm=True)
+    k0, k1, blo, bup, st, rd = propagate_nodes_sharded(inst, PAR, lo, up, rank=0, world=1)
     assert (k0, k1) == (0, 16)
     for k in range(16):
         ref = O.propagate_parallel(inst, PAR, lo[k], up[k])
