@@ -487,21 +487,25 @@ struct pg_session {
   // used by the worklist marks and the batched branch-and-bound nodes
   void ensure_col_index() {
     if (d_col_ptr) return;
-    cudaStream_t st = stream;
-    t_alloc_stream = st;
+    t_alloc_stream = stream;
+    build_col_index(d_row_ptr, d_colx, nullptr, stream);
+  }
+  // rp/cols: a CSR whose row r is session row rowmap[r] (nullptr: r itself)
+  void build_col_index(const int32_t* rp, const int32_t* cols, const int32_t* rowmap,
+                       cudaStream_t st) {
     d_col_ptr = dalloc<int32_t>((size_t)n + 1);
     d_col_item = dalloc<int32_t>(nnz);
     int32_t* cnt = dalloc<int32_t>((size_t)n + 1);
     PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)n + 1), st));
-    if (nnz) k_csc_count<<<grid_for(nnz, 256, 16), 256, 0, st>>>(d_colx, nnz, cnt);
+    if (nnz) k_csc_count<<<grid_for(nnz, 256, 16), 256, 0, st>>>(cols, nnz, cnt);
     size_t tmp_bytes = 0;
     PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, d_col_ptr, n + 1, st));
     void* tmp = dalloc<unsigned char>(tmp_bytes);
     PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, d_col_ptr, n + 1, st));
     PG_CUDA(cudaMemcpyAsync(cnt, d_col_ptr, sizeof(int32_t) * ((size_t)n + 1),
                             cudaMemcpyDeviceToDevice, st));
-    if (m) k_csc_fill<<<grid_for(nnz * 32 / kWalkChunk + 1, 256, 16), 256, 0, st>>>(d_row_ptr, d_colx, m, cnt,
-                                                                         d_col_item);
+    if (m) k_csc_fill<<<grid_for(nnz * 32 / kWalkChunk + 1, 256, 16), 256, 0, st>>>(rp, cols, m, cnt,
+                                                                                   rowmap, d_col_item);
     PG_CUDA(cudaGetLastError());
     dfree(tmp);
     dfree(cnt);
@@ -799,7 +803,13 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     auto h2d = [&](void* dst, const void* src, size_t bytes, cudaStream_t q) {
       if (bytes) PG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, q));
     };
+    // row_ptr first: the ordering on stream 2 starts at once instead of
+    // queueing behind the matrix on the copy engine
+    h2d(t_rp, p->row_ptr, sizeof(int32_t) * ((size_t)m + 1), s2);
     h2d(t_cols, p->col_idx, sizeof(int32_t) * nnz, st);
+    cudaEvent_t ev_cols = nullptr;
+    PG_CUDA(cudaEventCreateWithFlags(&ev_cols, cudaEventDisableTiming));
+    PG_CUDA(cudaEventRecord(ev_cols, st));
     h2d(t_vals, p->values, sizeof(double) * nnz, st);
     h2d(t_lhs, p->lhs, sizeof(double) * m, st);
     h2d(t_rhs, p->rhs, sizeof(double) * m, st);
@@ -809,16 +819,16 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     // grouped by exact length (stable radix sort), then the rows split into
     // segments in input order.  Row order is not observable -- candidates
     // merge by exact max/min and each row is summed on its own.
-    h2d(t_rp, p->row_ptr, sizeof(int32_t) * ((size_t)m + 1), s2);
     void* tmp = nullptr;
     size_t tmp_bytes = 0;
     auto cub_tmp = [&](size_t need) {
       if (need > tmp_bytes) {
+        cudaStream_t prev = t_alloc_stream;
         t_alloc_stream = s2;
         dfree(tmp);
         tmp = dalloc<unsigned char>(need);
         tmp_bytes = need;
-        t_alloc_stream = st;
+        t_alloc_stream = prev;
       }
     };
     std::vector<int32_t> cls(kMaxClasses + 4, 0);
@@ -855,11 +865,12 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       s->short_rows = row;
       s->nsrow = m - row;
     }
+    // the ordering's buffers come from stream 2's allocation order, so it
+    // never waits behind the upload on stream 1
+    t_alloc_stream = s2;
     s->d_srow = dalloc<int32_t>(s->nsrow);
     s->d_sfirst = dalloc<int32_t>((size_t)s->nsrow + 1);
     int32_t* scnt = dalloc<int32_t>((size_t)s->nsrow + 1);
-    PG_CUDA(cudaEventRecord(s->ev_join, st));
-    PG_CUDA(cudaStreamWaitEvent(s2, s->ev_join, 0));  // allocations above happen on stream 1
     int32_t h_nseg = 0;
     if (s->nsrow) {
       k_seg_counts<<<s->grid_for((int64_t)s->nsrow + 1, 256), 256, 0, s2>>>(
@@ -880,8 +891,6 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     uint32_t* skey2 = dalloc<uint32_t>(s->nseg);
     int32_t* sidx = dalloc<int32_t>(s->nseg);
     int32_t* sorder = dalloc<int32_t>(s->nseg);
-    PG_CUDA(cudaEventRecord(s->ev_join, st));
-    PG_CUDA(cudaStreamWaitEvent(s2, s->ev_join, 0));
     if (s->nseg) {
       k_emit_segs<<<s->grid_for((int64_t)s->nsrow * 32, 256, 16), 256, 0, s2>>>(
           s->d_row_ptr, s->d_sfirst, (int)s->short_rows, s->nsrow, chunk, segs_in, skey, sidx);
@@ -896,6 +905,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       k_order_segs<<<s->grid_for(s->nseg, 256), 256, 0, s2>>>(segs_in, sorder, s->nseg, s->d_segs);
     }
     PG_CUDA(cudaGetLastError());
+    t_alloc_stream = st;
     tm.lap("ordering + tables (dev)");
 
     s->d_colx = dalloc<int32_t>(nnz + 4);  // +16 B: bulk copies round up to 16 B
@@ -930,71 +940,61 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     PG_CUDA(cudaMemsetAsync(s->d_ctl, 0, sizeof(NodeCtl), st));  // cold starts
     PG_CUDA(cudaMemsetAsync(s->d_st, 0, sizeof(DevState), st));
     PG_CUDA(cudaMemsetAsync(s->d_row_done, 0, sizeof(int32_t) * std::max<int32_t>(1, s->nsrow), st));
+    t_alloc_stream = s2;
     s->d_split = dalloc<int32_t>(std::max<int32_t>(1, s->nsrow) + 1);
     if (s->nsrow) {
       int32_t* cnt = s->d_split + s->nsrow;  // the count rides at the end
-      PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), st));
-      PG_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
-      k_split_list<<<s->grid_for(s->nsrow, 256), 256, 0, st>>>(s->d_sfirst, s->nsrow, s->d_split, cnt);
-      PG_CUDA(cudaMemcpyAsync(&s->nsplit, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      PG_CUDA(cudaStreamSynchronize(st));
+      PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), s2));
+      k_split_list<<<s->grid_for(s->nsrow, 256), 256, 0, s2>>>(s->d_sfirst, s->nsrow, s->d_split, cnt);
+      PG_CUDA(cudaMemcpyAsync(&s->nsplit, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost, s2));
+      PG_CUDA(cudaStreamSynchronize(s2));
     }
+    t_alloc_stream = st;
     PG_CUDA(cudaMemsetAsync(s->d_colx, 0, sizeof(int32_t) * (nnz + 4), st));
     PG_CUDA(cudaMemsetAsync(s->d_vals, 0, sizeof(double) * (nnz + 2), st));
-    // the ordering (stream 2) must be complete before the permutation
-    PG_CUDA(cudaEventRecord(s->ev_join, s2));
-    PG_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
-    if (m) {
-      k_permute_rows<<<s->grid_for(std::max<int64_t>(m, nnz * 32 / kWalkChunk + 1), 256, 16), 256, 0, st>>>(
-          t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, s->d_integral, s->d_colx,
-          s->d_vals, s->d_lhs, s->d_rhs, m, cfg->infinity_threshold);
-      PG_CUDA(cudaGetLastError());
-    }
-    if (cfg->scalar_mode == PG_NARROW32) {
-      // the float working copy (engine_common.hpp:24-38) and chunk scratch
-      k_to_f32<<<s->grid_for(nnz, 256), 256, 0, st>>>(s->d_vals, nnz);
-      k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_lhs, m);
-      k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_rhs, m);
-      const int chunk = cfg->nnz_budget;
-      s->f32_maxc = s->max_len() > chunk ? (s->max_len() + chunk - 1) / chunk : 1;
-      s->d_f32_part = dalloc<ActF>((size_t)s->grid_for(m, 256, 4) * 256 * s->f32_maxc);
-      PG_CUDA(cudaGetLastError());
-    }
+    // sliced-ELL tables (units, regions, slice descriptors) depend on the
+    // ordering only: built on stream 2 while the upload is still running
+    UnitDesc* u_in = nullptr;
+    int32_t *k0_in = nullptr, *uk0 = nullptr, *uidx = nullptr, *uord = nullptr, *rcnt = nullptr;
+    uint32_t *ukey = nullptr, *ukey2 = nullptr;
+    long long *elems = nullptr, *soff = nullptr, total = 0;
+    void *stmp = nullptr, *stmp2 = nullptr;
+    t_alloc_stream = s2;
     // sliced-ELL copy (sell.cuh): units sorted by length, slices per
     // lanes-per-unit region, transposed fill
     s->nunits = s->nseg + (int32_t)s->short_rows;
     if (s->nunits) {
       const int32_t nu = s->nunits;
-      UnitDesc* u_in = dalloc<UnitDesc>(nu);
-      int32_t* k0_in = dalloc<int32_t>(nu);
-      int32_t* uk0 = dalloc<int32_t>(nu);
-      uint32_t* ukey = dalloc<uint32_t>(nu);
-      uint32_t* ukey2 = dalloc<uint32_t>(nu);
-      int32_t* uidx = dalloc<int32_t>(nu);
-      int32_t* uord = dalloc<int32_t>(nu);
-      int32_t* rcnt = dalloc<int32_t>(5);
+      u_in = dalloc<UnitDesc>(nu);
+      k0_in = dalloc<int32_t>(nu);
+      uk0 = dalloc<int32_t>(nu);
+      ukey = dalloc<uint32_t>(nu);
+      ukey2 = dalloc<uint32_t>(nu);
+      uidx = dalloc<int32_t>(nu);
+      uord = dalloc<int32_t>(nu);
+      rcnt = dalloc<int32_t>(5);
       s->d_units = dalloc<UnitDesc>(nu);
-      PG_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(int32_t) * 5, st));
-      k_make_units<<<s->grid_for(nu, 256), 256, 0, st>>>(s->d_segs, s->nseg, s->d_srow, s->d_sfirst,
+      PG_CUDA(cudaMemsetAsync(rcnt, 0, sizeof(int32_t) * 5, s2));
+      k_make_units<<<s->grid_for(nu, 256), 256, 0, s2>>>(s->d_segs, s->nseg, s->d_srow, s->d_sfirst,
                                                            lay, s->d_row_ptr, nu, chunk, u_in, k0_in,
                                                            ukey, uidx);
       int bits = 1;
       while (bits < 32 && (1u << bits) <= (uint32_t)chunk) ++bits;
       size_t need = 0;
-      PG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, ukey, ukey2, uidx, uord, nu, 0, bits, st));
-      void* stmp = dalloc<unsigned char>(need);
-      PG_CUDA(cub::DeviceRadixSort::SortPairs(stmp, need, ukey, ukey2, uidx, uord, nu, 0, bits, st));
-      k_order_units<<<s->grid_for(nu, 256), 256, 0, st>>>(u_in, k0_in, uord, nu, s->d_units, uk0);
+      PG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, ukey, ukey2, uidx, uord, nu, 0, bits, s2));
+      stmp = dalloc<unsigned char>(need);
+      PG_CUDA(cub::DeviceRadixSort::SortPairs(stmp, need, ukey, ukey2, uidx, uord, nu, 0, bits, s2));
+      k_order_units<<<s->grid_for(nu, 256), 256, 0, s2>>>(u_in, k0_in, uord, nu, s->d_units, uk0);
       // lanes per unit at least 2^lg_min: a small instance spreads its chains
       // so that about one slice per resident warp remains
       const int64_t resident = (int64_t)s->num_sms * s->sell_per_sm * kSellWarps;
       int lg_min = 0;
       while (lg_min < 3 && ((int64_t)nu << lg_min) < resident * 32) ++lg_min;
       s->lg_min = lg_min;
-      k_unit_regions<<<s->grid_for(nu, 256), 256, 0, st>>>(s->d_units, nu, lg_min, rcnt);
+      k_unit_regions<<<s->grid_for(nu, 256), 256, 0, s2>>>(s->d_units, nu, lg_min, rcnt);
       int32_t hc[5] = {0, 0, 0, 0, 0};
-      PG_CUDA(cudaMemcpyAsync(hc, rcnt, sizeof(hc), cudaMemcpyDeviceToHost, st));
-      PG_CUDA(cudaStreamSynchronize(st));
+      PG_CUDA(cudaMemcpyAsync(hc, rcnt, sizeof(hc), cudaMemcpyDeviceToHost, s2));
+      PG_CUDA(cudaStreamSynchronize(s2));
       SellRegions R{};
       R.ustart[0] = 0;
       R.ustart[1] = hc[3];
@@ -1017,17 +1017,51 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         s->group_start = std::min(s->nslices, R.sstart[3] + (ub - R.ustart[3] + 31) / 32);
       }
       s->d_slices = dalloc<SliceDesc>(s->nslices);
-      long long* elems = dalloc<long long>((size_t)s->nslices + 1);
-      long long* soff = dalloc<long long>((size_t)s->nslices + 1);
-      k_slice_desc<<<s->grid_for((int64_t)s->nslices + 1, 256), 256, 0, st>>>(s->d_units, R,
+      elems = dalloc<long long>((size_t)s->nslices + 1);
+      soff = dalloc<long long>((size_t)s->nslices + 1);
+      k_slice_desc<<<s->grid_for((int64_t)s->nslices + 1, 256), 256, 0, s2>>>(s->d_units, R,
                                                                               s->d_slices, elems);
       need = 0;
-      PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, elems, soff, s->nslices + 1, st));
-      void* stmp2 = dalloc<unsigned char>(need);
-      PG_CUDA(cub::DeviceScan::ExclusiveSum(stmp2, need, elems, soff, s->nslices + 1, st));
-      long long total = 0;
-      PG_CUDA(cudaMemcpyAsync(&total, soff + s->nslices, sizeof(long long), cudaMemcpyDeviceToHost, st));
-      PG_CUDA(cudaStreamSynchronize(st));
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, elems, soff, s->nslices + 1, s2));
+      stmp2 = dalloc<unsigned char>(need);
+      PG_CUDA(cub::DeviceScan::ExclusiveSum(stmp2, need, elems, soff, s->nslices + 1, s2));
+      total = 0;
+      PG_CUDA(cudaMemcpyAsync(&total, soff + s->nslices, sizeof(long long), cudaMemcpyDeviceToHost, s2));
+      PG_CUDA(cudaStreamSynchronize(s2));
+    }
+    t_alloc_stream = st;
+    // worklist: the column index from the caller's row order (rows renamed
+    // through the inverse permutation) on stream 2 as soon as the column
+    // indices have arrived, while the values are still uploading
+    if ((cfg->flags & PG_FLAG_WORKLIST) && m) {
+      t_alloc_stream = s2;
+      int32_t* inv = dalloc<int32_t>(m);
+      k_invert_perm<<<s->grid_for(m, 256), 256, 0, s2>>>(t_perm, m, inv);
+      PG_CUDA(cudaStreamWaitEvent(s2, ev_cols, 0));
+      s->build_col_index(t_rp, t_cols, inv, s2);
+      dfree(inv);
+      t_alloc_stream = st;
+    }
+    // the ordering (stream 2) must be complete before the permutation
+    PG_CUDA(cudaEventRecord(s->ev_join, s2));
+    PG_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+    if (m) {
+      k_permute_rows<<<s->grid_for(std::max<int64_t>(m, nnz * 32 / kWalkChunk + 1), 256, 16), 256, 0, st>>>(
+          t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, s->d_integral, s->d_colx,
+          s->d_vals, s->d_lhs, s->d_rhs, m, cfg->infinity_threshold);
+      PG_CUDA(cudaGetLastError());
+    }
+    if (cfg->scalar_mode == PG_NARROW32) {
+      // the float working copy (engine_common.hpp:24-38) and chunk scratch
+      k_to_f32<<<s->grid_for(nnz, 256), 256, 0, st>>>(s->d_vals, nnz);
+      k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_lhs, m);
+      k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_rhs, m);
+      const int chunk = cfg->nnz_budget;
+      s->f32_maxc = s->max_len() > chunk ? (s->max_len() + chunk - 1) / chunk : 1;
+      s->d_f32_part = dalloc<ActF>((size_t)s->grid_for(m, 256, 4) * 256 * s->f32_maxc);
+      PG_CUDA(cudaGetLastError());
+    }
+    if (s->nunits) {
       s->sell_elems = total;
       s->d_sv = dalloc<double>((size_t)total + 1);
       s->d_sc = dalloc<int32_t>((size_t)total + 1);
@@ -1113,6 +1147,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         PG_CUDA(cudaStreamSetAttribute(s->stream, cudaStreamAttributeAccessPolicyWindow, &av));
       }
     }
+    cudaEventDestroy(ev_cols);
     if (cfg->loop_mode == PG_LOOP_GRAPH) s->build_graph();
     tm.lap("graph instantiate");
     return s;

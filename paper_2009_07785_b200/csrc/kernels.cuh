@@ -923,12 +923,20 @@ __global__ void k_csc_count(const int32_t* __restrict__ colx, int64_t nnz,
     atomicAdd(&cnt[colx[k] & 0x7fffffff], 1);
 }
 
-// rows into their columns' ranges (entry-balanced walk)
+// rows into their columns' ranges (entry-balanced walk); row r is named
+// rowmap[r] when given (a CSR in the caller's row order)
 __global__ void k_csc_fill(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ colx,
-                           int m, int32_t* __restrict__ cursor, int32_t* __restrict__ col_row) {
+                           int m, int32_t* __restrict__ cursor, const int32_t* __restrict__ rowmap,
+                           int32_t* __restrict__ col_row) {
   walk_entries(row_ptr, m, row_ptr[m], [&](bool valid, int64_t k, int r) {
-    if (valid) col_row[atomicAdd(&cursor[colx[k] & 0x7fffffff], 1)] = r;
+    if (valid) col_row[atomicAdd(&cursor[colx[k] & 0x7fffffff], 1)] = rowmap ? rowmap[r] : r;
   });
+}
+
+// inv[perm[i]] = i
+__global__ void k_invert_perm(const int32_t* __restrict__ perm, int m, int32_t* __restrict__ inv) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x)
+    inv[perm[i]] = i;
 }
 
 }  // namespace pgb
