@@ -207,6 +207,7 @@ struct pg_session {
   DevCfg dcfg{};
   int num_sms = 148;
   int sell_per_sm = 1;   // resident k_sell CTAs per SM
+  int sell_dense_per_sm = 1;  // the same for the full sweep (less shared memory)
   int cand_per_sm = 1;   // resident k_cand CTAs per SM
   int loop_grid = 0;     // co-resident CTAs of the persistent loop kernel
   int nodes_per_sm = 1;  // resident k_nodes CTAs per SM
@@ -371,10 +372,11 @@ struct pg_session {
   // the worklist sweep (each returns at once when the round is of the other kind)
   template <bool kB16>
   void launch_sell(const RoundArgsG<kB16>& G, int grid, bool rowcheck) {
+    const int dgrid = std::max(1, std::min((nslices + 7) / 8, num_sms * sell_dense_per_sm));
     if (rowcheck)
-      k_sell<true, true, kB16><<<grid, kSellThreads, kSellSmem, stream>>>(G, dcfg);
+      k_sell<true, true, kB16><<<dgrid, kSellThreads, kSellSmemDense, stream>>>(G, dcfg);
     else
-      k_sell<false, true, kB16><<<grid, kSellThreads, kSellSmem, stream>>>(G, dcfg);
+      k_sell<false, true, kB16><<<dgrid, kSellThreads, kSellSmemDense, stream>>>(G, dcfg);
     if (dirty.enabled) {
       if (rowcheck)
         k_sell<true, false, kB16><<<grid, kSellThreads, kSellSmem, stream>>>(G, dcfg);
@@ -717,7 +719,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       // kernel attributes and occupancies, once per device (they cost ~0.7 ms)
       struct Occ {
         bool ok = false;
-        int sell = 1, cand = 1, loop_grid = 0, nodes = 1;
+        int sell = 1, sell_dense = 1, cand = 1, loop_grid = 0, nodes = 1;
       };
       static Occ occ[64];
       static std::mutex mu;
@@ -733,12 +735,17 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         for (const void* f : {(const void*)k_loop<true>, (const void*)k_loop<false>})
           PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(LoopSmem)));
-        int o16 = 0;
-        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.sell, k_sell<true, true, false>,
+        int o16 = 0, d32 = 0, d16 = 0;
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.sell, k_sell<true, false, false>,
                                                               kSellThreads, kSellSmem));
-        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o16, k_sell<true, true, true>,
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o16, k_sell<true, false, true>,
                                                               kSellThreads, kSellSmem));
         o.sell = std::min(o.sell, o16);
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d32, k_sell<true, true, false>,
+                                                              kSellThreads, kSellSmemDense));
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d16, k_sell<true, true, true>,
+                                                              kSellThreads, kSellSmemDense));
+        o.sell_dense = std::min(d32, d16);
         PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.cand, k_cand, kCandThreads, 0));
         int per = 0, per2 = 0;
         PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_loop<true>, kSellThreads,
@@ -751,6 +758,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         o.ok = true;
       }
       s->sell_per_sm = std::max(1, o.sell);
+      s->sell_dense_per_sm = std::max(1, o.sell_dense);
       s->cand_per_sm = std::max(1, o.cand);
       s->loop_grid = o.loop_grid;
       s->nodes_per_sm = std::max(1, o.nodes);

@@ -64,6 +64,9 @@ namespace pgb {
 #ifndef PG_SELL_LGMAX
 #define PG_SELL_LGMAX 3
 #endif
+#ifndef PG_SELL_MINB_DENSE
+#define PG_SELL_MINB_DENSE 2  // resident CTAs per SM the full sweep is compiled for
+#endif
 #ifndef PG_SELL_MINB
 #define PG_SELL_MINB 2
 #endif
@@ -184,6 +187,11 @@ struct SellWarpSmem {
 };
 
 constexpr size_t kSellSmem = sizeof(SellWarpSmem) * kSellWarps;
+// full sweeps never touch the wide-unit buffers: their warps' records are
+// packed at this stride (the dynamic shared memory of the dense kernel)
+constexpr size_t kSellDenseStride = __builtin_offsetof(SellWarpSmem, wbuf);
+constexpr size_t kSellSmemDense = kSellDenseStride * kSellWarps;
+static_assert(kSellDenseStride % 16 == 0, "warp records stay 16 B aligned");
 
 // exact pipeline over queue entries [0, cnt), one per lane
 template <class RA>
@@ -787,7 +795,9 @@ template <bool kRowCheck, bool kDense, class RA>
 __device__ __forceinline__ void sell_sweep(const RA& A, const DevCfg& cfg,
                                            SellWarpSmem* smem) {
   const int lane = threadIdx.x & 31;
-  SellWarpSmem& W = smem[threadIdx.x >> 5];
+  SellWarpSmem& W = *reinterpret_cast<SellWarpSmem*>(
+      reinterpret_cast<unsigned char*>(smem) +
+      (size_t)(threadIdx.x >> 5) * (kDense ? kSellDenseStride : sizeof(SellWarpSmem)));
   const bool full = kDense;
   const int par = (ld_gpu(&A.st->round) + 1) & 1;
   const uint8_t* rflag = A.dirty.row_flag + (size_t)par * A.dirty.ms;
@@ -854,7 +864,8 @@ __device__ __forceinline__ bool sell_dense_round(const RoundArgs& A) {
 }
 
 template <bool kRowCheck, bool kDense, bool kB16>
-__global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB) k_sell(const RoundArgsG<kB16> A,
+__global__ void __launch_bounds__(kSellThreads, kDense ? PG_SELL_MINB_DENSE : PG_SELL_MINB)
+    k_sell(const RoundArgsG<kB16> A,
                                                                      const DevCfg cfg) {
   extern __shared__ __align__(16) unsigned char sell_dyn[];  // kSellWarps x SellWarpSmem
   SellWarpSmem* smem = reinterpret_cast<SellWarpSmem*>(sell_dyn);
