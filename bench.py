@@ -245,15 +245,7 @@ def bench_single(args, inst, world, rank, local):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")
     for _ in range(args.warmup):
         r = sess.run()
-    # k_sell + k_cand + k_commit (+ k_mark with the worklist)
-    # our kernels per round: k_sell (full sweep) + k_cand + k_commit, k_split_finish
-    # with split rows, and with the worklist the worklist k_sell + k_commit_list
-    # + k_mark; k_reset (+ k_mark_vars) per solve.  The persistent loop is one
-    # kernel per solve (+ k_reset).
-    launches_per_round = ((2 if info["slices"] else 0) + 1 + (1 if info["split_rows"] else 0) +
-                          (3 if args.worklist else 0))
-    if info["persistent"]:
-        launches_per_round = 0
+    launches_per_round, per_solve = solve_launches(info, args.worklist)
 
     def barrier():
         torch.cuda.synchronize()
@@ -275,7 +267,6 @@ def bench_single(args, inst, world, rank, local):
         wall_ms = (time.perf_counter() - t0) * 1e3
     ms = _max_over_ranks(torch, dist, world, local, float(np.sum(step_ms))) / args.steps
     R = rounds[-1]
-    per_solve = (1 + (1 if args.worklist else 0)) + (1 if info["persistent"] else 0)
     gpu_launches = sum(per_solve + rr * launches_per_round for rr in rounds)
 
     # dominant kernels alone (roofline), first-round snapshot
@@ -394,6 +385,20 @@ def bench_nodes(args, inst, world, rank, local):
     return line
 
 
+def solve_launches(info, worklist):
+    """Our kernels per round and per solve (engine.cu enqueue_round /
+    enqueue_reset): k_sell (full sweep) + k_cand + k_commit, k_split_finish
+    with split rows, and with the worklist the worklist k_sell +
+    k_commit_list + k_mark; per solve k_reset (+ k_mark_vars).  The
+    persistent loop is one kernel per solve (+ k_reset)."""
+    per_round = ((2 if info["slices"] else 0) + 1 + (1 if info["split_rows"] else 0) +
+                 (3 if worklist else 0))
+    if info["persistent"]:
+        per_round = 0
+    per_solve = 1 + (1 if worklist else 0) + (1 if info["persistent"] else 0)
+    return per_round, per_solve
+
+
 def bench_rowshard(args, inst, world, rank, local):
     """C5: one 50M-entry set-partitioning instance, row-sharded over the
     GPUs; one NCCL max all-reduce merges the bound keys every round."""
@@ -412,9 +417,16 @@ def bench_rowshard(args, inst, world, rank, local):
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        gpu_launches = 0
+        info = rs.session.info()
+        per_round, per_solve = solve_launches(info, args.worklist)
         for _ in range(args.steps):
             r = rs.run()
             times.append(r.elapsed_ns / 1e6)
+            # row shards: no k_commit_list; k_flag_to_slot, or the delta pair
+            pr = (per_round - (1 if args.worklist else 0) + (2 if delta else 1)) if rs.comm \
+                else per_round
+            gpu_launches += per_solve + r.rounds_executed * pr
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -431,7 +443,7 @@ def bench_rowshard(args, inst, world, rank, local):
     line["delta_rounds"] = rs.session.info()["delta_rounds"]
     line.update({"rounds": R, "status": r.status.name, "rounds_per_s": round(R / (ms / 1e3), 1),
                  "gbs_per_round": round(b_round(m, n, nnz) * R / (ms / 1e3) / 1e9, 1),
-                 "clocks": clk.summary(), "gpu_launches": None,
+                 "clocks": clk.summary(), "gpu_launches": gpu_launches,
                  "e2e": {"value": round(ms, 4), "unit": "ms", "h2d_bytes_per_step": 0,
                          "d2h_bytes_per_step": 8 * R}})
     if rank == 0 and not args.no_cpu_baseline:
