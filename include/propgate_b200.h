@@ -225,6 +225,17 @@ int pg_nccl_unique_id(uint8_t* out128);
 int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank,
                            int32_t world);
 
+/* Single-process multi-GPU: one host thread per device
+ * cfg->device .. cfg->device + ngpus - 1, each a row-shard session
+ * (nnz-balanced contiguous rows, all columns) attached to one NCCL
+ * communicator, solved together; same results and statuses as
+ * pg_propagate (constraints_processed counts all rows).  mode:
+ * PG_MULTI_ROWS (the only mode: a single instance shards by rows; node
+ * batches use pg_session_propagate_nodes per process). */
+#define PG_MULTI_ROWS 0
+int pg_multi_propagate(const pg_problem* prob, const pg_config* cfg, int32_t ngpus,
+                       int32_t mode, pg_result* res);
+
 /* Session statistics, in this order: m, n, nnz, slices (sliced-ELL, 32
  * chains each), split-candidate rows (> 16 entries), segments (chains of
  * those rows), short rows, short-row entries, segment entries, chains,

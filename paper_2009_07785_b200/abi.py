@@ -19,6 +19,7 @@ GEN_PATH = os.path.join(PKG_DIR, "libpgen.so")
 
 PG_OK, PG_EINVAL, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_ENODEV, PG_ERANGE = 0, -1, -2, -3, -4, -5, -6
 PG_CONVERGED, PG_ROUNDLIMIT, PG_INFEASIBLE = 0, 1, 2
+PG_MULTI_ROWS = 0
 PG_WIDE64, PG_NARROW32 = 0, 1
 PG_LOOP_GRAPH, PG_LOOP_HOST = 0, 1
 PG_FLAG_ROWCHECK, PG_FLAG_WORKLIST, PG_FLAG_DELTA_EXCHANGE = 0x1, 0x2, 0x4
@@ -123,6 +124,8 @@ PROTOTYPES = {
                                              _dp, _dp, _lp]),
     "pg_nccl_unique_id": (C.c_int, [C.POINTER(C.c_uint8)]),
     "pg_session_attach_comm": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint8), C.c_int32, C.c_int32]),
+    "pg_multi_propagate": (C.c_int, [C.POINTER(PgProblem), C.POINTER(PgConfig), C.c_int32, C.c_int32,
+                                     C.POINTER(PgResult)]),
     "pg_csr_from_triplets": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, _ip, _ip, _dp, C.c_int32,
                                        _ip, _ip, _dp, _lp]),
     "pg_last_error": (C.c_char_p, []),

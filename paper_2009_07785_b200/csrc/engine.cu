@@ -1855,6 +1855,111 @@ int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank, i
   });
 }
 
+int pg_multi_propagate(const pg_problem* p, const pg_config* cfg, int32_t ngpus, int32_t mode,
+                       pg_result* res) {
+  // one host thread per GPU, each a row-shard session (nnz-balanced
+  // contiguous rows, all columns) on its device, one NCCL communicator;
+  // rank 0's result is returned (every rank holds the same bounds)
+  if (!p || !cfg || !res) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  if (mode != PG_MULTI_ROWS) {
+    g_err = "mode must be PG_MULTI_ROWS";
+    return PG_EINVAL;
+  }
+  int rc = pg_config_validate(cfg);
+  if (rc) return rc;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    g_err = "no CUDA device visible (the B200 engine has no CPU fallback)";
+    return PG_ENODEV;
+  }
+  if (ngpus < 1 || cfg->device < 0 || cfg->device + ngpus > ndev) {
+    g_err = "ngpus out of range (devices cfg->device .. cfg->device + ngpus - 1 must exist)";
+    return PG_EINVAL;
+  }
+  if (!p->row_ptr || p->num_rows < 0) {
+    g_err = "problem arrays are NULL";
+    return PG_EINVAL;
+  }
+  uint8_t uid[128];
+  if ((rc = pg_nccl_unique_id(uid))) return rc;
+  const int32_t m = p->num_rows;
+  // shard g: rows [r[g], r[g+1]), ~nnz / ngpus entries each
+  std::vector<int32_t> r(ngpus + 1, 0);
+  for (int g = 1; g < ngpus; ++g) {
+    const int64_t target = p->nnz * g / ngpus;
+    r[g] = (int32_t)(std::lower_bound(p->row_ptr, p->row_ptr + m + 1, target) - p->row_ptr);
+    r[g] = std::max(r[g], r[g - 1]);
+  }
+  r[ngpus] = m;
+  std::vector<std::vector<int32_t>> rps(ngpus);
+  std::vector<int> rcs(ngpus, PG_OK), stage(ngpus, 0);
+  std::vector<std::string> errs(ngpus);
+  std::vector<pg_session*> ss(ngpus, nullptr);
+  std::vector<pg_result> rr(ngpus);
+  std::mutex mu;
+  std::condition_variable cv;
+  int created = 0;
+  bool abort_all = false;
+  auto work = [&](int g) {
+    pg_problem q = *p;
+    const int32_t k0 = p->row_ptr[r[g]];
+    rps[g].resize((size_t)(r[g + 1] - r[g]) + 1);
+    for (int32_t i = r[g]; i <= r[g + 1]; ++i) rps[g][i - r[g]] = p->row_ptr[i] - k0;
+    q.num_rows = r[g + 1] - r[g];
+    q.nnz = p->row_ptr[r[g + 1]] - k0;
+    q.row_ptr = rps[g].data();
+    q.col_idx = p->col_idx ? p->col_idx + k0 : nullptr;
+    q.values = p->values ? p->values + k0 : nullptr;
+    q.lhs = p->lhs ? p->lhs + r[g] : nullptr;
+    q.rhs = p->rhs ? p->rhs + r[g] : nullptr;
+    pg_config c = *cfg;
+    c.device = cfg->device + g;
+    int e = pg_session_create(&q, &c, &ss[g]);
+    {
+      // every rank must have a session before any enters the NCCL init
+      std::unique_lock<std::mutex> lk(mu);
+      if (e) abort_all = true;
+      ++created;
+      cv.notify_all();
+      cv.wait(lk, [&] { return created == ngpus; });
+      if (abort_all) {
+        rcs[g] = e;
+        errs[g] = e ? pg_last_error() : "";
+        return;
+      }
+    }
+    e = pg_session_attach_comm(ss[g], uid, g, ngpus);
+    if (!e) {
+      rr[g] = pg_result{};
+      if (g == 0) rr[g] = *res;
+      e = pg_session_propagate(ss[g], nullptr, nullptr, &rr[g]);
+    }
+    rcs[g] = e;
+    if (e) errs[g] = pg_last_error();
+  };
+  std::vector<std::thread> th;
+  for (int g = 1; g < ngpus; ++g) th.emplace_back(work, g);
+  work(0);
+  for (auto& t : th) t.join();
+  for (int g = 0; g < ngpus; ++g)
+    if (ss[g]) pg_session_destroy(ss[g]);
+  for (int g = 0; g < ngpus; ++g)
+    if (rcs[g]) {
+      g_err = "rank " + std::to_string(g) + ": " + errs[g];
+      return rcs[g];
+    }
+  const pg_result out = rr[0];
+  res->status = out.status;
+  res->rounds_executed = out.rounds_executed;
+  res->total_bound_changes = out.total_bound_changes;
+  res->constraints_processed = (int64_t)out.rounds_executed * m;
+  res->elapsed_ns = out.elapsed_ns;
+  return PG_OK;
+}
+
 int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info) {
   if (!s || !info) {
     g_err = "NULL argument";

@@ -59,6 +59,19 @@ def csr_from_triplets_gpu(rows, cols, values, num_rows: int, num_cols: int,
     return SparseMatrix(num_rows, num_cols, rp, ci[:k], vo[:k])
 
 
+def propagate_multi_gpu(instance: ProblemInstance, cfg: EngineConfig | None = None,
+                        ngpus: int = 1) -> PropagationResult:
+    """pg_multi_propagate: one process, ngpus devices (cfg.device ..), row
+    shards merged over NCCL every round; same results as propagate_gpu."""
+    cfg = cfg or EngineConfig()
+    c = cfg.to_c()
+    p = instance.to_c()
+    r, lo, up, prc = new_c_result(instance.num_cols(), cfg.round_limit)
+    abi.check(_lib().pg_multi_propagate(C.byref(p), C.byref(c), ngpus, abi.PG_MULTI_ROWS,
+                                        C.byref(r)), "pg_multi_propagate")
+    return result_from_c(r, lo, up, prc)
+
+
 def propagate_gpu(instance: ProblemInstance, cfg: EngineConfig | None = None) -> PropagationResult:
     cfg = cfg or EngineConfig()
     c = cfg.to_c()

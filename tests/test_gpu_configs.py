@@ -187,3 +187,25 @@ def test_batched_nodes_many(row_check):
             assert st[k] == int(ref.status) and rd[k] == ref.rounds_executed, k
             assert np.array_equal(O.canon(blo[k]), O.canon(ref.bounds.lower)), k
             assert np.array_equal(O.canon(bup[k]), O.canon(ref.bounds.upper)), k
+
+
+@pytest.mark.gpu
+def test_multi_propagate_single_process():
+    """pg_multi_propagate (one host thread per GPU, NCCL row shards) with the
+    devices this box has: bit-exact with the oracle; more GPUs than exist is
+    PG_EINVAL"""
+    import torch
+    from paper_2009_07785_b200.engine import propagate_multi_gpu
+    try:
+        from paper_2009_07785_b200.multi import nccl_unique_id
+        nccl_unique_id()
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    ng = torch.cuda.device_count()
+    for inst in (G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003),
+                 G.gen_random(4000, 4000, 9, mean_row_nnz=10.0, integral_fraction=0.5)):
+        for wl in (False, True):
+            r = propagate_multi_gpu(inst, EngineConfig(row_check=False, worklist=wl), ngpus=ng)
+            assert_bit_exact(r, O.propagate_parallel(inst, PAR), inst.name)
+    with pytest.raises(ValueError):
+        propagate_multi_gpu(inst, EngineConfig(), ngpus=ng + 1)
