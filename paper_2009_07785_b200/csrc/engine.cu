@@ -788,7 +788,6 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     const int64_t nnz = s->nnz;
     const int32_t short_max = (int32_t)std::min<int64_t>(cfg->nnz_budget, kShortMax);
     const int32_t chunk = cfg->nnz_budget;
-    const int32_t nb = short_max + 2;  // length classes 0..short_max, then segment rows
     cudaStream_t st = s->stream, s2 = s->stream2;
 
     // buffers: the caller's arrays staged in input row order, the ordering work

@@ -142,7 +142,7 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
 }
 
 __device__ __forceinline__ void ld_snap(const Snap* p, double& lo, double& up, double& q) {
-  long long f;
+  [[maybe_unused]] long long f;  // the flags word rides along in the 256-bit load
   asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];"
       : "=d"(lo), "=d"(up), "=d"(q), "=l"(f)
       : "l"(p));

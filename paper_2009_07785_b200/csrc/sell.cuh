@@ -95,7 +95,7 @@ __device__ __forceinline__ void ld_snap_keep(const Snap* p, uint64_t pol, double
   ld_snap(p, lo, up, q);
   return;
 #endif
-  long long f;
+  [[maybe_unused]] long long f;  // the flags word rides along in the 256-bit load
   asm volatile("ld.global.nc.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
                : "=d"(lo), "=d"(up), "=d"(q), "=l"(f)
                : "l"(p), "l"(pol));
@@ -360,7 +360,7 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
                                            int lane, bool full, const uint8_t* rflag,
                                            uint64_t pol_keep, uint64_t pol_stream, bool& inf_flag,
                                            const DevCfg& cfg) {
-  constexpr int G = 1 << LG, H = 32 >> LG;
+  constexpr int H = 32 >> LG;
   const int j = lane >> (5 - LG), u = lane & (H - 1);
   UnitDesc ud = {0, -1};
   bool active = u < sd.count;
@@ -376,7 +376,6 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
   const double* sv = A.sv + sd.off + lane;
   const int32_t* sc = A.sc + sd.off + lane;
   uint32_t* sw = A.sw + sd.off + lane;
-  const bool whole = ud.ref >= 0;
   const int steps = sd.steps;
   const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
 
