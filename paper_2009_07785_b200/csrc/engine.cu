@@ -198,6 +198,54 @@ Nccl g_nccl;
 
 }  // namespace
 
+// Streams and events of finished sessions, kept per device for the next
+// session (creating them costs ~0.1 ms per one-shot call).  Pending
+// stream-ordered work on a returned stream simply precedes the next user's.
+struct StreamSet {
+  cudaStream_t st = nullptr, st2 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, fork = nullptr, join = nullptr;
+};
+struct StreamPool {
+  std::mutex mu;
+  std::vector<StreamSet> free_sets[64];
+  StreamSet get(int dev) {  // the caller has made `dev` current
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (dev >= 0 && dev < 64 && !free_sets[dev].empty()) {
+        const StreamSet x = free_sets[dev].back();
+        free_sets[dev].pop_back();
+        return x;
+      }
+    }
+    StreamSet x;
+    PG_CUDA(cudaStreamCreateWithFlags(&x.st, cudaStreamNonBlocking));
+    PG_CUDA(cudaStreamCreateWithFlags(&x.st2, cudaStreamNonBlocking));
+    PG_CUDA(cudaEventCreate(&x.ev0));
+    PG_CUDA(cudaEventCreate(&x.ev1));
+    PG_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
+    PG_CUDA(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
+    return x;
+  }
+  void put(int dev, const StreamSet& x) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      if (dev >= 0 && dev < 64 && free_sets[dev].size() < 4 && x.st && x.st2 && x.ev0 && x.ev1 &&
+          x.fork && x.join) {
+        free_sets[dev].push_back(x);
+        return;
+      }
+    }
+    for (cudaEvent_t e : {x.ev0, x.ev1, x.fork, x.join})
+      if (e) cudaEventDestroy(e);
+    for (cudaStream_t q : {x.st, x.st2})
+      if (q) cudaStreamDestroy(q);
+  }
+  static StreamPool& get() {
+    static StreamPool* p = new StreamPool;  // never destroyed (reaper thread)
+    return *p;
+  }
+};
+
 struct pg_session {
   int dev = 0;
   cudaStream_t stream = nullptr;
@@ -308,11 +356,7 @@ struct pg_session {
     t_alloc_stream = stream;
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
-    if (ev0) cudaEventDestroy(ev0);
-    if (ev1) cudaEventDestroy(ev1);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
-    if (stream2) cudaStreamDestroy(stream2);
+
     if (comm) g_nccl.comm_destroy(comm);
     for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up, (void*)d_delta,
                     (void*)d_delta_all, (void*)d_dcnt, (void*)d_dcnt_all})
@@ -324,7 +368,7 @@ struct pg_session {
                     d_flags, d_chg, d_row_unit, d_part_unit, d_unit_slice, d_wide_list, d_unit_list, d_tflag, d_tlist};
     for (void* p : ptrs) dfree(p);  // stream-ordered: no device sync here
     if (h_st) cudaFreeHost(h_st);
-    if (stream) cudaStreamDestroy(stream);
+    StreamPool::get().put(dev, StreamSet{stream, stream2, ev0, ev1, ev_fork, ev_join});
   }
 
   int grid_for(int64_t items, int threads, int per_sm = 8) const {
@@ -775,13 +819,16 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->dcfg.chunk = cfg->nnz_budget;
     s->dcfg.round_limit = cfg->round_limit;
     s->dcfg.flags = cfg->flags;
-    PG_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+    {
+      const StreamSet x = StreamPool::get().get(s->dev);
+      s->stream = x.st;
+      s->stream2 = x.st2;
+      s->ev0 = x.ev0;
+      s->ev1 = x.ev1;
+      s->ev_fork = x.fork;
+      s->ev_join = x.join;
+    }
     t_alloc_stream = s->stream;
-    PG_CUDA(cudaEventCreate(&s->ev0));
-    PG_CUDA(cudaStreamCreateWithFlags(&s->stream2, cudaStreamNonBlocking));
-    PG_CUDA(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
-    PG_CUDA(cudaEventCreateWithFlags(&s->ev_join, cudaEventDisableTiming));
-    PG_CUDA(cudaEventCreate(&s->ev1));
 
     tm.lap("streams/attributes");
     const int32_t m = s->m, n = s->n;
