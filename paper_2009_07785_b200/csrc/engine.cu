@@ -803,7 +803,10 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       }
       s->sell_per_sm = std::max(1, o.sell);
       s->sell_dense_per_sm = std::max(1, o.sell_dense);
-      s->cand_per_sm = std::max(1, o.cand);
+      // one k_cand CTA per SM: the queues are drained by tickets, and fewer
+      // CTAs start and drain faster (A/B: 1 < 2 < full occupancy on C2/C5)
+      s->cand_per_sm = 1;
+      if (const char* e = getenv("PG_CAND_PER_SM")) s->cand_per_sm = std::max(1, atoi(e));
       s->loop_grid = o.loop_grid;
       s->nodes_per_sm = std::max(1, o.nodes);
     }
