@@ -499,13 +499,16 @@ struct pg_session {
                                        kNcclMax, comm, stream);
       if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllReduce: ") + g_nccl.error(rc)};
     }
-    k_commit<<<grid_for(n, kCommitThreads, 4), kCommitThreads, 0, stream>>>(
+    // commit / list / mark grids per SM (env overrides: A/B experiments)
+    static const int commit_per_sm = getenv("PG_COMMIT_PER_SM") ? atoi(getenv("PG_COMMIT_PER_SM")) : 2;
+    static const int list_per_sm = getenv("PG_LIST_PER_SM") ? atoi(getenv("PG_LIST_PER_SM")) : 2;
+    k_commit<<<grid_for(n, kCommitThreads, commit_per_sm), kCommitThreads, 0, stream>>>(
         d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0,
         comm ? 0 : 1);
     if (dirty.enabled && !comm)
-      k_commit_list<<<num_sms * 2, kCommitThreads, 0, stream>>>(
+      k_commit_list<<<num_sms * list_per_sm, kCommitThreads, 0, stream>>>(
           d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, touch, cond, use_graph ? 1 : 0);
-    if (dirty.enabled) k_mark<<<num_sms * 2, 256, 0, stream>>>(dirty, d_st);
+    if (dirty.enabled) k_mark<<<num_sms * list_per_sm, 256, 0, stream>>>(dirty, d_st);
     PG_CUDA(cudaGetLastError());
   }
 
