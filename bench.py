@@ -122,7 +122,7 @@ def dist_init():
 
 
 def make_instance(config, seed):
-    from paper_2009_07785_b200 import generators as G
+    from instances import generators as G
     return G.config_instance(config, seed)
 
 
@@ -324,7 +324,7 @@ def bench_single(args, inst, world, rank, local):
 
 
 def c4_nodes(inst, root_lo, root_up, k0, k1):
-    from paper_2009_07785_b200 import generators as G
+    from instances import generators as G
     from paper_2009_07785_b200.engine import node_overrides
     lo, up = G.gen_nodes(inst, root_lo, root_up, K=k1 - k0, seed_base=4_000_000 + k0)
     return lo, up, node_overrides(root_lo, root_up, lo, up)

@@ -170,6 +170,18 @@ int pg_session_create(const pg_problem* prob, const pg_config* cfg,
                       pg_session** out);
 void pg_session_destroy(pg_session* s);
 
+/* pg_session_create returns once the caller's arrays have been copied (they
+ * may be freed or reused right away). */
+
+/* pg_round on a resident session (propagate_round_parallel,
+ * par_engine.hpp:33-36): one round on the snapshot lb_in/ub_in, the matrix
+ * set up once per session instead of once per call (a branch-and-bound
+ * caller of the one-round API).  Wide64 single-GPU sessions only
+ * (PG_EINVAL otherwise). */
+int pg_session_round(pg_session* s, const double* lb_in, const double* ub_in,
+                     double* lb_out, double* ub_out, int32_t* changed,
+                     int32_t* infeasible, int64_t* changes);
+
 /* Propagate from new start bounds (NULL = the problem's own bounds), host
  * buffers in and out.  Same semantics as pg_propagate. */
 int pg_session_propagate(pg_session* s, const double* lower,

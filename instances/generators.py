@@ -1,4 +1,4 @@
-"""Seeded synthetic instances (ingest side; see csrc/gen/pgen.cpp).
+"""Seeded synthetic instances (test/bench input; see instances/pgen.cpp).
 
 gen_random / gen_cascade restate the reference generators
 (core/src/generators.cpp:13-168) bit-for-bit; the config generators follow
@@ -16,14 +16,57 @@ import ctypes as C
 
 import numpy as np
 
-from . import abi
-from .model import ProblemInstance
+import os
+
+from paper_2009_07785_b200 import abi
+from paper_2009_07785_b200.model import ProblemInstance
+
+GEN_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libpgen.so")
+_gen = None
+
+
+def load_gen(path: str = GEN_PATH):
+    """libpgen.so (instances/pgen.cpp), built by __graft_entry__.build()."""
+    global _gen
+    if _gen is not None:
+        return _gen
+    if not os.path.exists(path):
+        raise abi.EngineError(f"{path} is missing: run __graft_entry__.build()")
+    g = C.CDLL(path)
+    g.pgen_view.argtypes = [C.c_void_p, C.POINTER(abi.PgProblem)]
+    g.pgen_view.restype = None
+    g.pgen_free.argtypes = [C.c_void_p]
+    g.pgen_free.restype = None
+    g.pgen_from_arrays.argtypes = [C.POINTER(abi.PgProblem)]
+    g.pgen_from_arrays.restype = C.c_void_p
+    g.pgen_random.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double,
+                              C.c_double, C.c_double, C.c_int64]
+    g.pgen_random.restype = C.c_void_p
+    g.pgen_cascade.argtypes = [C.c_int32]
+    g.pgen_cascade.restype = C.c_void_p
+    g.pgen_powerlaw.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double,
+                                C.c_int32, C.c_double, C.c_double, C.c_double]
+    g.pgen_powerlaw.restype = C.c_void_p
+    g.pgen_longrows.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
+                                C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double]
+    g.pgen_longrows.restype = C.c_void_p
+    g.pgen_setpart.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
+                               C.c_uint64, C.c_int32]
+    g.pgen_setpart.restype = C.c_void_p
+    g.pgen_nodes.argtypes = [C.POINTER(abi.PgProblem), abi._dp, abi._dp, C.c_int32, C.c_uint64, C.c_int32,
+                             C.c_int32, abi._dp, abi._dp]
+    g.pgen_nodes.restype = C.c_int
+    g.pgen_acceptance_sizes.argtypes = [C.c_int32, abi._ip, abi._ip]
+    g.pgen_acceptance_sizes.restype = None
+    _gen = g
+    return g
+
 
 
 def _take(h, name) -> ProblemInstance:
     if not h:
         raise ValueError(f"{name}: invalid generator arguments")
-    g = abi.load_gen()
+    g = load_gen()
     try:
         p = abi.PgProblem()
         g.pgen_view(h, C.byref(p))
@@ -35,19 +78,19 @@ def _take(h, name) -> ProblemInstance:
 def gen_random(num_rows=100, num_cols=100, seed=0, mean_row_nnz=6.0, integral_fraction=0.3,
                infinite_bound_fraction=0.05, infinite_side_fraction=0.25, max_nnz=0):
     """RandomInstanceOptions defaults (generators.hpp:19-28)."""
-    h = abi.load_gen().pgen_random(num_rows, num_cols, seed, mean_row_nnz, integral_fraction,
+    h = load_gen().pgen_random(num_rows, num_cols, seed, mean_row_nnz, integral_fraction,
                                    infinite_bound_fraction, infinite_side_fraction, max_nnz)
     return _take(h, f"random_r{num_rows}_c{num_cols}_s{seed}")
 
 
 def gen_cascade(m: int):
-    return _take(abi.load_gen().pgen_cascade(m), f"cascade{m}")
+    return _take(load_gen().pgen_cascade(m), f"cascade{m}")
 
 
 def gen_powerlaw(num_rows=1_000_000, num_cols=1_000_000, seed=20090778, x_min=4.25, beta=1.5,
                  cap=10_000, integral_fraction=0.5, infinite_bound_fraction=0.05,
                  infinite_side_fraction=0.25):
-    h = abi.load_gen().pgen_powerlaw(num_rows, num_cols, seed, x_min, beta, cap, integral_fraction,
+    h = load_gen().pgen_powerlaw(num_rows, num_cols, seed, x_min, beta, cap, integral_fraction,
                                      infinite_bound_fraction, infinite_side_fraction)
     return _take(h, f"powerlaw_r{num_rows}_c{num_cols}_s{seed}")
 
@@ -55,7 +98,7 @@ def gen_powerlaw(num_rows=1_000_000, num_cols=1_000_000, seed=20090778, x_min=4.
 def gen_longrows(num_rows=100_000, num_cols=200_000, seed=3001, long_every=100, long_min=100_000,
                  long_max=150_000, mean_short=8.0, integral_fraction=0.5,
                  infinite_bound_fraction=0.05, infinite_side_fraction=0.25):
-    h = abi.load_gen().pgen_longrows(num_rows, num_cols, seed, long_every, long_min, long_max,
+    h = load_gen().pgen_longrows(num_rows, num_cols, seed, long_every, long_min, long_max,
                                      mean_short, integral_fraction, infinite_bound_fraction,
                                      infinite_side_fraction)
     return _take(h, f"longrows_r{num_rows}_c{num_cols}_s{seed}")
@@ -63,7 +106,7 @@ def gen_longrows(num_rows=100_000, num_cols=200_000, seed=3001, long_every=100, 
 
 def gen_setpart(num_rows=1_000_000, num_cols=5_000_000, per_row=50, s1_fraction=0.1,
                 f_fixed=0.2, seed=5001, infeasible=False):
-    h = abi.load_gen().pgen_setpart(num_rows, num_cols, per_row, s1_fraction, f_fixed, seed,
+    h = load_gen().pgen_setpart(num_rows, num_cols, per_row, s1_fraction, f_fixed, seed,
                                     1 if infeasible else 0)
     return _take(h, f"setpart_r{num_rows}_c{num_cols}_s{seed}{'_inf' if infeasible else ''}")
 
@@ -77,7 +120,7 @@ def gen_nodes(inst: ProblemInstance, root_lower, root_upper, K: int, seed_base=4
     rl = np.ascontiguousarray(root_lower, dtype=np.float64)
     ru = np.ascontiguousarray(root_upper, dtype=np.float64)
     p = inst.to_c()
-    rc = abi.load_gen().pgen_nodes(C.byref(p), abi.ptr(rl, C.c_double), abi.ptr(ru, C.c_double), K,
+    rc = load_gen().pgen_nodes(C.byref(p), abi.ptr(rl, C.c_double), abi.ptr(ru, C.c_double), K,
                                    seed_base, dmin, dmax, abi.ptr(lo, C.c_double),
                                    abi.ptr(up, C.c_double))
     if rc != 0:
@@ -108,7 +151,7 @@ def acceptance_suite_params(count=500):
     (tests/acceptance.cpp:56-75)."""
     rows = np.zeros(count, dtype=np.int32)
     cols = np.zeros(count, dtype=np.int32)
-    abi.load_gen().pgen_acceptance_sizes(count, abi.ptr(rows, C.c_int32), abi.ptr(cols, C.c_int32))
+    load_gen().pgen_acceptance_sizes(count, abi.ptr(rows, C.c_int32), abi.ptr(cols, C.c_int32))
     return [(int(r), int(c), 1000 + i, 50000) for i, (r, c) in enumerate(zip(rows, cols))]
 
 

@@ -25,7 +25,7 @@
 #include <random>
 #include <vector>
 
-#include "../../../include/propgate_b200.h"
+#include "../include/propgate_b200.h"
 
 namespace {
 

@@ -15,7 +15,6 @@ import numpy as np
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
 REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.path.join(PKG_DIR, "libpropgate_b200.so")
-GEN_PATH = os.path.join(PKG_DIR, "libpgen.so")
 
 PG_OK, PG_EINVAL, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_ENODEV, PG_ERANGE = 0, -1, -2, -3, -4, -5, -6
 PG_CONVERGED, PG_ROUNDLIMIT, PG_INFEASIBLE = 0, 1, 2
@@ -115,6 +114,7 @@ PROTOTYPES = {
     "pg_session_create": (C.c_int, [C.POINTER(PgProblem), C.POINTER(PgConfig), C.POINTER(C.c_void_p)]),
     "pg_session_destroy": (None, [C.c_void_p]),
     "pg_session_propagate": (C.c_int, [C.c_void_p, _dp, _dp, C.POINTER(PgResult)]),
+    "pg_session_round": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, _ip, _ip, _lp]),
     "pg_session_run": (C.c_int, [C.c_void_p, C.POINTER(PgResult)]),
     "pg_session_propagate_batch": (C.c_int, [C.c_void_p, C.c_int32, _dp, _dp, _dp, _dp, _ip, _ip]),
     "pg_session_time_round_kernel": (C.c_int, [C.c_void_p, C.c_int32, _dp, _dp]),
@@ -138,7 +138,6 @@ class EngineError(RuntimeError):
 
 
 _lib = None
-_gen = None
 
 
 def load_library(path: str | None = None):
@@ -170,39 +169,3 @@ def check(rc: int, what: str):
         if rc == PG_ERANGE:  # std::out_of_range in the reference
             raise IndexError(f"{what}: {msg}")
         raise EngineError(f"{what} failed ({rc}): {msg}")
-
-
-def load_gen(path: str = GEN_PATH):
-    global _gen
-    if _gen is not None:
-        return _gen
-    if not os.path.exists(path):
-        raise EngineError(f"{path} is missing: run __graft_entry__.build()")
-    g = C.CDLL(path)
-    g.pgen_view.argtypes = [C.c_void_p, C.POINTER(PgProblem)]
-    g.pgen_view.restype = None
-    g.pgen_free.argtypes = [C.c_void_p]
-    g.pgen_free.restype = None
-    g.pgen_from_arrays.argtypes = [C.POINTER(PgProblem)]
-    g.pgen_from_arrays.restype = C.c_void_p
-    g.pgen_random.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double,
-                              C.c_double, C.c_double, C.c_int64]
-    g.pgen_random.restype = C.c_void_p
-    g.pgen_cascade.argtypes = [C.c_int32]
-    g.pgen_cascade.restype = C.c_void_p
-    g.pgen_powerlaw.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_double, C.c_double,
-                                C.c_int32, C.c_double, C.c_double, C.c_double]
-    g.pgen_powerlaw.restype = C.c_void_p
-    g.pgen_longrows.argtypes = [C.c_int32, C.c_int32, C.c_uint64, C.c_int32, C.c_int32,
-                                C.c_int32, C.c_double, C.c_double, C.c_double, C.c_double]
-    g.pgen_longrows.restype = C.c_void_p
-    g.pgen_setpart.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_double, C.c_double,
-                               C.c_uint64, C.c_int32]
-    g.pgen_setpart.restype = C.c_void_p
-    g.pgen_nodes.argtypes = [C.POINTER(PgProblem), _dp, _dp, C.c_int32, C.c_uint64, C.c_int32,
-                             C.c_int32, _dp, _dp]
-    g.pgen_nodes.restype = C.c_int
-    g.pgen_acceptance_sizes.argtypes = [C.c_int32, _ip, _ip]
-    g.pgen_acceptance_sizes.restype = None
-    _gen = g
-    return g

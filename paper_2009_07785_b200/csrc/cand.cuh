@@ -98,19 +98,24 @@ __device__ __forceinline__ void cand_push(CandWarpSmem& W, int& qn, bool pass, d
 }
 
 // entry k of the row in slot `slot`: gather, filter
-__device__ __forceinline__ bool cand_entry(const RoundArgs& A, const CandWarpSmem& W, int slot,
+template <class RA>
+__device__ __forceinline__ bool cand_entry(const RA& A, const CandWarpSmem& W, int slot,
                                            int k, double& a, double& lo, double& up, int32_t& c) {
   a = __ldg(A.vals + k);
   c = __ldg(A.colx + k);
   double q;
-  ld_snap(A.snap + (c & 0x7fffffff), lo, up, q);
+  if constexpr (coherent_v<RA>)
+    ld_snap_coh(A.snap + (c & 0x7fffffff), lo, up, q);
+  else
+    ld_snap(A.snap + (c & 0x7fffffff), lo, up, q);
   const double bmin = a > 0 ? lo : up;
   const double bmax = a > 0 ? up : lo;
   const RowFilter f = {W.tr[slot], W.tl[slot], W.mode[slot]};
   return entry_may(f, fabs(a) * q, isinf(bmin), isinf(bmax));
 }
 
-__device__ __forceinline__ void cand_sweep(const RoundArgs& A, const DevCfg& cfg,
+template <class RA>
+__device__ __forceinline__ void cand_sweep(const RA& A, const DevCfg& cfg,
                                            CandWarpSmem* smem) {
   const int lane = threadIdx.x & 31;
   CandWarpSmem& W = smem[threadIdx.x >> 5];

@@ -546,14 +546,14 @@ struct pg_session {
     d_col_item = dalloc<int32_t>(nnz);
     int32_t* cnt = dalloc<int32_t>((size_t)n + 1);
     PG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * ((size_t)n + 1), st));
-    if (nnz) k_csc_count<<<grid_for(nnz, 256, 16), 256, 0, st>>>(cols, nnz, cnt);
+    if (nnz) k_csc_count<<<grid_for(nnz, 256, 16), 256, 0, st>>>(cols, nnz, n, cnt);
     size_t tmp_bytes = 0;
     PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, cnt, d_col_ptr, n + 1, st));
     void* tmp = dalloc<unsigned char>(tmp_bytes);
     PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, d_col_ptr, n + 1, st));
     PG_CUDA(cudaMemcpyAsync(cnt, d_col_ptr, sizeof(int32_t) * ((size_t)n + 1),
                             cudaMemcpyDeviceToDevice, st));
-    if (m) k_csc_fill<<<grid_for(nnz * 32 / kWalkChunk + 1, 256, 16), 256, 0, st>>>(rp, cols, m, cnt,
+    if (m) k_csc_fill<<<grid_for(nnz * 32 / kWalkChunk + 1, 256, 16), 256, 0, st>>>(rp, cols, m, n, cnt,
                                                                                    rowmap, d_col_item);
     PG_CUDA(cudaGetLastError());
     dfree(tmp);
@@ -575,7 +575,7 @@ struct pg_session {
   }
 
   void enqueue_persistent() {
-    const RoundArgs A = round_args();
+    const RoundArgsL A{round_args()};
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3(loop_grid);
     lc.blockDim = dim3(kSellThreads);
@@ -693,12 +693,18 @@ struct pg_session {
     }
     PG_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(DevState), cudaMemcpyDeviceToHost, stream));
     PG_CUDA(cudaStreamSynchronize(stream));
+    check_input();
     float ms = 0.f;
     PG_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
     return (int64_t)((double)ms * 1e6);
   }
 
   bool bounds_done = false;  // run_solve already downloaded the bounds
+
+  // a col_idx outside [0, n) found during setup (k_permute_rows); h_st fresh
+  void check_input() const {
+    if (h_st->bad_input) throw Error{PG_EINVAL, "col_idx entry outside [0, num_cols)"};
+  }
 
   void fill_result(pg_result* res, int64_t elapsed) {
     res->status = h_st->status < 0 ? PG_ROUNDLIMIT : h_st->status;
@@ -856,7 +862,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     int32_t* idx = dalloc<int32_t>(m);
     int32_t* t_perm = dalloc<int32_t>(m);
     int32_t* slen = dalloc<int32_t>((size_t)m + 1);
-    int32_t* counts = dalloc<int32_t>(kMaxClasses + 4);  // + u64 sum of len^2 at [kMaxClasses + 2]
+    int32_t* counts = dalloc<int32_t>(kMaxClasses + 5);  // + u64 sum of len^2 at [kMaxClasses + 2], bad row_ptr flag at [+4]
     PG_CUDA(cudaEventRecord(s->ev_fork, st));
     PG_CUDA(cudaStreamWaitEvent(s2, s->ev_fork, 0));
     // stream 1: the bulk of the upload (asynchronous from pinned memory)
@@ -891,9 +897,11 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         t_alloc_stream = prev;
       }
     };
-    std::vector<int32_t> cls(kMaxClasses + 4, 0);
+    std::vector<int32_t> cls(kMaxClasses + 5, 0);
     if (m) {
-      k_row_keys<<<s->grid_for(m, 256), 256, 0, s2>>>(t_rp, m, short_max, key, idx);
+      PG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (kMaxClasses + 5), s2));
+      k_row_keys<<<s->grid_for(m, 256), 256, 0, s2>>>(t_rp, m, nnz, short_max, key, idx,
+                                                      counts + kMaxClasses + 4);
       size_t need = 0;
       PG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, idx, t_perm, m, 0, 5, s2));
       cub_tmp(need);
@@ -902,14 +910,15 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, slen, s->d_row_ptr, m + 1, s2));
       cub_tmp(need);
       PG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, need, slen, s->d_row_ptr, m + 1, s2));
-      PG_CUDA(cudaMemsetAsync(counts, 0, sizeof(int32_t) * (kMaxClasses + 4), s2));
       k_class_counts<<<s->grid_for(m, 256), 256, 0, s2>>>(key2, m, counts);
       auto* len2 = reinterpret_cast<unsigned long long*>(counts + kMaxClasses + 2);
       k_len2_sum<<<s->grid_for(m, 256), 256, 0, s2>>>(t_rp, m, len2);
-      PG_CUDA(cudaMemcpyAsync(cls.data(), counts, sizeof(int32_t) * (kMaxClasses + 4),
+      PG_CUDA(cudaMemcpyAsync(cls.data(), counts, sizeof(int32_t) * (kMaxClasses + 5),
                               cudaMemcpyDeviceToHost, s2));
       PG_CUDA(cudaStreamSynchronize(s2));
       unsigned long long l2 = 0;
+      if (cls[kMaxClasses + 4])
+        throw Error{PG_EINVAL, "row_ptr must be non-decreasing with entries in [0, nnz]"};
       std::memcpy(&l2, cls.data() + kMaxClasses + 2, sizeof(l2));
       s->row_density = (double)l2 / std::max(1.0, (double)n * (double)nnz);
     }
@@ -1108,7 +1117,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     if (m) {
       k_permute_rows<<<s->grid_for(std::max<int64_t>(m, nnz * 32 / kWalkChunk + 1), 256, 16), 256, 0, st>>>(
           t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, s->d_integral, s->d_colx,
-          s->d_vals, s->d_lhs, s->d_rhs, m, cfg->infinity_threshold);
+          s->d_vals, s->d_lhs, s->d_rhs, m, n, cfg->infinity_threshold, s->d_st);
       PG_CUDA(cudaGetLastError());
     }
     if (cfg->scalar_mode == PG_NARROW32) {
@@ -1315,7 +1324,10 @@ int pg_config_validate(const pg_config* cfg) {
   return validate(cfg);
 }
 
-int pg_session_create(const pg_problem* p, const pg_config* cfg, pg_session** out) {
+namespace {
+// session setup without the final wait: the one-shot calls (pg_propagate,
+// pg_round) go straight on to the solve, which syncs before they return
+int session_create_async(const pg_problem* p, const pg_config* cfg, pg_session** out) {
   if (!out) {
     g_err = "out is NULL";
     return PG_EINVAL;
@@ -1327,6 +1339,24 @@ int pg_session_create(const pg_problem* p, const pg_config* cfg, pg_session** ou
     *out = create_session(p, cfg);
     return PG_OK;
   });
+}
+}  // namespace
+
+int pg_session_create(const pg_problem* p, const pg_config* cfg, pg_session** out) {
+  int rc = session_create_async(p, cfg, out);
+  if (rc) return rc;
+  // the caller's arrays (pinned ones are copied asynchronously) may be freed
+  // or reused as soon as this returns
+  rc = guarded([&] {
+    PG_CUDA(cudaStreamSynchronize((*out)->stream2));
+    PG_CUDA(cudaStreamSynchronize((*out)->stream));
+    return PG_OK;
+  });
+  if (rc) {
+    pg_session_destroy(*out);
+    *out = nullptr;
+  }
+  return rc;
 }
 
 void pg_session_destroy(pg_session* s) { delete s; }
@@ -1361,13 +1391,69 @@ int pg_session_propagate(pg_session* s, const double* lower, const double* upper
   });
 }
 
+int pg_session_round(pg_session* s, const double* lb_in, const double* ub_in, double* lb_out,
+                     double* ub_out, int32_t* changed, int32_t* infeasible, int64_t* changes) {
+  // propagate_round_parallel (par_engine.cpp:277-312) on a resident session:
+  // one round on the caller snapshot, no bounds_crossed pre-check, no row
+  // check, in double; the matrix setup is paid once per session, not per call
+  if (!s || !lb_in || !ub_in || !lb_out || !ub_out || !changed || !infeasible || !changes) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  if (s->cfg.scalar_mode != PG_WIDE64) {
+    g_err = "pg_session_round needs a Wide64 session (propagate_round_parallel works in double)";
+    return PG_EINVAL;
+  }
+  if (s->comm) {
+    g_err = "pg_session_round: row-sharded sessions are not supported";
+    return PG_EINVAL;
+  }
+  return guarded([&] {
+    PG_CUDA(cudaSetDevice(s->dev));
+    s->upload_bounds(lb_in, ub_in);
+    const pg_config saved = s->cfg;
+    const DevCfg dsaved = s->dcfg;
+    s->cfg.flags &= ~PG_FLAG_ROWCHECK;
+    s->dcfg.flags = s->cfg.flags;
+    s->dcfg.round_limit = 1;
+    struct Restore {
+      pg_session* s;
+      pg_config c;
+      DevCfg d;
+      ~Restore() {
+        s->cfg = c;
+        s->dcfg = d;
+      }
+    } restore{s, saved, dsaved};
+    PG_CUDA(cudaMemsetAsync(s->d_ctl, 0, sizeof(NodeCtl), s->stream));  // a cold start
+    s->enqueue_reset(false, false);
+    s->enqueue_round(false);
+    long long ch = 0;
+    PG_CUDA(cudaMemcpyAsync(&ch, s->d_per_round, sizeof(long long), cudaMemcpyDeviceToHost, s->stream));
+    PG_CUDA(cudaMemcpyAsync(s->h_st, s->d_st, sizeof(DevState), cudaMemcpyDeviceToHost, s->stream));
+    k_decode<<<s->grid_for(s->n, 256), 256, 0, s->stream>>>(s->d_key_out, s->d_lo_res, s->d_up_res,
+                                                            s->n);
+    PG_CUDA(cudaGetLastError());
+    PG_CUDA(cudaMemcpyAsync(lb_out, s->d_lo_res, sizeof(double) * s->n, cudaMemcpyDeviceToHost,
+                            s->stream));
+    PG_CUDA(cudaMemcpyAsync(ub_out, s->d_up_res, sizeof(double) * s->n, cudaMemcpyDeviceToHost,
+                            s->stream));
+    PG_CUDA(cudaStreamSynchronize(s->stream));
+    s->check_input();
+    *changes = ch;
+    *changed = ch > 0;
+    *infeasible = s->h_st->status == PG_INFEASIBLE;
+    return PG_OK;
+  });
+}
+
 int pg_propagate(const pg_problem* p, const pg_config* cfg, pg_result* res) {
   if (!res) {
     g_err = "result is NULL";
     return PG_EINVAL;
   }
   pg_session* s = nullptr;
-  int rc = pg_session_create(p, cfg, &s);
+  int rc = session_create_async(p, cfg, &s);
   if (rc) return rc;
   PhaseTimer tm;
   rc = pg_session_run(s, res);
@@ -1380,7 +1466,7 @@ int pg_propagate(const pg_problem* p, const pg_config* cfg, pg_result* res) {
 int pg_round(const pg_problem* p, const pg_config* cfg, const double* lb_in, const double* ub_in,
              double* lb_out, double* ub_out, int32_t* changed, int32_t* infeasible,
              int64_t* changes) {
-  if (!cfg || !lb_in || !ub_in || !lb_out || !ub_out || !changed || !infeasible || !changes) {
+  if (!p || !cfg || !lb_in || !ub_in || !lb_out || !ub_out || !changed || !infeasible || !changes) {
     g_err = "NULL argument";
     return PG_EINVAL;
   }
@@ -1397,7 +1483,7 @@ int pg_round(const pg_problem* p, const pg_config* cfg, const double* lb_in, con
   q.lower = lb_in;
   q.upper = ub_in;
   pg_session* s = nullptr;
-  rc = pg_session_create(&q, &c, &s);
+  rc = session_create_async(&q, &c, &s);
   if (rc) return rc;
   rc = guarded([&] {
     PG_CUDA(cudaSetDevice(s->dev));

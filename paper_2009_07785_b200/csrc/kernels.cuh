@@ -58,6 +58,7 @@ struct DevState {
   long long last_changes;            // changes of the previous round (worklist heuristics)
   uint32_t bar_count;                // grid barrier of the persistent round loop (loop.cuh)
   uint32_t bar_gen;
+  int32_t bad_input;                 // a col_idx outside [0, n) (set at session setup, sticky)
 };
 
 // Device-side worklist (PG_FLAG_WORKLIST): a round only
@@ -141,11 +142,21 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
+// read-only path: the snapshot is constant for the kernel's lifetime (every
+// per-round kernel; NOT the persistent loop, see ld_snap_coh)
 __device__ __forceinline__ void ld_snap(const Snap* p, double& lo, double& up, double& q) {
   [[maybe_unused]] long long f;  // the flags word rides along in the 256-bit load
-  asm("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];"
-      : "=d"(lo), "=d"(up), "=d"(q), "=l"(f)
-      : "l"(p));
+  asm volatile("ld.global.nc.v4.b64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(lo), "=d"(up), "=d"(q), "=l"(f)
+               : "l"(p));
+}
+// coherent path (L2, weak loads ordered by the grid barrier's fences): the
+// persistent loop rewrites the snapshot between its rounds inside one kernel
+__device__ __forceinline__ void ld_snap_coh(const Snap* p, double& lo, double& up, double& q) {
+  const double2 b = __ldcg(reinterpret_cast<const double2*>(p));
+  lo = b.x;
+  up = b.y;
+  q = __ldcg(&p->q);
 }
 
 // ---- exactness-preserving filters -----------------------------------------------
@@ -365,6 +376,14 @@ template <class RA>
 constexpr bool gather16_v = false;
 template <>
 constexpr bool gather16_v<RoundArgsG<true>> = true;
+// the persistent round loop (loop.cuh): snapshot and bounds records are
+// rewritten by the commit phase inside the same kernel, so its gathers use
+// coherent loads (never ld.global.nc)
+struct RoundArgsL : RoundArgs {};
+template <class RA>
+constexpr bool coherent_v = false;
+template <>
+constexpr bool coherent_v<RoundArgsL> = true;
 
 // A row's activity is complete: row check (propcore.hpp:147-156, cpu_seq's
 // verdicts), exactness-preserving row filter, and -- if some entry may
@@ -811,7 +830,8 @@ __global__ void k_permute_rows(const int32_t* __restrict__ rp, const int32_t* __
                                const int32_t* __restrict__ new_rp,
                                const uint8_t* __restrict__ integral, int32_t* __restrict__ colx,
                                double* __restrict__ new_vals, double* __restrict__ new_lhs,
-                               double* __restrict__ new_rhs, int m, double thr) {
+                               double* __restrict__ new_rhs, int m, int n, double thr,
+                               DevState* __restrict__ st) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
     const int old = perm[i];
     const double l = lhs[old], h = rhs[old];
@@ -821,8 +841,16 @@ __global__ void k_permute_rows(const int32_t* __restrict__ rp, const int32_t* __
   walk_entries(new_rp, m, new_rp[m], [&](bool valid, int64_t k, int r) {
     if (!valid) return;
     const int64_t src = rp[perm[r]] + (k - new_rp[r]);
-    const int32_t c = cols[src];
-    colx[k] = integral[c] ? (int32_t)(c | 0x80000000u) : c;
+    int32_t c = cols[src];
+    if ((uint32_t)c >= (uint32_t)n) {
+      // an out-of-range column index (undefined behaviour in the reference):
+      // reported as PG_EINVAL after the solve; the entry is parked on the
+      // padding column so that no kernel reads outside the arrays
+      st->bad_input = 1;
+      colx[k] = n;
+    } else {
+      colx[k] = integral[c] ? (int32_t)(c | 0x80000000u) : c;
+    }
     new_vals[k] = vals[src];
   });
 }
@@ -916,20 +944,24 @@ __global__ void k_max_row_len(const int32_t* __restrict__ rp, int m, int32_t* __
 // ---- worklist index (session init) -----------------------------------------------
 
 // column counts (flat over the entries)
-__global__ void k_csc_count(const int32_t* __restrict__ colx, int64_t nnz,
+__global__ void k_csc_count(const int32_t* __restrict__ colx, int64_t nnz, int n,
                             int32_t* __restrict__ cnt) {
   for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz;
        k += (int64_t)gridDim.x * blockDim.x)
-    atomicAdd(&cnt[colx[k] & 0x7fffffff], 1);
+  {
+    const uint32_t c = (uint32_t)colx[k] & 0x7fffffffu;
+    if (c < (uint32_t)n) atomicAdd(&cnt[c], 1);  // out of range: rejected at setup
+  }
 }
 
 // rows into their columns' ranges (entry-balanced walk); row r is named
 // rowmap[r] when given (a CSR in the caller's row order)
 __global__ void k_csc_fill(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ colx,
-                           int m, int32_t* __restrict__ cursor, const int32_t* __restrict__ rowmap,
-                           int32_t* __restrict__ col_row) {
+                           int m, int n, int32_t* __restrict__ cursor,
+                           const int32_t* __restrict__ rowmap, int32_t* __restrict__ col_row) {
   walk_entries(row_ptr, m, row_ptr[m], [&](bool valid, int64_t k, int r) {
-    if (valid) col_row[atomicAdd(&cursor[colx[k] & 0x7fffffff], 1)] = rowmap ? rowmap[r] : r;
+    const uint32_t c = (uint32_t)colx[k] & 0x7fffffffu;
+    if (valid && c < (uint32_t)n) col_row[atomicAdd(&cursor[c], 1)] = rowmap ? rowmap[r] : r;
   });
 }
 

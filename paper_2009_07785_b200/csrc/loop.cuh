@@ -42,7 +42,7 @@ union LoopSmem {
 
 template <bool kRowCheck>
 __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB)
-    k_loop(const RoundArgs A, const DevCfg cfg, Snap* __restrict__ snap, int n,
+    k_loop(const RoundArgsL A, const DevCfg cfg, Snap* __restrict__ snap, int n,
            long long* __restrict__ per_round, const int32_t* __restrict__ split, int nsplit) {
   extern __shared__ __align__(16) unsigned char loop_dyn[];  // LoopSmem
   LoopSmem& sm = *reinterpret_cast<LoopSmem*>(loop_dyn);
@@ -59,7 +59,9 @@ __global__ void __launch_bounds__(kSellThreads, PG_SELL_MINB)
       split_finish_body<kRowCheck, 64>(A, split, nsplit, sm.split, cfg);
       grid_barrier(A.st);
     }
-    if (ld_gpu(&A.st->wl_long)) {
+    // phase 2 of split rows: pieces of long rows AND batches of short split
+    // rows (a row of nnz_budget < len <= kCandShort entries, nnz_budget < 32)
+    if (ld_gpu(&A.st->wl_long) || ld_gpu(&A.st->wl_short)) {
       cand_sweep(A, cfg, sm.cand);
       grid_barrier(A.st);
     }

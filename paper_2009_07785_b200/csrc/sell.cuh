@@ -141,7 +141,9 @@ __device__ __forceinline__ double column_q_inline(double lo, double up, bool int
 template <class RA>
 __device__ __forceinline__ void ld_col(const RA& A, int32_t c, uint64_t pol, bool frac_any,
                                        const DevCfg& cfg, double& lo, double& up, double& q) {
-  if constexpr (gather16_v<RA>) {
+  if constexpr (coherent_v<RA>) {
+    ld_snap_coh(A.snap + (c & 0x7fffffff), lo, up, q);
+  } else if constexpr (gather16_v<RA>) {
     double2 b;
     asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
                  : "=d"(b.x), "=d"(b.y)

@@ -12,10 +12,18 @@ namespace pgb {
 
 // length class of every row: exact length for short rows, one class for the
 // rows that are split into segments; plus the identity permutation
-__global__ void k_row_keys(const int32_t* __restrict__ rp, int m, int short_max,
-                           uint8_t* __restrict__ key, int32_t* __restrict__ idx) {
+// (and the row_ptr check: non-decreasing, inside [0, nnz]; a violation is
+// flagged and session setup fails with PG_EINVAL before any entry is read)
+__global__ void k_row_keys(const int32_t* __restrict__ rp, int m, int64_t nnz, int short_max,
+                           uint8_t* __restrict__ key, int32_t* __restrict__ idx,
+                           int32_t* __restrict__ bad) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < m; i += gridDim.x * blockDim.x) {
-    const int L = rp[i + 1] - rp[i];
+    const int a = rp[i], b = rp[i + 1];
+    int L = b - a;
+    if (a < 0 || b < a || (int64_t)b > nnz) {
+      *bad = 1;
+      L = 0;
+    }
     key[i] = (uint8_t)(L <= short_max ? L : short_max + 1);
     idx[i] = i;
   }

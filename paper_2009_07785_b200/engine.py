@@ -173,6 +173,21 @@ class Session:
         abi.check(_lib().pg_session_propagate(self._h, lp, up_, C.byref(r)), "pg_session_propagate")
         return result_from_c(r, lo, up, prc)
 
+    def round(self, snap: RoundSnapshot) -> RoundOutcome:
+        """propagate_round_parallel on the resident matrix (pg_session_round)."""
+        n = self.instance.num_cols()
+        lb_in = np.ascontiguousarray(snap.bounds_in.lower, dtype=np.float64)
+        ub_in = np.ascontiguousarray(snap.bounds_in.upper, dtype=np.float64)
+        lo = np.empty(n)
+        up = np.empty(n)
+        ch, inf, cnt = C.c_int32(), C.c_int32(), C.c_int64()
+        abi.check(_lib().pg_session_round(self._h, abi.ptr(lb_in, C.c_double),
+                                          abi.ptr(ub_in, C.c_double), abi.ptr(lo, C.c_double),
+                                          abi.ptr(up, C.c_double), C.byref(ch), C.byref(inf),
+                                          C.byref(cnt)), "pg_session_round")
+        snap.bounds_out = VariableBounds(lo, up)
+        return RoundOutcome(bool(ch.value), bool(inf.value), int(cnt.value))
+
     def run(self, download=False) -> PropagationResult:
         """Solve from the device-resident start bounds (nothing crosses PCIe
         unless download=True)."""

@@ -4,7 +4,7 @@ Everything here is produced by the REFERENCE itself -- its sources compiled
 unmodified into oracle/_ref/libpropgate_ref.so by oracle/build_ref.sh -- and
 committed as small .npz fixtures, so tests/test_oracle.py can check the C
 restatement (oracle/liboracle.so) and the generator restatement
-(paper_2009_07785_b200/libpgen.so) without /root/reference present.
+(instances/libpgen.so) without /root/reference present.
 
   propcore.npz    compute_row_activities / residual_activities /
                   compute_bound_candidates / classify_constraint / tighten on
@@ -40,7 +40,7 @@ sys.path.insert(0, ROOT)
 
 from oracle import oracle as O  # noqa: E402
 from paper_2009_07785_b200 import abi  # noqa: E402
-from paper_2009_07785_b200 import generators as G  # noqa: E402
+from instances import generators as G  # noqa: E402
 from paper_2009_07785_b200.model import EngineConfig, ProblemInstance  # noqa: E402
 
 FIXTURE_DIR = "/root/reference/proj/tests/fixtures"

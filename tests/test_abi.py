@@ -10,7 +10,7 @@ import subprocess
 import pytest
 
 from paper_2009_07785_b200 import abi
-from paper_2009_07785_b200 import generators as G
+from instances import generators as G
 from paper_2009_07785_b200.model import EngineConfig
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

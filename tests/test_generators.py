@@ -5,7 +5,7 @@ import sys
 
 import numpy as np
 
-from paper_2009_07785_b200 import generators as G
+from instances import generators as G
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -74,7 +74,7 @@ def test_nodes_branch_on_integer_columns():
 
 
 def test_thread_count_independent():
-    code = ("import sys; sys.path.insert(0, %r); from paper_2009_07785_b200 import generators as G;"
+    code = ("import sys; sys.path.insert(0, %r); from instances import generators as G;"
             "import hashlib, numpy as np; i = G.gen_powerlaw(20000, 20000, 7);"
             "print(hashlib.sha256(np.ascontiguousarray(i.matrix.col_idx).tobytes() + "
             "i.matrix.values.tobytes() + i.rhs.tobytes()).hexdigest())" % ROOT)

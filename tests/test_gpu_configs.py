@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from paper_2009_07785_b200 import generators as G
+from instances import generators as G
 from paper_2009_07785_b200.engine import Session, propagate_gpu
 from paper_2009_07785_b200.model import EngineConfig, LoopMode, PropagationStatus
 from paper_2009_07785_b200.multi import RowShardedSession, propagate_nodes_sharded

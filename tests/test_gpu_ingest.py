@@ -50,7 +50,7 @@ def test_triplets_large_vs_oracle(m, n, k, ncol):
 def test_triplets_then_propagate():
     """ingest -> propagate: the device-built CSR drives the engine like the
     reference's own csr_from_triplets output"""
-    from paper_2009_07785_b200 import generators as G
+    from instances import generators as G
     from paper_2009_07785_b200.engine import propagate_gpu
     from paper_2009_07785_b200.model import EngineConfig, ProblemInstance
     inst = G.config_instance("c1")

@@ -14,7 +14,7 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from paper_2009_07785_b200 import generators as G
+from instances import generators as G
 from paper_2009_07785_b200.engine import (RoundSnapshot, Session, partition_row_blocks,
                                           propagate_gpu, propagate_round_gpu)
 from paper_2009_07785_b200.model import (EngineConfig, LoopMode, ProblemInstance,
@@ -227,6 +227,62 @@ def test_round_api_matches_oracle_round():
         lo, up = snap.bounds_out.lower, snap.bounds_out.upper
 
 
+def test_session_round_matches_oracle_round():
+    """pg_session_round: the one-round API on a resident session (matrix set
+    up once), chained like a branch-and-bound caller would."""
+    inst = G.gen_powerlaw(20000, 20000, 5, cap=3000)
+    lo, up = inst.bounds.lower.copy(), inst.bounds.upper.copy()
+    for cfg in (EngineConfig(row_check=True), EngineConfig(row_check=False, worklist=True)):
+        lo, up = inst.bounds.lower.copy(), inst.bounds.upper.copy()
+        with Session(inst, cfg) as s:
+            for _ in range(4):
+                snap = RoundSnapshot(VariableBounds(lo, up))
+                out = s.round(snap)
+                ref = O.propagate_round_parallel(inst, PAR, lo, up)
+                assert out.changes == ref["changes"] and out.infeasible == ref["infeasible"]
+                assert np.array_equal(O.canon(snap.bounds_out.lower), O.canon(ref["lower"]))
+                assert np.array_equal(O.canon(snap.bounds_out.upper), O.canon(ref["upper"]))
+                lo, up = snap.bounds_out.lower, snap.bounds_out.upper
+            # the session still solves normally afterwards (row check restored)
+            assert_bit_exact(s.propagate(), O.propagate_parallel(inst, cfg), "after rounds")
+
+
+@pytest.mark.parametrize("loop", [LoopMode.Graph, LoopMode.Host])
+def test_small_budget_short_split_rows(loop):
+    """nnz_budget < 32: split rows of nnz_budget < len <= 32 entries go on the
+    short phase-2 queue; the persistent loop (Graph mode, small instance) and
+    the per-phase kernels (Host mode) must both drain it."""
+    inst = G.gen_random(3000, 2500, 21, mean_row_nnz=24.0, integral_fraction=0.5)
+    for budget, vt in ((16, 8), (20, 4), (8, 8)):
+        cfg = EngineConfig(row_check=False, nnz_budget=budget, vector_threshold=vt, loop_mode=loop)
+        assert_bit_exact(propagate_gpu(inst, cfg), O.propagate_parallel(inst, cfg),
+                         f"budget {budget}")
+
+
+def test_bad_indices_rejected_without_poisoning_the_context():
+    """Out-of-range col_idx / non-monotone row_ptr: PG_EINVAL, not a device
+    fault (the reference has undefined behaviour here); later solves in the
+    same process still work."""
+    from paper_2009_07785_b200.abi import EngineError
+    inst = G.gen_random(500, 400, 3, mean_row_nnz=6.0)
+    bad = G.gen_random(500, 400, 3, mean_row_nnz=6.0)
+    bad.matrix.col_idx[7] = 400 + 12345
+    with pytest.raises(EngineError) as e:
+        propagate_gpu(bad, PAR)
+    assert "col_idx" in str(e.value)
+    bad2 = G.gen_random(500, 400, 3, mean_row_nnz=6.0)
+    bad2.matrix.col_idx[3] = -5
+    with pytest.raises(EngineError):
+        propagate_gpu(bad2, EngineConfig(row_check=False, worklist=True))
+    bad3 = G.gen_random(500, 400, 3, mean_row_nnz=6.0)
+    rp = bad3.matrix.row_ptr
+    rp[10], rp[11] = rp[11], rp[10] - 1
+    with pytest.raises(EngineError) as e:
+        propagate_gpu(bad3, PAR)
+    assert "row_ptr" in str(e.value)
+    assert_bit_exact(propagate_gpu(inst, PAR), O.propagate_parallel(inst, PAR), "after bad input")
+
+
 def test_partition_matches_reference_partitioner():
     inst = G.gen_random(3000, 3000, 11, mean_row_nnz=40.0)
     starts, kinds = partition_row_blocks(inst, PAR)
@@ -372,7 +428,7 @@ import sys
 sys.path.insert(0, {root!r})
 import numpy as np
 from oracle import oracle as O
-from paper_2009_07785_b200 import generators as G
+from instances import generators as G
 from paper_2009_07785_b200.engine import propagate_gpu
 from paper_2009_07785_b200.model import EngineConfig
 PAR = EngineConfig(row_check=False)

@@ -18,7 +18,7 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from oracle import oracle as O
-from paper_2009_07785_b200 import generators as G
+from instances import generators as G
 from paper_2009_07785_b200.model import EngineConfig, PropagationStatus
 from paper_2009_07785_b200.multi import node_shards, row_shards, shard_instance
 

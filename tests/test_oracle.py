@@ -14,7 +14,7 @@ import pytest
 
 from oracle import oracle as O
 from paper_2009_07785_b200 import abi
-from paper_2009_07785_b200 import generators as G
+from instances import generators as G
 from paper_2009_07785_b200.model import EngineConfig, ProblemInstance, PropagationStatus
 
 GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")

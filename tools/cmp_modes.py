@@ -5,7 +5,7 @@ import sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
-from paper_2009_07785_b200 import generators as G  # noqa: E402
+from instances import generators as G  # noqa: E402
 from paper_2009_07785_b200.engine import Session  # noqa: E402
 from paper_2009_07785_b200.model import EngineConfig  # noqa: E402
 

@@ -3,7 +3,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 os.environ["PG_TIMING"] = "1"
 import torch  # noqa
 from bench import pinned_copy  # noqa
-from paper_2009_07785_b200 import generators as G  # noqa
+from instances import generators as G  # noqa
 from paper_2009_07785_b200.engine import propagate_gpu  # noqa
 from paper_2009_07785_b200.model import EngineConfig  # noqa
 inst = pinned_copy(G.config_instance(sys.argv[1] if len(sys.argv) > 1 else "c2"))

@@ -4,7 +4,8 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2009_07785_b200 import abi, generators as G  # noqa: E402
+from paper_2009_07785_b200 import abi
+from instances import generators as G  # noqa: E402
 from paper_2009_07785_b200.model import EngineConfig  # noqa: E402
 
 inst = G.config_instance(sys.argv[1] if len(sys.argv) > 1 else "c2")
