@@ -253,7 +253,10 @@ int pg_multi_propagate(const pg_problem* prob, const pg_config* cfg, int32_t ngp
  * those rows), short rows, short-row entries, segment entries, chains,
  * sliced-ELL elements (entries + padding), split rows (> nnz_budget),
  * persistent loop (1: the whole solve is one cooperative kernel), rounds of
- * the last solve that used the sparse delta exchange. */
+ * the last solve that used the sparse delta exchange, host round trips of
+ * the last row-sharded solve (one per graph of unrolled rounds), delta
+ * rounds held by a capacity overflow and resumed with the dense all-reduce,
+ * rounds per unrolled graph, graphs of delta rounds launched. */
 int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info);
 
 /* Thread-local message of the last failed call on this thread. */

@@ -344,10 +344,27 @@ struct pg_session {
   int* d_dcnt_all = nullptr;
   int* h_dcnt = nullptr;
   int32_t delta_cap = 0, delta_rounds = 0;
+  // row shards in graph mode: graphs of kShardRounds unrolled rounds -- one
+  // with the dense all-reduce, one per delta capacity tier (fixed-size
+  // all-gathers) -- launched by the host, which reads the round state once
+  // per graph (engine.cu run_shard_solve); no NCCL call sits inside a
+  // conditional node
+  static constexpr int kMaxTiers = 3;
+  int shard_rounds = 4;
+  bool unrolled = false;             // capturing / running the unrolled graphs
+  cudaGraphExec_t shard_dense = nullptr;
+  cudaGraphExec_t shard_delta[kMaxTiers] = {nullptr, nullptr, nullptr};
+  int32_t delta_caps[kMaxTiers] = {0, 0, 0};
+  int ntiers = 0;
+  int64_t host_syncs = 0;            // host round trips of the last solve
+  int64_t held_rounds = 0;           // delta rounds held by an overflow (resumed densely)
+  int64_t delta_graphs = 0;          // graphs of delta rounds launched (the rest were dense)
   bool delta_mode() const { return comm && (cfg.flags & PG_FLAG_DELTA_EXCHANGE); }
   // branch-and-bound: the root fixpoint and the next solve's start control
   NodeCtl* d_ctl = nullptr;
   double* d_root_lo = nullptr;
+  double* d_keep_lo = nullptr;  // pg_session_round: the session's start bounds, kept aside
+  double* d_keep_up = nullptr;
   double* d_root_up = nullptr;
   bool has_root = false;
 
@@ -356,9 +373,10 @@ struct pg_session {
     t_alloc_stream = stream;
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
+    destroy_shard_graphs();
 
     if (comm) g_nccl.comm_destroy(comm);
-    for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up, (void*)d_delta,
+    for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up, (void*)d_keep_lo, (void*)d_keep_up, (void*)d_delta,
                     (void*)d_delta_all, (void*)d_dcnt, (void*)d_dcnt_all})
       dfree(p);
     if (h_dcnt) cudaFreeHost(h_dcnt);
@@ -432,7 +450,10 @@ struct pg_session {
   // One round: phase 1 (k_sell), phase 2 (k_cand), [row shards: all-reduce],
   // commit + decision (k_commit), [worklist: k_mark].  k1_begin/k1_end
   // bracket the two compute phases (bench.py's roofline timing).
-  void enqueue_round(bool use_graph, cudaEvent_t k1_begin = nullptr, cudaEvent_t k1_end = nullptr) {
+  // tier >= 0: an unrolled row-shard round exchanging sparse deltas at the
+  // fixed capacity delta_caps[tier] (held on overflow, see k_delta_apply)
+  void enqueue_round(bool use_graph, cudaEvent_t k1_begin = nullptr, cudaEvent_t k1_end = nullptr,
+                     int tier = -1) {
     const bool rowcheck = (cfg.flags & PG_FLAG_ROWCHECK) != 0;
     const RoundArgs A = round_args();
     if (k1_begin) PG_CUDA(cudaEventRecord(k1_begin, stream));
@@ -461,7 +482,21 @@ struct pg_session {
     }
     if (k1_end) PG_CUDA(cudaEventRecord(k1_end, stream));
     bool dense_exchange = comm != nullptr;
-    if (comm && delta_mode() && !use_graph) {
+    if (comm && tier >= 0) {
+      const int cap = delta_caps[tier];
+      PG_CUDA(cudaMemsetAsync(d_dcnt, 0, 2 * sizeof(int), stream));
+      k_delta_compact<<<grid_for(n, 256, 8), 256, 0, stream>>>(d_bnd, d_key_out, n, d_st, d_delta,
+                                                                cap, d_dcnt);
+      PG_CUDA(cudaGetLastError());
+      int rc = g_nccl.all_gather_fn(d_dcnt, d_dcnt_all, 2, kNcclInt32, comm, stream);
+      if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllGather: ") + g_nccl.error(rc)};
+      rc = g_nccl.all_gather_fn(d_delta, d_delta_all, 3 * (size_t)cap, kNcclInt64, comm, stream);
+      if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllGather: ") + g_nccl.error(rc)};
+      k_delta_apply<<<grid_for(cap, 256, 8), 256, 0, stream>>>(d_delta_all, d_dcnt_all, world, cap,
+                                                               d_key_out, d_st, 1);
+      PG_CUDA(cudaGetLastError());
+      dense_exchange = false;
+    } else if (comm && delta_mode() && !use_graph && !unrolled) {
       // sparse delta exchange: all-gather the
       // counts; when every rank changed at most delta_cap columns, all-gather
       // the (column, keys) items and max-merge them, else the dense all-reduce.
@@ -485,7 +520,7 @@ struct pg_session {
           if (rc != 0) throw Error{PG_ENCCL, std::string("ncclAllGather: ") + g_nccl.error(rc)};
         }
         k_delta_apply<<<grid_for(std::max(maxc, 1), 256, 8), 256, 0, stream>>>(
-            d_delta_all, d_dcnt_all, world, maxc, d_key_out, d_st);
+            d_delta_all, d_dcnt_all, world, maxc, d_key_out, d_st, 0);
         PG_CUDA(cudaGetLastError());
       }
     }
@@ -503,8 +538,8 @@ struct pg_session {
     static const int commit_per_sm = getenv("PG_COMMIT_PER_SM") ? atoi(getenv("PG_COMMIT_PER_SM")) : 2;
     static const int list_per_sm = getenv("PG_LIST_PER_SM") ? atoi(getenv("PG_LIST_PER_SM")) : 2;
     k_commit<<<grid_for(n, kCommitThreads, commit_per_sm), kCommitThreads, 0, stream>>>(
-        d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond, use_graph ? 1 : 0,
-        comm ? 0 : 1);
+        d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond,
+        use_graph && !unrolled ? 1 : 0, comm ? 0 : 1);
     if (dirty.enabled && !comm)
       k_commit_list<<<num_sms * list_per_sm, kCommitThreads, 0, stream>>>(
           d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, touch, cond, use_graph ? 1 : 0);
@@ -597,7 +632,89 @@ struct pg_session {
                                  (const int32_t*)d_split, nsplit));
   }
 
+  // row shards: the unrolled round graphs (see shard_dense)
+  void build_shard_graphs() {
+    destroy_shard_graphs();
+    if (const char* e = getenv("PG_SHARD_ROUNDS")) shard_rounds = std::max(1, atoi(e));
+    unrolled = true;
+    struct Off {
+      bool* f;
+      ~Off() { *f = false; }
+    } off{&unrolled};
+    auto capture = [&](int tier) {
+      cudaGraph_t g = nullptr;
+      PG_CUDA(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal));
+      for (int r = 0; r < shard_rounds; ++r) enqueue_round(false, nullptr, nullptr, tier);
+      PG_CUDA(cudaStreamEndCapture(stream, &g));
+      cudaGraphExec_t x = nullptr;
+      const cudaError_t e = cudaGraphInstantiate(&x, g, 0);
+      cudaGraphDestroy(g);
+      PG_CUDA(e);
+      return x;
+    };
+    shard_dense = capture(-1);
+    if (delta_mode())
+      for (int t = 0; t < ntiers; ++t) shard_delta[t] = capture(t);
+  }
+  void destroy_shard_graphs() {
+    if (shard_dense) cudaGraphExecDestroy(shard_dense);
+    shard_dense = nullptr;
+    for (auto& x : shard_delta) {
+      if (x) cudaGraphExecDestroy(x);
+      x = nullptr;
+    }
+  }
+
+  // A row-sharded solve in graph mode: reset, then graphs of shard_rounds
+  // rounds until the (identical on every rank) state says done.  The first
+  // rounds exchange densely; once a round changed few enough sides, the
+  // smallest delta tier whose capacity covers that count (a rank's changed
+  // columns never exceed the round's changed sides, and the next round's
+  // rarely exceed this one's); a held round (overflow) is resumed densely.
+  // Every rank reads the same merged state, so all pick the same graph.
+  void run_shard_solve(bool check_crossed) {
+    host_syncs = 0;
+    held_rounds = 0;
+    delta_graphs = 0;
+    // test knob: always the given delta tier after the first graph (forces
+    // overflows, i.e. held and resumed rounds)
+    static const int force_tier = getenv("PG_SHARD_TIER") ? atoi(getenv("PG_SHARD_TIER")) : -1;
+    enqueue_reset(false, check_crossed);
+    h_st->done = 0;
+    h_st->stall = 0;
+    bool first = true;
+    for (;;) {
+      cudaGraphExec_t g = shard_dense;
+      if (h_st->stall) {
+        ++held_rounds;
+        k_shard_resume<<<1, 32, 0, stream>>>(d_st);
+        PG_CUDA(cudaGetLastError());
+      } else if (!first && delta_mode() && force_tier >= 0 && force_tier < ntiers) {
+        g = shard_delta[force_tier];
+      } else if (!first && delta_mode()) {
+        const long long want = h_st->last_changes;
+        for (int t = ntiers - 1; t >= 0; --t)
+          if (shard_delta[t] && want <= delta_caps[t]) {
+            g = shard_delta[t];
+            break;
+          }
+      }
+      PG_CUDA(cudaGraphLaunch(g, stream));
+      delta_graphs += g != shard_dense;
+      PG_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(DevState), cudaMemcpyDeviceToHost, stream));
+      PG_CUDA(cudaStreamSynchronize(stream));
+      ++host_syncs;
+      first = false;
+      if (h_st->done) break;
+    }
+    delta_rounds = h_st->delta_rounds;
+  }
+
   void build_graph() {
+    if (comm) {
+      build_shard_graphs();
+      return;
+    }
     PG_CUDA(cudaGraphCreate(&graph, 0));
     if (use_persistent()) {
       PG_CUDA(cudaStreamBeginCaptureToGraph(stream, graph, nullptr, nullptr, 0,
@@ -653,7 +770,11 @@ struct pg_session {
   int64_t run_solve(bool check_crossed = true, pg_result* res = nullptr) {
     bounds_done = false;
     delta_rounds = 0;
-    if (cfg.loop_mode == PG_LOOP_GRAPH && check_crossed && !delta_mode()) {
+    if (comm && cfg.loop_mode == PG_LOOP_GRAPH) {
+      PG_CUDA(cudaEventRecord(ev0, stream));
+      run_shard_solve(check_crossed);
+      PG_CUDA(cudaEventRecord(ev1, stream));
+    } else if (cfg.loop_mode == PG_LOOP_GRAPH && check_crossed && !delta_mode()) {
       PG_CUDA(cudaEventRecord(ev0, stream));
       PG_CUDA(cudaGraphLaunch(exec, stream));
       PG_CUDA(cudaEventRecord(ev1, stream));
@@ -1410,6 +1531,14 @@ int pg_session_round(pg_session* s, const double* lb_in, const double* ub_in, do
   }
   return guarded([&] {
     PG_CUDA(cudaSetDevice(s->dev));
+    // the caller's snapshot replaces the start bounds for this round only:
+    // later pg_session_run / propagate calls start from the session's own
+    if (!s->d_keep_lo) {
+      s->d_keep_lo = dalloc<double>(s->n);
+      s->d_keep_up = dalloc<double>(s->n);
+    }
+    PG_CUDA(cudaMemcpyAsync(s->d_keep_lo, s->d_lo0, sizeof(double) * s->n, cudaMemcpyDeviceToDevice, s->stream));
+    PG_CUDA(cudaMemcpyAsync(s->d_keep_up, s->d_up0, sizeof(double) * s->n, cudaMemcpyDeviceToDevice, s->stream));
     s->upload_bounds(lb_in, ub_in);
     const pg_config saved = s->cfg;
     const DevCfg dsaved = s->dcfg;
@@ -1438,6 +1567,8 @@ int pg_session_round(pg_session* s, const double* lb_in, const double* ub_in, do
                             s->stream));
     PG_CUDA(cudaMemcpyAsync(ub_out, s->d_up_res, sizeof(double) * s->n, cudaMemcpyDeviceToHost,
                             s->stream));
+    PG_CUDA(cudaMemcpyAsync(s->d_lo0, s->d_keep_lo, sizeof(double) * s->n, cudaMemcpyDeviceToDevice, s->stream));
+    PG_CUDA(cudaMemcpyAsync(s->d_up0, s->d_keep_up, sizeof(double) * s->n, cudaMemcpyDeviceToDevice, s->stream));
     PG_CUDA(cudaStreamSynchronize(s->stream));
     s->check_input();
     *changes = ch;
@@ -1974,6 +2105,12 @@ int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank, i
     // a round whose every rank changed at most n/16 columns goes sparse
     // (C5 changes <= 253k of 10M sides after round 1)
     s->delta_cap = std::max(1024, s->n / 16);
+    // unrolled graphs all-gather a fixed capacity: tiers n/16, n/64, n/256
+    s->ntiers = 0;
+    for (int div : {16, 64, 256}) {
+      const int c = std::max(1024, s->n / div);
+      if (s->ntiers == 0 || c < s->delta_caps[s->ntiers - 1]) s->delta_caps[s->ntiers++] = c;
+    }
     s->d_delta = dalloc<DeltaItem>(s->delta_cap);
     s->d_delta_all = dalloc<DeltaItem>((size_t)s->delta_cap * world);
     s->d_dcnt = dalloc<int>(2);
@@ -2105,7 +2242,8 @@ int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info) {
   }
   const int64_t v[] = {s->m, s->n, s->nnz, s->nslices, s->nsrow, s->nseg,
                        s->short_rows, s->short_nnz, s->seg_nnz, s->nunits, s->sell_elems,
-                       s->nsplit, s->use_persistent() ? 1 : 0, s->delta_rounds};
+                       s->nsplit, s->use_persistent() ? 1 : 0, s->delta_rounds,
+                       s->host_syncs, s->held_rounds, s->shard_rounds, s->delta_graphs};
   for (int i = 0; i < n_info && i < (int)(sizeof(v) / sizeof(v[0])); ++i) info[i] = v[i];
   return PG_OK;
 }

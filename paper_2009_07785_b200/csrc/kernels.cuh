@@ -59,7 +59,22 @@ struct DevState {
   uint32_t bar_count;                // grid barrier of the persistent round loop (loop.cuh)
   uint32_t bar_gen;
   int32_t bad_input;                 // a col_idx outside [0, n) (set at session setup, sticky)
+  // row shards, unrolled graphs (engine.cu build_shard_graphs)
+  int32_t stall;                     // a delta exchange overflowed its capacity: the round is
+                                     // held (not committed) until the host resumes it densely
+  int32_t resume;                    // the next round resumes a held one: exchange + commit only
+  int32_t delta_rounds;              // rounds merged by the sparse delta exchange (this solve)
 };
+
+// Row shards run graphs of R unrolled rounds (no conditional nodes around
+// NCCL calls); a round's kernels return at once once the solve is decided
+// (done) or held (stall), and the compute phases also in a resumed round.
+__device__ __forceinline__ bool round_off(DevState* st) {
+  return (ld_gpu(&st->done) | ld_gpu(&st->stall)) != 0;
+}
+__device__ __forceinline__ bool compute_off(DevState* st) {
+  return (ld_gpu(&st->done) | ld_gpu(&st->stall) | ld_gpu(&st->resume)) != 0;
+}
 
 // Device-side worklist (PG_FLAG_WORKLIST): a round only
 // visits work items containing a row with a variable changed in the previous
@@ -597,6 +612,7 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
       st->nunit[cb] = 0;
       st->ntouch = 0;
       st->sparse_commit = kList;
+      st->resume = 0;
       __threadfence();
       if (use_graph) cudaGraphSetConditional(cond, status >= 0 ? 0u : 1u);
     }
@@ -609,6 +625,7 @@ __global__ void __launch_bounds__(kCommitThreads)
              const Dirty D, cudaGraphConditionalHandle cond, int use_graph, int allow_list) {
   // a worklist round of a single session is committed by k_commit_list; with
   // row shards every column may have moved on another rank: always in full
+  if (round_off(st)) return;
   if (allow_list && ld_gpu(&st->sparse_round)) return;
   commit_body(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph);
 }
@@ -619,7 +636,7 @@ __global__ void __launch_bounds__(kCommitThreads)
                   const longlong2* __restrict__ key_out, int n, DevState* __restrict__ st,
                   long long* __restrict__ per_round, const DevCfg cfg, const Dirty D, const Touch T,
                   cudaGraphConditionalHandle cond, int use_graph) {
-  if (!ld_gpu(&st->sparse_round)) return;
+  if (round_off(st) || !ld_gpu(&st->sparse_round)) return;
   commit_body<true>(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph, &T);
 }
 
@@ -682,6 +699,9 @@ __global__ void __launch_bounds__(kCommitThreads)
       st->frac_any = atomicAdd(&st->frac_tmp, 0);
       st->frac_tmp = 0;
       st->ticket_reset = 0;
+      st->stall = 0;
+      st->resume = 0;
+      st->delta_rounds = 0;
       __threadfence();
       if (use_graph) cudaGraphSetConditional(cond, cr ? 0u : 1u);
     }
@@ -690,8 +710,8 @@ __global__ void __launch_bounds__(kCommitThreads)
 
 // Row-sharded rounds: this rank's infeasibility into the slot that rides the
 // bound all-reduce (max over {lb key, -ub key, flag}).
-__global__ void k_flag_to_slot(const DevState* __restrict__ st, longlong2* __restrict__ slot) {
-  if (threadIdx.x == 0) slot->x = ld_gpu(&st->infeasible) ? 1 : 0;
+__global__ void k_flag_to_slot(DevState* __restrict__ st, longlong2* __restrict__ slot) {
+  if (threadIdx.x == 0 && !round_off(st)) slot->x = ld_gpu(&st->infeasible) ? 1 : 0;
 }
 
 // ---- row shards: sparse delta exchange ---------------
@@ -706,9 +726,10 @@ struct DeltaItem {
 // cnt[1] = its infeasibility flag; cnt zeroed before the launch
 __global__ void __launch_bounds__(256)
     k_delta_compact(const double2* __restrict__ bnd, const longlong2* __restrict__ key_out, int n,
-                    const DevState* __restrict__ st, DeltaItem* __restrict__ out, int cap,
+                    DevState* __restrict__ st, DeltaItem* __restrict__ out, int cap,
                     int* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
+  if (round_off(st)) return;  // counts stay zero (memset before the launch)
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[1] = ld_gpu(&st->infeasible) ? 1 : 0;
   for (int j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; j0 < n; j0 += gridDim.x * blockDim.x) {
     const int j = j0 + lane;
@@ -729,10 +750,25 @@ __global__ void __launch_bounds__(256)
 }
 
 // every rank's items (rank r: all[r * stride .. + cnt_all[2r]]) merged by max
+// held_ok: an overflow (some rank changed more than `stride` columns; the
+// items were all-gathered at a fixed capacity) holds the round instead of
+// applying a partial set -- the host resumes it with the dense all-reduce
+// (unrolled graphs); without it the caller sized the gather to the counts
 __global__ void __launch_bounds__(256)
     k_delta_apply(const DeltaItem* __restrict__ all, const int* __restrict__ cnt_all, int world,
-                  int stride, longlong2* __restrict__ key_out, DevState* __restrict__ st) {
+                  int stride, longlong2* __restrict__ key_out, DevState* __restrict__ st,
+                  int held_ok) {
+  if (round_off(st)) return;
+  if (held_ok) {
+    int maxc = 0;
+    for (int r = 0; r < world; ++r) maxc = max(maxc, cnt_all[2 * r]);
+    if (maxc > stride) {
+      if (blockIdx.x == 0 && threadIdx.x == 0) st->stall = 1;
+      return;
+    }
+  }
   if (blockIdx.x == 0 && threadIdx.x < world && cnt_all[2 * threadIdx.x + 1]) st->infeasible = 1;
+  if (blockIdx.x == 0 && threadIdx.x == 0) st->delta_rounds += 1;
   for (int r = 0; r < world; ++r) {
     const int c = min(cnt_all[2 * r], stride);
     const DeltaItem* a = all + (size_t)r * stride;
@@ -742,6 +778,15 @@ __global__ void __launch_bounds__(256)
       red_max(k, d.lo);
       red_max(k + 1, d.nup);
     }
+  }
+}
+
+// the host resumes a held round (unrolled row-shard graphs): the next round
+// skips its compute phases and merges the held local results densely
+__global__ void k_shard_resume(DevState* __restrict__ st) {
+  if (threadIdx.x == 0) {
+    st->stall = 0;
+    st->resume = 1;
   }
 }
 
@@ -897,7 +942,7 @@ __global__ void k_apply_node(double* __restrict__ lo0, double* __restrict__ up0,
 // column changed in round r (one warp per changed column).
 __device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__ st) {
   const int r = ld_gpu(&st->round);
-  if (!D.enabled || ld_gpu(&st->done) || ld_gpu(&st->full)) return;
+  if (!D.enabled || round_off(st) || ld_gpu(&st->full)) return;
   const int cb = r & 1, nb = (r + 1) & 1;
   const int nchg = ld_gpu(&st->nchg[cb]);
   uint8_t* flag = D.row_flag + (size_t)nb * D.ms;

@@ -75,12 +75,14 @@ class RowShardedSession:
     """This rank's row shard of one instance, merged over NCCL every round."""
 
     def __init__(self, inst: ProblemInstance, cfg: EngineConfig, rank: int, world: int,
-                 group=None, uid: bytes | None = None, force_comm: bool = False):
+                 group=None, uid: bytes | None = None, force_comm: bool = False,
+                 shard: ProblemInstance | None = None):
         """world == 1 is the plain single-GPU engine (nothing to exchange)
-        unless force_comm attaches a one-rank communicator (tests)."""
+        unless force_comm attaches a one-rank communicator (tests).  `shard`:
+        this rank's rows already cut (e.g. in pinned host memory)."""
         self.rank, self.world = rank, world
         self.r0, self.r1 = row_shards(inst.matrix.row_ptr, world)[rank]
-        self.shard = shard_instance(inst, self.r0, self.r1)
+        self.shard = shard if shard is not None else shard_instance(inst, self.r0, self.r1)
         self.session = Session(self.shard, cfg)
         self.comm = world > 1 or force_comm
         if not self.comm:

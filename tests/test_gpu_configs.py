@@ -98,12 +98,51 @@ def test_row_sharded_delta_exchange_world1(worklist):
             assert_bit_exact(r, O.propagate_parallel(inst, PAR), inst.name)
             info = rs.session.info()
             assert 0 < info["delta_rounds"] <= r.rounds_executed, info
+            # graphs of unrolled rounds: one host round trip per graph, not per round
+            R = info["shard_rounds"]
+            assert info["host_syncs"] <= -(-r.rounds_executed // R) + info["held_rounds"], info
         finally:
             rs.close()
     bad = G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003, infeasible=True)
     rs = RowShardedSession(bad, EngineConfig(delta_exchange=True), rank=0, world=1, force_comm=True)
     assert rs.propagate().status == PropagationStatus.Infeasible
     rs.close()
+
+
+def test_row_sharded_held_rounds_resume_bit_exact(monkeypatch):
+    """Unrolled row-shard graphs with the smallest delta tier forced: rounds
+    whose changes overflow the fixed all-gather capacity are held (not
+    committed) and resumed with the dense all-reduce -- still bit-exact, and
+    the decision stays one host round trip per graph."""
+    try:
+        from paper_2009_07785_b200.multi import nccl_unique_id
+        nccl_unique_id()
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    import subprocess, sys, os
+    code = (
+        "import numpy as np\n"
+        "from oracle import oracle as O\n"
+        "from instances import generators as G\n"
+        "from paper_2009_07785_b200.model import EngineConfig\n"
+        "from paper_2009_07785_b200.multi import RowShardedSession\n"
+        "inst = G.gen_setpart(20000, 100000, 50, f_fixed=0.2, seed=5003)\n"
+        "PAR = EngineConfig(row_check=False)\n"
+        "for wl in (False, True):\n"
+        "    rs = RowShardedSession(inst, EngineConfig(row_check=False, worklist=wl, delta_exchange=True), 0, 1, force_comm=True)\n"
+        "    r = rs.propagate(); ref = O.propagate_parallel(inst, PAR); info = rs.session.info()\n"
+        "    assert r.status == ref.status and r.rounds_executed == ref.rounds_executed, (r.rounds_executed, ref.rounds_executed)\n"
+        "    assert r.per_round_changes == ref.per_round_changes\n"
+        "    assert np.array_equal(O.canon(r.bounds.lower), O.canon(ref.bounds.lower))\n"
+        "    assert np.array_equal(O.canon(r.bounds.upper), O.canon(ref.bounds.upper))\n"
+        "    assert info['held_rounds'] > 0, info\n"
+        "    rs.close()\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PG_SHARD_TIER="2", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stdout + out.stderr
 
 
 @pytest.mark.slow
