@@ -43,4 +43,17 @@ if [ -f "$REPO/paper_2009_07785_b200/libpropgate_b200.so" ]; then
   $CXX -pthread -o "$OUT/gpu_dropin" $LIBOBJS "$OBJ/gpu_dropin.o" \
       -L"$REPO/paper_2009_07785_b200" -lpropgate_b200 -Wl,-rpath,'$ORIGIN/../../paper_2009_07785_b200'
 fi
+# the reference's bench harness with EngineId::Gpu:
+# patched COPIES of harness.hpp / harness.cpp (oracle/patch_harness.py) +
+# tests/cpp/harness_gpu.cpp, linked with the GPU engine
+if [ -f "$REPO/paper_2009_07785_b200/libpropgate_b200.so" ]; then
+  PATCHED="$OUT/patched"
+  python3 "$HERE/patch_harness.py" "$REF" "$PATCHED"
+  PFLAGS="-O2 -std=c++20 -pthread -I$PATCHED -I$REF/core/include -I$REF/core/src -I$JSON_INC -I$REPO/include"
+  $CXX $PFLAGS -c "$PATCHED/harness.cpp" -o "$OBJ/harness_gpu_patched.o"
+  $CXX $PFLAGS -c "$REPO/tests/cpp/harness_gpu.cpp" -o "$OBJ/harness_gpu_main.o"
+  $CXX -pthread -o "$OUT/harness_gpu" "$OBJ/model.o" "$OBJ/generators.o" "$OBJ/seq_engine.o" \
+      "$OBJ/par_engine.o" "$OBJ/mps.o" "$OBJ/harness_gpu_patched.o" "$OBJ/harness_gpu_main.o" \
+      -L"$REPO/paper_2009_07785_b200" -lpropgate_b200 -Wl,-rpath,'$ORIGIN/../../paper_2009_07785_b200'
+fi
 echo "build_ref: ok -> $OUT"

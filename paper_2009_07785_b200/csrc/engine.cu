@@ -27,6 +27,7 @@
 #include <deque>
 #include <cstdlib>
 #include <limits>
+#include <atomic>
 #include <mutex>
 #include <thread>
 #include <cstdio>
@@ -168,6 +169,7 @@ struct Nccl {
   int (*get_unique_id)(NcclUid*) = nullptr;
   int (*comm_init_rank)(void**, int, NcclUid, int) = nullptr;
   int (*comm_destroy)(void*) = nullptr;
+  int (*comm_abort)(void*) = nullptr;
   int (*all_reduce_fn)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*all_gather_fn)(const void*, void*, size_t, int, void*, cudaStream_t) = nullptr;
   const char* (*error_string)(int) = nullptr;
@@ -181,6 +183,7 @@ struct Nccl {
     get_unique_id = (int (*)(NcclUid*))dlsym(h, "ncclGetUniqueId");
     comm_init_rank = (int (*)(void**, int, NcclUid, int))dlsym(h, "ncclCommInitRank");
     comm_destroy = (int (*)(void*))dlsym(h, "ncclCommDestroy");
+    comm_abort = (int (*)(void*))dlsym(h, "ncclCommAbort");
     all_reduce_fn = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(
         h, "ncclAllReduce");
     all_gather_fn = (int (*)(const void*, void*, size_t, int, void*, cudaStream_t))dlsym(
@@ -322,6 +325,7 @@ struct pg_session {
   cudaStream_t stream2 = nullptr;  // session setup: ordering overlapped with the upload
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void* comm = nullptr;  // NCCL communicator of the row-sharded mode
+  std::atomic<bool> comm_aborted{false};  // another rank failed: the communicator was aborted
   int32_t rank = 0, world = 1;
   // sum(len^2) / (n nnz): how often consecutive entries of a row hit
   // neighbouring columns; dense rows gather the 16 B bounds records (two per
@@ -375,7 +379,7 @@ struct pg_session {
     if (graph) cudaGraphDestroy(graph);
     destroy_shard_graphs();
 
-    if (comm) g_nccl.comm_destroy(comm);
+    if (comm && !comm_aborted) g_nccl.comm_destroy(comm);  // an aborted one is freed already
     for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up, (void*)d_keep_lo, (void*)d_keep_up, (void*)d_delta,
                     (void*)d_delta_all, (void*)d_dcnt, (void*)d_dcnt_all})
       dfree(p);
@@ -2094,7 +2098,8 @@ int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank, i
     void* comm = nullptr;
     const int rc = g_nccl.comm_init_rank(&comm, world, uid, rank);
     if (rc != 0) throw Error{PG_ENCCL, std::string("ncclCommInitRank: ") + g_nccl.error(rc)};
-    if (s->comm) g_nccl.comm_destroy(s->comm);
+    if (s->comm && !s->comm_aborted) g_nccl.comm_destroy(s->comm);
+    s->comm_aborted = false;
     s->comm = comm;
     s->rank = rank;
     s->world = world;
@@ -2213,7 +2218,19 @@ int pg_multi_propagate(const pg_problem* p, const pg_config* cfg, int32_t ngpus,
       e = pg_session_propagate(ss[g], nullptr, nullptr, &rr[g]);
     }
     rcs[g] = e;
-    if (e) errs[g] = pg_last_error();
+    if (e) {
+      errs[g] = pg_last_error();
+      // a failed rank must not leave the others waiting in a collective:
+      // abort every attached communicator (ncclCommAbort is safe from
+      // another thread and ends their in-flight NCCL work with an error)
+      std::lock_guard<std::mutex> lk(mu);
+      if (!abort_all && g_nccl.comm_abort) {
+        abort_all = true;
+        for (int k = 0; k < ngpus; ++k)
+          if (k != g && ss[k] && ss[k]->comm && !ss[k]->comm_aborted.exchange(true))
+            g_nccl.comm_abort(ss[k]->comm);
+      }
+    }
   };
   std::vector<std::thread> th;
   for (int g = 1; g < ngpus; ++g) th.emplace_back(work, g);
