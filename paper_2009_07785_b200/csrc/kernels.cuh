@@ -460,6 +460,9 @@ template <int kThreads>
 __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, int& f) {
   __shared__ unsigned long long s_sum[kThreads / 32];
   __shared__ int s_f[kThreads / 32];
+  // the previous call's reads (thread 0) precede this call's writes
+  // (compute-sanitizer racecheck: the persistent loop calls this every round)
+  __syncthreads();
   for (int o = 16; o > 0; o >>= 1) {
     v += __shfl_xor_sync(0xffffffffu, v, o);
     f |= __shfl_xor_sync(0xffffffffu, f, o);
@@ -1005,8 +1008,9 @@ __global__ void k_csc_fill(const int32_t* __restrict__ row_ptr, const int32_t* _
                            int m, int n, int32_t* __restrict__ cursor,
                            const int32_t* __restrict__ rowmap, int32_t* __restrict__ col_row) {
   walk_entries(row_ptr, m, row_ptr[m], [&](bool valid, int64_t k, int r) {
+    if (!valid) return;  // k may be past the last entry
     const uint32_t c = (uint32_t)colx[k] & 0x7fffffffu;
-    if (valid && c < (uint32_t)n) col_row[atomicAdd(&cursor[c], 1)] = rowmap ? rowmap[r] : r;
+    if (c < (uint32_t)n) col_row[atomicAdd(&cursor[c], 1)] = rowmap ? rowmap[r] : r;
   });
 }
 

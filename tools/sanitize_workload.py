@@ -1,0 +1,89 @@
+"""Small workloads for compute-sanitizer (tools/sanitize.sh): every kernel
+family of the engine on instances small enough for the tools' overhead.
+
+  cascade(50)                host loop and graph loop
+  C1 shape (3k x 3k)         persistent k_loop (grid barrier), row check, worklist
+  long rows (C3 shape, 2k)   split rows: chunks, k_split_finish, k_cand
+  set partitioning (C5)      per-round kernels (host loop), worklist
+  B&B nodes                  k_nodes (batched), warm-started
+  Narrow32                   k_round_f32
+  row shards (NCCL, 1 rank)  unrolled round graphs, dense and delta exchanges
+  ingest                     pg_csr_from_triplets (device sort/segment/sum)
+Each result is checked against the oracle so a sanitizer run is also a
+parity run."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from instances import generators as G  # noqa: E402
+from oracle import oracle as O  # noqa: E402
+from paper_2009_07785_b200.engine import Session, node_overrides, propagate_gpu  # noqa: E402
+from paper_2009_07785_b200.model import EngineConfig, LoopMode, ScalarMode  # noqa: E402
+
+
+def same(gpu, ref, what):
+    ok = (gpu.status == ref.status and gpu.rounds_executed == ref.rounds_executed and
+          np.array_equal(O.canon(gpu.bounds.lower), O.canon(ref.bounds.lower)) and
+          np.array_equal(O.canon(gpu.bounds.upper), O.canon(ref.bounds.upper)))
+    print(("ok  " if ok else "BAD ") + what, gpu.status.name, gpu.rounds_executed, flush=True)
+    return ok
+
+
+def main():
+    bad = 0
+    par = EngineConfig(row_check=False)
+    c = G.gen_cascade(50)
+    for loop in (LoopMode.Host, LoopMode.Graph):
+        bad += not same(propagate_gpu(c, EngineConfig(row_check=False, loop_mode=loop)),
+                        O.propagate_parallel(c, par), f"cascade50 {loop.name}")
+    r = G.gen_random(3000, 3000, 1, mean_row_nnz=8.0, integral_fraction=0.5)
+    for wl in (False, True):
+        cfg = EngineConfig(row_check=True, worklist=wl)
+        bad += not same(propagate_gpu(r, cfg), O.propagate_parallel(r, cfg), f"c1-shape wl={wl}")
+    lr = G.gen_longrows(2000, 4000, 3001, long_every=100, long_min=3000, long_max=5000)
+    for loop in (LoopMode.Host, LoopMode.Graph):
+        cfg = EngineConfig(row_check=False, loop_mode=loop)
+        bad += not same(propagate_gpu(lr, cfg), O.propagate_parallel(lr, cfg), f"longrows {loop.name}")
+    sp = G.gen_setpart(4000, 20000, 50, f_fixed=0.2, seed=5001)
+    cfg = EngineConfig(row_check=False, worklist=True, loop_mode=LoopMode.Host)
+    bad += not same(propagate_gpu(sp, cfg), O.propagate_parallel(sp, cfg), "setpart host wl")
+    nd = G.gen_random(4000, 4000, 4, mean_row_nnz=8.0, integral_fraction=0.5)
+    with Session(nd, EngineConfig(row_check=False, worklist=True)) as s:
+        root = s.set_root()
+        lo, up = G.gen_nodes(nd, root.bounds.lower, root.bounds.upper, K=12)
+        ptr, vs, ls, us = node_overrides(root.bounds.lower, root.bounds.upper, lo, up)
+        st, rd, blo, bup, _ = s.propagate_nodes(ptr, vs, ls, us, want_bounds=True)
+        for k in range(12):
+            ref = O.propagate_parallel(nd, par, lo[k], up[k])
+            ok = st[k] == int(ref.status) and np.array_equal(O.canon(blo[k]), O.canon(ref.bounds.lower))
+            bad += not ok
+        print(("ok  " if bad == 0 else "BAD ") + "nodes x12", flush=True)
+    f32 = EngineConfig(row_check=False, scalar_mode=ScalarMode.Narrow32)
+    bad += not same(propagate_gpu(r, f32), O.propagate_parallel(r, f32), "narrow32")
+    try:
+        from paper_2009_07785_b200.multi import RowShardedSession
+        for delta in (False, True):
+            cfg = EngineConfig(row_check=False, worklist=True, delta_exchange=delta)
+            rs = RowShardedSession(sp, cfg, rank=0, world=1, force_comm=True)
+            bad += not same(rs.propagate(), O.propagate_parallel(sp, par), f"row shards delta={delta}")
+            rs.close()
+    except Exception as e:  # NCCL missing: reported, not fatal
+        print("row shards skipped:", e)
+    from paper_2009_07785_b200.engine import csr_from_triplets_gpu
+    rng = np.random.default_rng(7)
+    rows = rng.integers(0, 500, 20000).astype(np.int32)
+    cols = rng.integers(0, 400, 20000).astype(np.int32)
+    vals = rng.standard_normal(20000)
+    g = csr_from_triplets_gpu(rows, cols, vals, 500, 400)
+    ref = O.csr_from_triplets(rows, cols, vals, 500, 400)
+    ok = all(np.array_equal(a, b) for a, b in zip((g.row_ptr, g.col_idx, g.values), ref))
+    print(("ok  " if ok else "BAD ") + "ingest", flush=True)
+    bad += not ok
+    print("workload mismatches:", bad)
+    sys.exit(1 if bad else 0)
+
+
+if __name__ == "__main__":
+    main()
