@@ -641,6 +641,9 @@ struct pg_session {
     destroy_shard_graphs();
     if (const char* e = getenv("PG_SHARD_ROUNDS")) shard_rounds = std::max(1, atoi(e));
     unrolled = true;
+    // the round kernels of these graphs check the device state first
+    dcfg.flags |= kUnrolledFlag;
+    dirty.unrolled = 1;
     struct Off {
       bool* f;
       ~Off() { *f = false; }

@@ -69,11 +69,19 @@ struct DevState {
 // Row shards run graphs of R unrolled rounds (no conditional nodes around
 // NCCL calls); a round's kernels return at once once the solve is decided
 // (done) or held (stall), and the compute phases also in a resumed round.
-__device__ __forceinline__ bool round_off(DevState* st) {
+// Only those sessions pay the state loads (kUnrolledFlag in the kernel's
+// DevCfg); the other loops never launch a round after the decision.
+constexpr uint32_t kUnrolledFlag = 0x40000000u;
+__device__ __forceinline__ bool round_off(DevState* st, const DevCfg& c) {
+  return (c.flags & kUnrolledFlag) && (ld_gpu(&st->done) | ld_gpu(&st->stall)) != 0;
+}
+// the exchange kernels of row-sharded rounds always check
+__device__ __forceinline__ bool state_off(DevState* st) {
   return (ld_gpu(&st->done) | ld_gpu(&st->stall)) != 0;
 }
-__device__ __forceinline__ bool compute_off(DevState* st) {
-  return (ld_gpu(&st->done) | ld_gpu(&st->stall) | ld_gpu(&st->resume)) != 0;
+__device__ __forceinline__ bool compute_off(DevState* st, const DevCfg& c) {
+  return (c.flags & kUnrolledFlag) &&
+         (ld_gpu(&st->done) | ld_gpu(&st->stall) | ld_gpu(&st->resume)) != 0;
 }
 
 // Device-side worklist (PG_FLAG_WORKLIST): a round only
@@ -103,6 +111,7 @@ struct Dirty {
   int32_t* unit_list;        // [2][nunits] marked one-lane units
   int32_t nslices, nunits;
   int32_t dense_nchg;        // more changed columns than this: next round is a full sweep
+  int32_t unrolled;          // row-shard graphs of unrolled rounds (round_off)
 };
 
 // Row r (sorted) becomes marked for the round of parity `par` (exactly once:
@@ -628,7 +637,7 @@ __global__ void __launch_bounds__(kCommitThreads)
              const Dirty D, cudaGraphConditionalHandle cond, int use_graph, int allow_list) {
   // a worklist round of a single session is committed by k_commit_list; with
   // row shards every column may have moved on another rank: always in full
-  if (round_off(st)) return;
+  if (round_off(st, cfg)) return;
   if (allow_list && ld_gpu(&st->sparse_round)) return;
   commit_body(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph);
 }
@@ -639,7 +648,7 @@ __global__ void __launch_bounds__(kCommitThreads)
                   const longlong2* __restrict__ key_out, int n, DevState* __restrict__ st,
                   long long* __restrict__ per_round, const DevCfg cfg, const Dirty D, const Touch T,
                   cudaGraphConditionalHandle cond, int use_graph) {
-  if (round_off(st) || !ld_gpu(&st->sparse_round)) return;
+  if (round_off(st, cfg) || !ld_gpu(&st->sparse_round)) return;
   commit_body<true>(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph, &T);
 }
 
@@ -714,7 +723,7 @@ __global__ void __launch_bounds__(kCommitThreads)
 // Row-sharded rounds: this rank's infeasibility into the slot that rides the
 // bound all-reduce (max over {lb key, -ub key, flag}).
 __global__ void k_flag_to_slot(DevState* __restrict__ st, longlong2* __restrict__ slot) {
-  if (threadIdx.x == 0 && !round_off(st)) slot->x = ld_gpu(&st->infeasible) ? 1 : 0;
+  if (threadIdx.x == 0 && !state_off(st)) slot->x = ld_gpu(&st->infeasible) ? 1 : 0;
 }
 
 // ---- row shards: sparse delta exchange ---------------
@@ -732,7 +741,7 @@ __global__ void __launch_bounds__(256)
                     DevState* __restrict__ st, DeltaItem* __restrict__ out, int cap,
                     int* __restrict__ cnt) {
   const int lane = threadIdx.x & 31;
-  if (round_off(st)) return;  // counts stay zero (memset before the launch)
+  if (state_off(st)) return;  // counts stay zero (memset before the launch)
   if (blockIdx.x == 0 && threadIdx.x == 0) cnt[1] = ld_gpu(&st->infeasible) ? 1 : 0;
   for (int j0 = (blockIdx.x * blockDim.x + threadIdx.x) & ~31; j0 < n; j0 += gridDim.x * blockDim.x) {
     const int j = j0 + lane;
@@ -761,7 +770,7 @@ __global__ void __launch_bounds__(256)
     k_delta_apply(const DeltaItem* __restrict__ all, const int* __restrict__ cnt_all, int world,
                   int stride, longlong2* __restrict__ key_out, DevState* __restrict__ st,
                   int held_ok) {
-  if (round_off(st)) return;
+  if (state_off(st)) return;
   if (held_ok) {
     int maxc = 0;
     for (int r = 0; r < world; ++r) maxc = max(maxc, cnt_all[2 * r]);
@@ -945,7 +954,7 @@ __global__ void k_apply_node(double* __restrict__ lo0, double* __restrict__ up0,
 // column changed in round r (one warp per changed column).
 __device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__ st) {
   const int r = ld_gpu(&st->round);
-  if (!D.enabled || round_off(st) || ld_gpu(&st->full)) return;
+  if (!D.enabled || (D.unrolled && state_off(st)) || ld_gpu(&st->full)) return;
   const int cb = r & 1, nb = (r + 1) & 1;
   const int nchg = ld_gpu(&st->nchg[cb]);
   uint8_t* flag = D.row_flag + (size_t)nb * D.ms;

@@ -62,7 +62,7 @@ __device__ __forceinline__ ActF actf_row(const RoundArgs& A, int r, int chunk, A
 template <bool kRowCheck>
 __global__ void __launch_bounds__(256) k_round_f32(const RoundArgs A, const DevCfg cfg, int m,
                                                    ActF* scratch, int maxc) {
-  if (compute_off(A.st)) return;
+  if (compute_off(A.st, cfg)) return;
   const float inf = CUDART_INF_F;
   const float eps = (float)cfg.int_eps;
   const float huge = (float)cfg.inf_thr;

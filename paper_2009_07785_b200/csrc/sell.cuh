@@ -157,85 +157,43 @@ __device__ __forceinline__ void ld_col(const RA& A, int32_t c, uint64_t pol, boo
 }
 
 // ---- filter words -----------------------------------------------------------------
-// Phase 1 leaves one 32-bit word per entry of a one-lane unit in the warp's
-// SHARED memory (never in HBM): the entry's filter term x = |a| q rounded up
-// to float, as a monotone int32 key (negative floats bit-reversed), with the
-// two infinity flags in the low bits (bit 0: min contribution infinite, bit
-// 1: max contribution infinite).  (w | 3) is the key of a float >= x, so a
-// threshold test on it is never stricter than the exact test, and every
-// entry that passes goes through the exact f64 pipeline.  A NaN term (a = 0
-// with an infinite bound: such an entry never yields a candidate) keys as
-// -inf.  The row's largest word bounds its largest term.
-__device__ __forceinline__ int32_t fkey_of(float f) {
-  const int32_t b = __float_as_int(f);
-  return b ^ ((b >> 31) & 0x7fffffff);
+// |a| q rounded toward +inf to float; bit 0 = min contribution infinite,
+// bit 1 = max contribution infinite.  +inf / NaN terms read back as NaN,
+// which every threshold test passes.
+// (+inf keeps its exponent; decoding sets the low bits of a positive word,
+// so it reads back as NaN)
+__device__ __forceinline__ uint32_t filt_encode(double x, bool imin, bool imax) {
+  const uint32_t b = __float_as_uint(__double2float_ru(x));
+  return (b & ~3u) | (imin ? 1u : 0u) | (imax ? 2u : 0u);
 }
-__device__ __forceinline__ float fkey_float(int32_t k) {  // the inverse of fkey_of
-  return __int_as_float(k ^ ((k >> 31) & 0x7fffffff));
+// a value >= the encoded term (low bits set for positive, cleared for negative)
+__device__ __forceinline__ double filt_term(uint32_t b) {
+  return (double)__uint_as_float((b & 0x80000000u) ? (b & ~3u) : (b | 3u));
 }
-// a double >= every term behind the largest word xk (+inf's key | 3 is a NaN pattern)
-__device__ __forceinline__ double fkey_bound(int32_t xk) {
-  const float f = fkey_float(xk | 3);
-  return f == f ? (double)f : CUDART_INF;
-}
-constexpr int32_t kFKeyMin = (int32_t)0x807fffff;  // key of -inf: the empty maximum
-__device__ __forceinline__ int32_t fword(double x, bool imin, bool imax) {
-  // a NaN term (a = 0 with an infinite bound, or a padding entry) keys as
-  // -inf: such an entry never yields a candidate, and it must not mask the
-  // row's real largest term (fmaxf drops the NaN)
-  const float f = fmaxf(__double2float_ru(x), -CUDART_INF_F);
-  return (fkey_of(f) & ~3) | (imin ? 1 : 0) | (imax ? 2 : 0);
-}
-// Per-unit form of the row filter: the smaller enabled threshold rounded
-// down to float (key), and the flag mask of the one-infinite-entry sides.
-// Testing x >= min(tr, tl) is testing both sides at once (kernels.cuh
-// entry_may), a little looser, never stricter.
-struct FTest {
-  int32_t tk;
-  int32_t fm;
-};
-__device__ __forceinline__ FTest ftest(const RowFilter& f) {
-  double t = CUDART_INF;
-  if (f.mode & 1) t = f.tr;
-  if (f.mode & 2) t = (f.mode & 1) ? fmin(t, f.tl) : f.tl;
-  FTest r;
-  r.tk = (f.mode & 3) ? fkey_of(__double2float_rd(t)) : 0x7fffffff;
-  r.fm = ((f.mode & 4) ? 1 : 0) | ((f.mode & 8) ? 2 : 0);
-  return r;
-}
-__device__ __forceinline__ bool fpass(const FTest& t, int32_t w) {
-  return (w | 3) >= t.tk || (w & t.fm) != 0;
-}
-__device__ __forceinline__ bool frow_may(const FTest& t, int32_t xk) {
-  return t.fm != 0 || (xk | 3) >= t.tk;
+__device__ __forceinline__ bool filt_may(const RowFilter& f, uint32_t b) {
+  const double x = filt_term(b);
+  return ((f.mode & 1) && !(f.tr > x)) || ((f.mode & 2) && !(f.tl > x)) ||
+         ((f.mode & 4) && (b & 1u)) || ((f.mode & 8) && (b & 2u));
 }
 
 // ---- per-warp shared state ----------------------------------------------------------
-constexpr int kSellWordSteps = 64;  // one-lane units are <= 64 entries (sell_lg)
 struct SellWarpSmem {
   double min_f[32], max_f[32], lhs[32], rhs[32], tr[32], tl[32];
-  int32_t min_i[32], max_i[32], tkey[32], fmask[32];
+  int32_t min_i[32], max_i[32];
   uint8_t mode[32], may[32];
   // entries that survive the filter: element offset in the slice, unit
   int32_t qe[64];
   uint8_t qu[64];
-  union {
-    // full sweeps: the filter words of the warp's one-lane slice(s),
-    // words[32 * step + lane] (a group of narrow slices: 16 steps each)
-    int32_t words[32 * kSellWordSteps];
-    // worklist rounds: {min, max} contributions of a wide unit's blocks
-    struct {
-      double2 wbuf[256];
-      double2 wbuf2[256];
-    };
-  };
+  double2 wbuf[256];  // worklist rounds: {min, max} contributions of a wide unit's block
+  double2 wbuf2[256];
 };
 
 constexpr size_t kSellSmem = sizeof(SellWarpSmem) * kSellWarps;
-constexpr size_t kSellDenseStride = sizeof(SellWarpSmem);
-constexpr size_t kSellSmemDense = kSellSmem;
-static_assert(sizeof(SellWarpSmem) % 16 == 0, "warp records stay 16 B aligned");
-static_assert(PG_SELL_GROUPW * PG_SELL_GROUP <= kSellWordSteps, "group words fit");
+// full sweeps never touch the wide-unit buffers: their warps' records are
+// packed at this stride (the dynamic shared memory of the dense kernel)
+constexpr size_t kSellDenseStride = __builtin_offsetof(SellWarpSmem, wbuf);
+constexpr size_t kSellSmemDense = kSellDenseStride * kSellWarps;
+static_assert(kSellDenseStride % 16 == 0, "warp records stay 16 B aligned");
 
 // exact pipeline over queue entries [0, cnt), one per lane
 template <class RA>
@@ -257,27 +215,25 @@ __device__ __forceinline__ bool sell_drain(const RA& A, const SellWarpSmem& W,
 }
 
 // One step of a unit's chain on this lane: contributions (propcore.hpp:50-62:
-// b by the sign of a; an infinite b is counted, a finite one adds a*b) and
-// the filter word (kept when kWord: one-lane units).  Adding +0.0 (an
-// infinite b, or a padding entry) is exact: the sums start at +0.0 and never
-// become -0.0.  With G = 2^LG lanes per unit, the G entries of the step sit
-// on lanes u, u + H, .. and are added in entry order (every lane of the unit
-// forms the same sum).
-template <int LG, bool kWord>
+// b by the sign of a; an infinite b is counted, a finite one adds a*b),
+// filter term and word.  Adding +0.0 (an infinite b, or a padding entry) is
+// exact: the sums start at +0.0 and never become -0.0.  With G = 2^LG lanes
+// per unit, the G entries of the step sit on lanes u, u + H, .. and are
+// added in entry order (every lane of the unit forms the same sum).
+template <int LG>
 __device__ __forceinline__ void sell_step(double a, double lo, double up, double q, int u, Act& act,
-                                          int32_t& xk, int32_t* pw) {
+                                          double& xmax, uint32_t* pw) {
   constexpr int G = 1 << LG, H = 32 >> LG;
-  const bool pos = a > 0;
-  const double bmin = pos ? lo : up;
-  const double bmax = pos ? up : lo;
-  const bool imin = fabs(bmin) == CUDART_INF, imax = fabs(bmax) == CUDART_INF;
+  const double bmin = a > 0 ? lo : up;
+  const double bmax = a > 0 ? up : lo;
+  const bool imin = isinf(bmin), imax = isinf(bmax);
   const double pmin = imin ? 0.0 : __dmul_rn(a, bmin);
   const double pmax = imax ? 0.0 : __dmul_rn(a, bmax);
   act.min_i += imin;
   act.max_i += imax;
-  const int32_t w = fword(fabs(a) * q, imin, imax);
-  xk = max(xk, w);
-  if (kWord) *pw = w;
+  const double x = fabs(a) * q;
+  xmax = fmax(xmax, x);
+  *pw = filt_encode(x, imin, imax);
   if (LG == 0) {
     act.min_f = __dadd_rn(act.min_f, pmin);
     act.max_f = __dadd_rn(act.max_f, pmax);
@@ -292,11 +248,11 @@ __device__ __forceinline__ void sell_step(double a, double lo, double up, double
   }
 }
 
-// a chunk of a split row: its partial record (xmax: a double >= the chunk's
-// largest term); after the sweep, k_split_finish combines the partials of
-// every row whose chunks all ran
+// a chunk of a split row: its partial record; after the sweep,
+// k_split_finish combines the partials of every row whose chunks all ran
+template <bool kRowCheck>
 __device__ __forceinline__ void chunk_done(const RoundArgs& A, const UnitDesc& ud, const Act& act,
-                                           double xmax) {
+                                           double xmax, bool& inf_flag, const DevCfg& cfg) {
   const SegDesc d = A.segs[-ud.ref - 1];
   SegPartial* P = A.partial + d.out;
   P->min_f = act.min_f;
@@ -309,26 +265,24 @@ __device__ __forceinline__ void chunk_done(const RoundArgs& A, const UnitDesc& u
 
 // Second half of a slice, after its chains: order-free reductions over a
 // unit's lanes, row finish on the owner lanes (row check, filter; chunks of
-// split rows: partial record), then phase 2: one-lane slices test the filter
-// words left in shared memory (`words`, this lane's column); multi-lane
-// slices (long units, which rarely may tighten) re-read the may-units'
-// entries and test them exactly.  Survivors are queued and drained 32 at a
-// time through the exact pipeline.
+// split rows: partial record, last chunk combines), then phase 2 over the
+// slice's filter words.
 template <bool kRowCheck, int LG, class RA>
 __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const SliceDesc& sd,
                                            const UnitDesc& ud, bool active, int len, int lane,
-                                           Act act, int32_t xk, double lhs_r, double rhs_r,
-                                           uint64_t pol_keep, uint64_t pol_stream, bool& inf_flag,
-                                           const DevCfg& cfg, const int32_t* words) {
+                                           Act act, double xmax, double lhs_r, double rhs_r,
+                                           uint64_t pol_keep, bool& inf_flag, const DevCfg& cfg) {
   constexpr int H = 32 >> LG;
   const int j = lane >> (5 - LG), u = lane & (H - 1);
   const bool whole = ud.ref >= 0;
+  const int steps = sd.steps;
+  uint32_t* sw = A.sw + sd.off + lane;
   // order-free parts over the unit's lanes
 #pragma unroll
   for (int o = H; o < 32; o <<= 1) {
     act.min_i += __shfl_xor_sync(0xffffffffu, act.min_i, o);
     act.max_i += __shfl_xor_sync(0xffffffffu, act.max_i, o);
-    xk = max(xk, __shfl_xor_sync(0xffffffffu, xk, o));
+    xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
   }
 
   // ---- row finish (owner lanes) ----------------------------------------------------
@@ -338,8 +292,7 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
       const double l = lhs_r, h = rhs_r;
       if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
       const RowFilter f = row_filter(act, l, h);
-      const FTest ft = ftest(f);
-      may = frow_may(ft, xk);
+      may = row_may(f, xmax);
       W.min_f[u] = act.min_f;
       W.max_f[u] = act.max_f;
       W.min_i[u] = act.min_i;
@@ -349,68 +302,34 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
       W.tr[u] = f.tr;
       W.tl[u] = f.tl;
       W.mode[u] = f.mode;
-      W.tkey[u] = ft.tk;
-      W.fmask[u] = ft.fm;
     } else {
-      chunk_done(A, ud, act, fkey_bound(xk));
+      chunk_done<kRowCheck>(A, ud, act, xmax, inf_flag, cfg);
     }
   }
   if (j == 0) W.may[u] = may;
   if (PG_SELL_DEBUG && (cfg.flags & 0x10000u)) return;  // timing experiments only: no phase 2
   if (!__any_sync(0xffffffffu, may)) return;
 
-  // ---- phase 2: filter -> queue -> exact pipeline ------------------------------------
+  // ---- phase 2: filter words -> queue -> exact pipeline ------------------------------
   __syncwarp();
   const bool umay = W.may[u] != 0;
-  // the longest may-unit bounds the pass
-  const int last = __reduce_max_sync(0xffffffffu, umay ? len : 0);
-  const int steps = (last + (1 << LG) - 1) >> LG;
-  int qn = 0;
-  FTest ft = {0x7fffffff, 0};
   RowFilter f = {0.0, 0.0, 0};
-  if (umay) {
-    ft = FTest{W.tkey[u], W.fmask[u]};
-    f = RowFilter{W.tr[u], W.tl[u], W.mode[u]};
-  }
-  const bool frac_any = LG > 0 && ld_gpu(&A.st->frac_any) != 0;
+  if (umay) f = RowFilter{W.tr[u], W.tl[u], W.mode[u]};
+  int qn = 0;
   for (int t0 = 0; t0 < steps; t0 += kSellUnroll) {
-    bool pass[kSellUnroll];
-    if (LG == 0) {
+    uint32_t b[kSellUnroll];
+    bool in[kSellUnroll];
 #pragma unroll
-      for (int k = 0; k < kSellUnroll; ++k) {
-        const bool in = umay && t0 + k < len;
-        pass[k] = in && fpass(ft, words[32 * (t0 + k)]);
-      }
-    } else {
-      // re-read and test exactly (entry_may): the words were not kept
-      double a[kSellUnroll];
-      int32_t c[kSellUnroll];
-      bool in[kSellUnroll];
-#pragma unroll
-      for (int k = 0; k < kSellUnroll; ++k) {
-        in[k] = umay && ((t0 + k) << LG) + j < len;
-        a[k] = 0.0;
-        c[k] = A.pad_col;
-        if (in[k]) {
-          a[k] = ld_stream_f64(A.sv + sd.off + 32 * (t0 + k) + lane, pol_stream);
-          c[k] = ld_stream_s32(A.sc + sd.off + 32 * (t0 + k) + lane, pol_stream);
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < kSellUnroll; ++k) {
-        double lo, up, q;
-        ld_col(A, c[k], pol_keep, frac_any, cfg, lo, up, q);
-        const double bmin = a[k] > 0 ? lo : up;
-        const double bmax = a[k] > 0 ? up : lo;
-        pass[k] = in[k] && entry_may(f, fabs(a[k]) * q, fabs(bmin) == CUDART_INF,
-                                     fabs(bmax) == CUDART_INF);
-      }
+    for (int k = 0; k < kSellUnroll; ++k) {
+      in[k] = umay && ((t0 + k) << LG) + j < len;
+      b[k] = in[k] ? sw[32 * (t0 + k)] : 0u;
     }
 #pragma unroll
     for (int k = 0; k < kSellUnroll; ++k) {
-      const unsigned m = __ballot_sync(0xffffffffu, pass[k]);
+      const bool pass = in[k] && filt_may(f, b[k]);
+      const unsigned m = __ballot_sync(0xffffffffu, pass);
       if (!m) continue;
-      if (pass[k]) {
+      if (pass) {
         const int slot = qn + __popc(m & ((1u << lane) - 1u));
         W.qe[slot] = 32 * (t0 + k) + lane;
         W.qu[slot] = (uint8_t)u;
@@ -436,104 +355,136 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
   __syncwarp();
 }
 
-// One slice by one warp, full sweep.  LG = log2(lanes per unit); every lane
-// walks every step of the slice (entries past a unit's end are padding:
-// value 0 in the padding column with bounds [0, 0], which adds +0.0).
-template <bool kRowCheck, int LG, class RA>
+// One slice by one warp.  LG = log2(lanes per unit); kDense: a full sweep
+// (no worklist), every lane walks every step of the slice.
+template <bool kRowCheck, int LG, bool kDense, class RA>
 __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const SliceDesc& sd,
-                                           int lane, uint64_t pol_keep, uint64_t pol_stream,
-                                           bool& inf_flag, const DevCfg& cfg) {
+                                           int lane, bool full, const uint8_t* rflag,
+                                           uint64_t pol_keep, uint64_t pol_stream, bool& inf_flag,
+                                           const DevCfg& cfg) {
   constexpr int H = 32 >> LG;
-  constexpr bool kWord = LG == 0;  // one-lane units keep their words (<= 64 steps)
-  const int u = lane & (H - 1);
+  const int j = lane >> (5 - LG), u = lane & (H - 1);
   UnitDesc ud = {0, -1};
-  const bool active = u < sd.count;
+  bool active = u < sd.count;
   if (active) ud = A.units[sd.first + u];
+  if (!full && active) {
+    // worklist: the unit's row must carry a mark (split rows: all chunks of a
+    // marked row are marked, so its finisher sees every partial)
+    const int fr = ud.ref >= 0 ? ud.ref : A.srow[A.segs[-ud.ref - 1].rslot];
+    active = rflag[fr] != 0;
+  }
+  if (!__any_sync(0xffffffffu, active)) return;
   const int len = active ? ud.len : 0;
-  const double* pa = A.sv + sd.off + lane;
-  const int32_t* pc = A.sc + sd.off + lane;
-  int32_t* pw = W.words + lane;
+  const double* sv = A.sv + sd.off + lane;
+  const int32_t* sc = A.sc + sd.off + lane;
+  uint32_t* sw = A.sw + sd.off + lane;
   const int steps = sd.steps;
   const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
-  const double lhs_r = active && ud.ref >= 0 ? A.lhs[ud.ref] : 0.0;
-  const double rhs_r = active && ud.ref >= 0 ? A.rhs[ud.ref] : 0.0;
 
   // ---- phase 1: the chains ------------------------------------------------------
   Act act = {0.0, 0.0, 0, 0};
-  int32_t xk = kFKeyMin;
-  constexpr int UL = LG >= PG_SELL_LGU ? PG_SELL_ULONG : kSellUnroll;
-  int t = 0;
-  double a[UL];
-  int32_t c[UL];
-  if (UL <= steps) {
+  double xmax = -CUDART_INF;
+  if (kDense) {
+    constexpr int UL = LG >= PG_SELL_LGU ? PG_SELL_ULONG : kSellUnroll;
+    // every lane walks all `steps` of the slice: entries past a unit's end are
+    // padding (value 0, the padding column with bounds [0, 0]) and add +0.0
+    const double* pa = sv;
+    const int32_t* pc = sc;
+    uint32_t* pw = sw;
+    int t = 0;
+    double a[UL];
+    int32_t c[UL];
+    if (UL <= steps) {
 #pragma unroll
-    for (int k = 0; k < UL; ++k) {
-      a[k] = ld_stream_f64(pa + 32 * k, pol_stream);
-      c[k] = ld_stream_s32(pc + 32 * k, pol_stream);
-    }
-  }
-  for (; t + UL <= steps; t += UL) {
-    if (PG_SELL_PF && lane == 0 && t + 5 * UL <= steps) {
-      prefetch_l2(pa + 32 * 4 * UL, 256u * UL);
-      prefetch_l2(pc + 32 * 4 * UL, 128u * UL);
-    }
-    double lo[UL], up[UL], q[UL];
-#pragma unroll
-    for (int k = 0; k < UL; ++k) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
-    // the next group's values and columns are in flight during this one
-    double an[UL];
-    int32_t cn[UL];
-    const bool more = t + 2 * UL <= steps;
-#pragma unroll
-    for (int k = 0; k < UL; ++k) {
-      an[k] = 0.0;
-      cn[k] = 0;
-      if (more) {
-        an[k] = ld_stream_f64(pa + 32 * (UL + k), pol_stream);
-        cn[k] = ld_stream_s32(pc + 32 * (UL + k), pol_stream);
+      for (int k = 0; k < UL; ++k) {
+        a[k] = ld_stream_f64(pa + 32 * k, pol_stream);
+        c[k] = ld_stream_s32(pc + 32 * k, pol_stream);
       }
     }
+    for (; t + UL <= steps; t += UL) {
+      if (PG_SELL_PF && lane == 0 && t + 5 * UL <= steps) {
+        prefetch_l2(pa + 32 * 4 * UL, 256u * UL);
+        prefetch_l2(pc + 32 * 4 * UL, 128u * UL);
+      }
+      double lo[UL], up[UL], q[UL];
 #pragma unroll
-    for (int k = 0; k < UL; ++k)
-      sell_step<LG, kWord>(a[k], lo[k], up[k], q[k], u, act, xk, pw + 32 * k);
+      for (int k = 0; k < UL; ++k)
+        ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
+      // the next group's values and columns are in flight during this one
+      double an[UL];
+      int32_t cn[UL];
+      const bool more = t + 2 * UL <= steps;
 #pragma unroll
-    for (int k = 0; k < UL; ++k) {
-      a[k] = an[k];
-      c[k] = cn[k];
+      for (int k = 0; k < UL; ++k) {
+        an[k] = 0.0;
+        cn[k] = 0;
+        if (more) {
+          an[k] = ld_stream_f64(pa + 32 * (UL + k), pol_stream);
+          cn[k] = ld_stream_s32(pc + 32 * (UL + k), pol_stream);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < UL; ++k)
+        sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xmax, pw + 32 * k);
+#pragma unroll
+      for (int k = 0; k < UL; ++k) {
+        a[k] = an[k];
+        c[k] = cn[k];
+      }
+      pa += 32 * UL;
+      pc += 32 * UL;
+      pw += 32 * UL;
     }
-    pa += 32 * UL;
-    pc += 32 * UL;
-    pw += 32 * UL;
-  }
-  for (; t < steps; ++t) {
-    const double a1 = ld_stream_f64(pa, pol_stream);
-    const int32_t c1 = ld_stream_s32(pc, pol_stream);
-    double lo1, up1, q1;
-    ld_col(A, c1, pol_keep, frac_any, cfg, lo1, up1, q1);
-    sell_step<LG, kWord>(a1, lo1, up1, q1, u, act, xk, pw);
-    pa += 32;
-    pc += 32;
-    pw += 32;
+    for (; t < steps; ++t) {
+      const double a1 = ld_stream_f64(pa, pol_stream);
+      const int32_t c1 = ld_stream_s32(pc, pol_stream);
+      double lo1, up1, q1;
+      ld_col(A, c1, pol_keep, frac_any, cfg, lo1, up1, q1);
+      sell_step<LG>(a1, lo1, up1, q1, u, act, xmax, pw);
+      pa += 32;
+      pc += 32;
+      pw += 32;
+    }
+  } else {
+    // worklist rounds: only the marked units' entries
+    for (int t0 = 0; t0 < steps; t0 += kSellUnroll) {
+      double a[kSellUnroll], lo[kSellUnroll], up[kSellUnroll], q[kSellUnroll];
+      int32_t c[kSellUnroll];
+      bool in[kSellUnroll];
+#pragma unroll
+      for (int k = 0; k < kSellUnroll; ++k) {
+        in[k] = ((t0 + k) << LG) + j < len;
+        a[k] = 0.0;
+        c[k] = A.pad_col;
+        if (in[k]) {
+          a[k] = ld_stream_f64(sv + 32 * (t0 + k), pol_stream);
+          c[k] = ld_stream_s32(sc + 32 * (t0 + k), pol_stream);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < kSellUnroll; ++k)
+        ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
+#pragma unroll
+      for (int k = 0; k < kSellUnroll; ++k)
+        if (t0 + k < steps) sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xmax, sw + 32 * (t0 + k));
+    }
   }
   if (PG_SELL_DEBUG && (cfg.flags & 0x40000u)) {  // timing experiments only: chains alone
-    if (act.min_f == 12345.678 && xk == 1) A.st->infeasible = 1;
+    if (act.min_f == 12345.678 && xmax == 1.0) A.st->infeasible = 1;
     return;
   }
-  slice_tail<kRowCheck, LG>(A, W, sd, ud, active, len, lane, act, xk, lhs_r, rhs_r, pol_keep,
-                            pol_stream, inf_flag, cfg, W.words + lane);
+  slice_tail<kRowCheck, LG>(A, W, sd, ud, active, len, lane, act, xmax, ud.ref >= 0 ? A.lhs[ud.ref] : 0.0,
+                            ud.ref >= 0 ? A.rhs[ud.ref] : 0.0, pol_keep, inf_flag, cfg);
 }
 
-// R narrow slices (one lane per unit, <= PG_SELL_GROUPW entries) by one
-// warp: every lane runs R independent chains, interleaved, with the next
-// step's gathers in flight while this step's contributions are formed, and
-// the per-slice latencies (descriptors, row sides, the ticket) paid once per
-// R slices.  Slice r's words go to words[r * 32 * GROUPW + 32 * step + lane].
-// Steps past a slice's width read nothing and add the padding entry's +0.0.
+// R narrow slices (one lane per unit) by one warp: every lane runs R
+// independent chains, interleaved, so each step has R entries in flight per
+// lane and the per-slice latencies (descriptors, row sides, the ticket)
+// are paid once per R slices.  Full sweeps only.
 template <bool kRowCheck, int R, class RA>
 __device__ __forceinline__ void sell_group(const RA& A, SellWarpSmem& W, int s0, int nr,
                                            int lane, uint64_t pol_keep, uint64_t pol_stream,
                                            bool& inf_flag, const DevCfg& cfg) {
-  constexpr int WS = 32 * PG_SELL_GROUPW;
   long long off[R];
   int steps[R], cnt[R];
   UnitDesc ud[R];
@@ -557,74 +508,59 @@ __device__ __forceinline__ void sell_group(const RA& A, SellWarpSmem& W, int s0,
     }
   }
   Act act[R];
-  int32_t xk[R];
+  double xmax[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     act[r] = Act{0.0, 0.0, 0, 0};
-    xk[r] = kFKeyMin;
+    xmax[r] = -CUDART_INF;
   }
   const int tmax = steps[0];  // the group's first slice is its widest
   const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
-  // pipeline: step t's gathers are in flight from step t - 1, step t + 1's
-  // values and columns from step t - 1
-  double a0[R], a1[R], lo0[R], up0[R], q0[R];
-  int32_t c1[R];
+  double a[R];
+  int32_t c[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    double a = 0.0;
-    int32_t c = A.pad_col;
+    a[r] = 0.0;
+    c[r] = A.pad_col;
     if (0 < steps[r]) {
-      a = ld_stream_f64(A.sv + off[r], pol_stream);
-      c = ld_stream_s32(A.sc + off[r], pol_stream);
-    }
-    a0[r] = a;
-    ld_col(A, c, pol_keep, frac_any, cfg, lo0[r], up0[r], q0[r]);
-    a1[r] = 0.0;
-    c1[r] = A.pad_col;
-    if (1 < steps[r]) {
-      a1[r] = ld_stream_f64(A.sv + off[r] + 32, pol_stream);
-      c1[r] = ld_stream_s32(A.sc + off[r] + 32, pol_stream);
+      a[r] = ld_stream_f64(A.sv + off[r], pol_stream);
+      c[r] = ld_stream_s32(A.sc + off[r], pol_stream);
     }
   }
   for (int t = 0; t < tmax; ++t) {
-    double lo1[R], up1[R], q1[R];
+    double lo[R], up[R], q[R];
 #pragma unroll
-    for (int r = 0; r < R; ++r) ld_col(A, c1[r], pol_keep, frac_any, cfg, lo1[r], up1[r], q1[r]);
-    double a2[R];
-    int32_t c2[R];
+    for (int r = 0; r < R; ++r) ld_col(A, c[r], pol_keep, frac_any, cfg, lo[r], up[r], q[r]);
+    double an[R];
+    int32_t cn[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      a2[r] = 0.0;
-      c2[r] = A.pad_col;
-      if (t + 2 < steps[r]) {
-        a2[r] = ld_stream_f64(A.sv + off[r] + 32 * (t + 2), pol_stream);
-        c2[r] = ld_stream_s32(A.sc + off[r] + 32 * (t + 2), pol_stream);
+      an[r] = 0.0;
+      cn[r] = A.pad_col;
+      if (t + 1 < steps[r]) {
+        an[r] = ld_stream_f64(A.sv + off[r] + 32 * (t + 1), pol_stream);
+        cn[r] = ld_stream_s32(A.sc + off[r] + 32 * (t + 1), pol_stream);
       }
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      sell_step<0, true>(a0[r], lo0[r], up0[r], q0[r], lane, act[r], xk[r],
-                         W.words + r * WS + 32 * t + lane);
+      if (t < steps[r]) sell_step<0>(a[r], lo[r], up[r], q[r], lane, act[r], xmax[r], A.sw + off[r] + 32 * t);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      a0[r] = a1[r];
-      lo0[r] = lo1[r];
-      up0[r] = up1[r];
-      q0[r] = q1[r];
-      a1[r] = a2[r];
-      c1[r] = c2[r];
+      a[r] = an[r];
+      c[r] = cn[r];
     }
   }
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     if (r < nr) {
       const SliceDesc d = {off[r] - lane, 0, 0, steps[r], (int16_t)cnt[r], 0, 0};
-      slice_tail<kRowCheck, 0>(A, W, d, ud[r], lane < cnt[r], ud[r].len, lane, act[r], xk[r],
-                               l[r], h[r], pol_keep, pol_stream, inf_flag, cfg,
-                               W.words + r * WS + lane);
+      slice_tail<kRowCheck, 0>(A, W, d, ud[r], lane < cnt[r], ud[r].len, lane, act[r], xmax[r],
+                               l[r], h[r], pol_keep, inf_flag, cfg);
     }
   }
 }
+
 // Persistent, one warp per slice (longest first).  kDense: a full sweep;
 // otherwise a worklist round (only the marked rows' units).  Both are
 // launched when the worklist is on; the one that does not match the round
@@ -727,7 +663,7 @@ __device__ __forceinline__ void sell_wide(const RA& A, SellWarpSmem& W, int par,
     dbg_t1 = clock64();
 #endif
     if (ud.ref < 0) {
-      if (lane == 0) chunk_done(A, ud, act, xm);
+      if (lane == 0) chunk_done<kRowCheck>(A, ud, act, xm, inf_flag, cfg);
 #if PG_SELL_DEBUG
       if (lane == 0 && (cfg.flags & 0x200000u))
         printf("[wide] chunk len %d phase1 %lld cyc\n", len, dbg_t1 - dbg_t0);
@@ -800,9 +736,9 @@ __device__ __forceinline__ void sell_units(const RA& A, int par, uint64_t pol_ke
     const long long off = A.slices[A.lg0_sstart + (k >> 5)].off + (k & 31);
     const double* sv = A.sv + off;
     const int32_t* sc = A.sc + off;
-    int32_t* sw = reinterpret_cast<int32_t*>(A.sw) + off;
+    uint32_t* sw = A.sw + off;
     Act act = {0.0, 0.0, 0, 0};
-    int32_t xk = kFKeyMin;
+    double xmax = -CUDART_INF;
     for (int t0 = 0; t0 < ud.len; t0 += 4) {
       double a[4], lo[4], up[4], q[4];
       int32_t c[4];
@@ -819,23 +755,23 @@ __device__ __forceinline__ void sell_units(const RA& A, int par, uint64_t pol_ke
       for (int k = 0; k < 4; ++k) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (t0 + k < ud.len) sell_step<0, true>(a[k], lo[k], up[k], q[k], 0, act, xk, sw + 32 * (t0 + k));
+        if (t0 + k < ud.len) sell_step<0>(a[k], lo[k], up[k], q[k], 0, act, xmax, sw + 32 * (t0 + k));
     }
     if (ud.ref < 0) {
-      chunk_done(A, ud, act, fkey_bound(xk));
+      chunk_done<kRowCheck>(A, ud, act, xmax, inf_flag, cfg);
       continue;
     }
     const double l = A.lhs[ud.ref], h = A.rhs[ud.ref];
     if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
-    const FTest ft = ftest(row_filter(act, l, h));
-    if (!frow_may(ft, xk)) continue;
+    const RowFilter f = row_filter(act, l, h);
+    if (!row_may(f, xmax)) continue;
     for (int t0 = 0; t0 < ud.len; t0 += 4) {
       // four entries' filter words, then the survivors' loads, then pipelines
       bool pass[4];
       double a[4], lo[4], up[4], q[4];
       int32_t c[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) pass[k] = t0 + k < ud.len && fpass(ft, sw[32 * (t0 + k)]);
+      for (int k = 0; k < 4; ++k) pass[k] = t0 + k < ud.len && filt_may(f, sw[32 * (t0 + k)]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         a[k] = 0.0;
@@ -863,7 +799,9 @@ __device__ __forceinline__ void sell_sweep(const RA& A, const DevCfg& cfg,
   SellWarpSmem& W = *reinterpret_cast<SellWarpSmem*>(
       reinterpret_cast<unsigned char*>(smem) +
       (size_t)(threadIdx.x >> 5) * (kDense ? kSellDenseStride : sizeof(SellWarpSmem)));
+  const bool full = kDense;
   const int par = (ld_gpu(&A.st->round) + 1) & 1;
+  const uint8_t* rflag = A.dirty.row_flag + (size_t)par * A.dirty.ms;
   const uint64_t pk = l2_policy_evict_last();
   const uint64_t ps = l2_policy_evict_first();
   bool inf_flag = false;
@@ -876,31 +814,37 @@ __device__ __forceinline__ void sell_sweep(const RA& A, const DevCfg& cfg,
   }
   // work items by ticket, longest first; the next ticket is taken when an
   // item starts and read when it ends (its latency hides under the item)
-  int cur = 0;
-  if (lane == 0) cur = atomicAdd(&A.st->work, 1);
-  cur = __shfl_sync(0xffffffffu, cur, 0);
+  int next = 0;
+  if (lane == 0) next = atomicAdd(&A.st->work, 1);
+  next = __shfl_sync(0xffffffffu, next, 0);
   const int nitems = A.group_start + (A.nslices - A.group_start + kSellGroup - 1) / kSellGroup;
-  while (cur < nitems) {
-    const int s = cur;
+  while (next < nitems) {
+    const int s = next;
     int nxt = 0;
     if (lane == 0) nxt = atomicAdd(&A.st->work, 1);
     if (s >= A.group_start) {
       // a group of narrow one-lane slices
       const int s0 = A.group_start + (s - A.group_start) * kSellGroup;
       const int nr = min(kSellGroup, A.nslices - s0);
-      sell_group<kRowCheck, kSellGroup>(A, W, s0, nr, lane, pk, ps, inf_flag, cfg);
+      if (kDense) {
+        sell_group<kRowCheck, kSellGroup>(A, W, s0, nr, lane, pk, ps, inf_flag, cfg);
+      } else {
+        for (int r = 0; r < nr; ++r)
+          sell_slice<kRowCheck, 0, kDense>(A, W, A.slices[s0 + r], lane, full, rflag, pk, ps,
+                                           inf_flag, cfg);
+      }
     } else {
       const SliceDesc sd = A.slices[s];
       if (PG_SELL_LGMAX >= 3 && sd.lg == 3)
-        sell_slice<kRowCheck, 3>(A, W, sd, lane, pk, ps, inf_flag, cfg);
+        sell_slice<kRowCheck, (PG_SELL_LGMAX >= 3 ? 3 : 0), kDense>(A, W, sd, lane, full, rflag, pk, ps, inf_flag, cfg);
       else if (PG_SELL_LGMAX >= 2 && sd.lg == 2)
-        sell_slice<kRowCheck, 2>(A, W, sd, lane, pk, ps, inf_flag, cfg);
+        sell_slice<kRowCheck, (PG_SELL_LGMAX >= 2 ? 2 : 0), kDense>(A, W, sd, lane, full, rflag, pk, ps, inf_flag, cfg);
       else if (PG_SELL_LGMAX >= 1 && sd.lg == 1)
-        sell_slice<kRowCheck, 1>(A, W, sd, lane, pk, ps, inf_flag, cfg);
+        sell_slice<kRowCheck, (PG_SELL_LGMAX >= 1 ? 1 : 0), kDense>(A, W, sd, lane, full, rflag, pk, ps, inf_flag, cfg);
       else
-        sell_slice<kRowCheck, 0>(A, W, sd, lane, pk, ps, inf_flag, cfg);
+        sell_slice<kRowCheck, 0, kDense>(A, W, sd, lane, full, rflag, pk, ps, inf_flag, cfg);
     }
-    cur = __shfl_sync(0xffffffffu, nxt, 0);
+    next = __shfl_sync(0xffffffffu, nxt, 0);
   }
   if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
 }
@@ -918,7 +862,7 @@ __global__ void __launch_bounds__(kSellThreads, kDense ? PG_SELL_MINB_DENSE : PG
                                                                      const DevCfg cfg) {
   extern __shared__ __align__(16) unsigned char sell_dyn[];  // kSellWarps x SellWarpSmem
   SellWarpSmem* smem = reinterpret_cast<SellWarpSmem*>(sell_dyn);
-  if (compute_off(A.st)) return;
+  if (compute_off(A.st, cfg)) return;
   const bool dense = sell_dense_round(A);
   // the round's kind, for the commit kernels (written before any of them runs)
   if (kDense && blockIdx.x == 0 && threadIdx.x == 0) A.st->sparse_round = dense ? 0 : 1;

@@ -47,5 +47,8 @@ with Session(inst, cfg) as s:
     ns, b = s.time_round_kernel(a.reps)
     print(f"k_tiles {ns/1e3:.1f} us  {b/ns:.1f} GB/s")
     if a.solve:
-        r = s.run()
-        print(r.status, r.rounds_executed, r.elapsed_ns / 1e6, "ms")
+        best = None
+        for _ in range(5):
+            r = s.run()
+            best = r.elapsed_ns if best is None else min(best, r.elapsed_ns)
+        print(f"solve status={int(r.status)} rounds={r.rounds_executed} best={best/1e6:.3f} ms")
