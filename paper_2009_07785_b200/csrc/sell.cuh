@@ -178,7 +178,7 @@ __device__ __forceinline__ bool filt_may(const RowFilter& f, uint32_t b) {
 
 // ---- per-warp shared state ----------------------------------------------------------
 struct SellWarpSmem {
-  double min_f[32], max_f[32], lhs[32], rhs[32], tr[32], tl[32];
+  double min_f[32], max_f[32], lhs[32], rhs[32];
   int32_t min_i[32], max_i[32];
   uint8_t mode[32], may[32];
   // entries that survive the filter: element offset in the slice, unit
@@ -299,8 +299,6 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
       W.max_i[u] = act.max_i;
       W.lhs[u] = l;
       W.rhs[u] = h;
-      W.tr[u] = f.tr;
-      W.tl[u] = f.tl;
       W.mode[u] = f.mode;
     } else {
       chunk_done<kRowCheck>(A, ud, act, xmax, inf_flag, cfg);
@@ -314,7 +312,8 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
   __syncwarp();
   const bool umay = W.may[u] != 0;
   RowFilter f = {0.0, 0.0, 0};
-  if (umay) f = RowFilter{W.tr[u], W.tl[u], W.mode[u]};
+  // the row's filter again from its record (the same as at row finish)
+  if (umay) f = row_filter(Act{W.min_f[u], W.max_f[u], W.min_i[u], W.max_i[u]}, W.lhs[u], W.rhs[u]);
   int qn = 0;
   for (int t0 = 0; t0 < steps; t0 += kSellUnroll) {
     uint32_t b[kSellUnroll];
