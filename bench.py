@@ -170,12 +170,13 @@ def pinned_copy(inst):
 
 # ---- parity against the committed reference digests ---------------------------------
 
-def parity(config, seed, res):
+def parity(config, seed, res, key="cpu_par"):
     """The result against the reference propagate_parallel digest (the
-    timed configuration's own instance); 'unpinned' when no digest exists."""
+    timed configuration's own instance; key cpu_par_f32: Narrow32);
+    'unpinned' when no digest exists."""
     from instances import digest as D
     try:
-        want = D.load()[config][str(seed)]["cpu_par"]
+        want = D.load()[config][str(seed)][key]
     except (OSError, KeyError):
         return "unpinned (no reference digest for this instance)", None
     diffs = D.compare(res, want)
@@ -235,7 +236,7 @@ def run_reference(args, rank, world):
     }
 
 
-def cpu_baseline(inst, budget_s=25.0, lower=None, upper=None):
+def cpu_baseline(inst, budget_s=25.0, lower=None, upper=None, cfg=None):
     """cpu_seq of the reference (1 core), best of up to 3 solves within ~budget
     (harness default best-of-3, harness.hpp:75)."""
     from oracle import oracle as O
@@ -243,7 +244,7 @@ def cpu_baseline(inst, budget_s=25.0, lower=None, upper=None):
 
     ref = O.ref_available()
     fn = O.ref_propagate_sequential if ref else O.propagate_sequential
-    cfg = EngineConfig()
+    cfg = cfg or EngineConfig()
     best, res, t0, runs = None, None, time.perf_counter(), 0
     while runs < 3 and (runs == 0 or time.perf_counter() - t0 < budget_s):
         res = fn(inst, cfg, lower, upper)
@@ -327,10 +328,13 @@ def bench_single(args, world, rank, local, config):
     from paper_2009_07785_b200.engine import Session, propagate_gpu
     from paper_2009_07785_b200.model import EngineConfig, LoopMode
 
+    from paper_2009_07785_b200.model import ScalarMode
     seed = args.seed if args.seed is not None else SEEDS[config]
     inst = make_instance(config, seed)
-    worklist = args.worklist if args.worklist is not None else config in ("c2", "c5")
+    f32 = args.scalar == "f32"
+    worklist = (args.worklist if args.worklist is not None else config in ("c2", "c5")) and not f32
     cfg = EngineConfig(device=local, worklist=worklist,
+                       scalar_mode=ScalarMode.Narrow32 if f32 else ScalarMode.Wide64,
                        loop_mode=LoopMode.Host if args.loop == "host" else LoopMode.Graph)
     m, n, nnz = inst.num_rows(), inst.num_cols(), inst.matrix.nnz()
     sess = Session(inst, cfg)
@@ -358,7 +362,7 @@ def bench_single(args, world, rank, local, config):
 
     # the timed configuration's result (one more solve, bounds downloaded)
     # against the reference's own cpu_par digest
-    par, _ = parity(config, seed, sess.run(download=True))
+    par, _ = parity(config, seed, sess.run(download=True), "cpu_par_f32" if f32 else "cpu_par")
 
     # dominant kernels alone (roofline), first-round snapshot
     k_ns, k_bytes = sess.time_round_kernel(reps=20)
@@ -375,16 +379,18 @@ def bench_single(args, world, rank, local, config):
         re = propagate_gpu(pinned, cfg)
         e2e.append((time.perf_counter() - t1) * 1e3)
     e2e_ms = _max_over_ranks(torch, dist, world, local, float(np.median(e2e[1:])))
-    e2e_par, _ = parity(config, seed, re)
+    e2e_par, _ = parity(config, seed, re, "cpu_par_f32" if f32 else "cpu_par")
 
     line = _common_line(args, world, ms, "weak", config, {
         "instance": inst.name, "seed": seed, "m": m, "n": n, "nnz": nnz,
         "parallelism": f"replicas x{world}" if world > 1 else "single-gpu",
-        "worklist": worklist, "row_check": True,
+        "worklist": worklist, "row_check": True, "scalar": args.scalar,
         "l2": "flushed between steps (256 MB write); instance > L2" if config != "c1"
               else "flushed between steps (256 MB write)",
         "slices": info["slices"], "chains": info["chains"], "sell_elems": info["sell_elems"],
         "split_segments": info["segments"]})
+    if f32:
+        line["dtype"] = "f32 activities / candidates, f64 acceptance (ScalarMode::Narrow32)"
     line.update({
         "rounds": R, "status": r.status.name,
         "parity": par if par == e2e_par else f"timed: {par}; e2e: {e2e_par}",
@@ -415,7 +421,8 @@ def bench_single(args, world, rank, local, config):
         "clocks": clk.summary(),
     })
     if rank == 0 and not args.no_cpu_baseline:
-        cb, _ = cpu_baseline(inst, budget_s=args.cpu_budget_s)
+        cb, _ = cpu_baseline(inst, budget_s=args.cpu_budget_s,
+                             cfg=EngineConfig(scalar_mode=ScalarMode.Narrow32) if f32 else None)
         line["cpu_baseline"] = cb
         line["speedup_vs_cpu_seq"] = round(cb["value"] / ms, 2)
         line["e2e_speedup_vs_cpu_seq"] = round(cb["value"] / e2e_ms, 2)
@@ -763,6 +770,8 @@ def main():
                     help="device-side worklist (exact); default: on for c2, c4, c5, off for c1/c3")
     ap.add_argument("--delta", type=int, default=None,
                     help="c5: sparse delta exchange rounds (default: on when world > 1)")
+    ap.add_argument("--scalar", default="f64", choices=["f64", "f32"],
+                    help="f32: ScalarMode::Narrow32 (run_parallel<float>), c1-c3")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-also", action="store_true", help="N > 1: skip the C4 line under 'also'")
     ap.add_argument("--cpu-budget-s", type=float, default=25.0)

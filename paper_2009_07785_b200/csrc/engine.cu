@@ -49,6 +49,7 @@
 #include "loop.cuh"
 #include "nodes.cuh"
 #include "narrow.cuh"
+#include "narrow_sell.cuh"
 #include "ingest.cuh"
 
 using namespace pgb;
@@ -263,7 +264,9 @@ struct pg_session {
   int loop_grid = 0;     // co-resident CTAs of the persistent loop kernel
   int nodes_per_sm = 1;  // resident k_nodes CTAs per SM
   int32_t max_row_len = -1;  // lazily: max_len()
-  ActF* d_f32_part = nullptr;  // Narrow32: per-thread chunk partials
+  ActF* d_f32_part = nullptr;  // Narrow32: per-thread chunk partials (k_round_f32)
+  ActF* d_ractf = nullptr;     // Narrow32 over the sliced-ELL copy: row records
+  ActF* d_partf = nullptr;     //   and chunk partials (narrow_sell.cuh)
   int f32_maxc = 1;
 
   // device arrays
@@ -386,7 +389,7 @@ struct pg_session {
     if (h_dcnt) cudaFreeHost(h_dcnt);
     void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
                     d_lo_res, d_up_res, d_segs, d_srow, d_sfirst, d_partial,
-                    d_ract, d_wl_short, d_wl_long, d_f32_part, d_split, d_bnd, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
+                    d_ract, d_wl_short, d_wl_long, d_f32_part, d_ractf, d_partf, d_split, d_bnd, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
                     d_flags, d_chg, d_row_unit, d_part_unit, d_unit_slice, d_wide_list, d_unit_list, d_tflag, d_tlist};
     for (void* p : ptrs) dfree(p);  // stream-ordered: no device sync here
     if (h_st) cudaFreeHost(h_st);
@@ -461,7 +464,22 @@ struct pg_session {
     const bool rowcheck = (cfg.flags & PG_FLAG_ROWCHECK) != 0;
     const RoundArgs A = round_args();
     if (k1_begin) PG_CUDA(cudaEventRecord(k1_begin, stream));
-    if (cfg.scalar_mode == PG_NARROW32) {
+    if (cfg.scalar_mode == PG_NARROW32 && nslices > 0 && d_ractf) {
+      // float chains and candidates over the sliced-ELL copy (narrow_sell.cuh)
+      const int grid = std::max(1, std::min((nslices + 7) / 8, num_sms * sell_per_sm));
+      if (rowcheck)
+        k_sellf_act<true><<<grid, kSellThreads, 0, stream>>>(A, dcfg, d_ractf, d_partf);
+      else
+        k_sellf_act<false><<<grid, kSellThreads, 0, stream>>>(A, dcfg, d_ractf, d_partf);
+      if (nsplit > 0) {
+        const int g = std::max(1, std::min((nsplit + 127) / 128, num_sms * 4));
+        if (rowcheck)
+          k_sellf_split<true><<<g, 128, 0, stream>>>(A, d_split, nsplit, d_ractf, d_partf, dcfg);
+        else
+          k_sellf_split<false><<<g, 128, 0, stream>>>(A, d_split, nsplit, d_ractf, d_partf, dcfg);
+      }
+      k_sellf_cand<<<grid, kSellThreads, 0, stream>>>(A, dcfg, d_ractf);
+    } else if (cfg.scalar_mode == PG_NARROW32) {
       if (m > 0) {
         const int grid = grid_for(m, 256, 4);
         if (rowcheck)
@@ -1253,9 +1271,16 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       k_to_f32<<<s->grid_for(nnz, 256), 256, 0, st>>>(s->d_vals, nnz);
       k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_lhs, m);
       k_to_f32<<<s->grid_for(m, 256), 256, 0, st>>>(s->d_rhs, m);
-      const int chunk = cfg->nnz_budget;
-      s->f32_maxc = s->max_len() > chunk ? (s->max_len() + chunk - 1) / chunk : 1;
-      s->d_f32_part = dalloc<ActF>((size_t)s->grid_for(m, 256, 4) * 256 * s->f32_maxc);
+      // row records and chunk partials of the sliced-ELL float round
+      // (PG_F32_ROWS=1: the one-thread-per-row kernel instead, for A/B)
+      if (!getenv("PG_F32_ROWS")) {
+        s->d_ractf = dalloc<ActF>(std::max<int32_t>(m, 1));
+        s->d_partf = dalloc<ActF>(std::max<int32_t>(s->nseg, 1));
+      } else {
+        const int chunk = cfg->nnz_budget;
+        s->f32_maxc = s->max_len() > chunk ? (s->max_len() + chunk - 1) / chunk : 1;
+        s->d_f32_part = dalloc<ActF>((size_t)s->grid_for(m, 256, 4) * 256 * s->f32_maxc);
+      }
       PG_CUDA(cudaGetLastError());
     }
     if (s->nunits) {

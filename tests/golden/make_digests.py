@@ -32,7 +32,7 @@ sys.path.insert(0, ROOT)
 from instances import digest as D  # noqa: E402
 from instances import generators as G  # noqa: E402
 from oracle import oracle as O  # noqa: E402
-from paper_2009_07785_b200.model import EngineConfig  # noqa: E402
+from paper_2009_07785_b200.model import EngineConfig, ScalarMode  # noqa: E402
 
 THREADS = os.cpu_count() or 1
 PAR = EngineConfig(row_check=False, worker_count=THREADS)
@@ -52,7 +52,7 @@ def entry(inst, seq_verdict=True):
     return e, par
 
 
-def main(configs):
+def main(configs, only_f32=False):
     if not O.ref_available():
         sys.exit("oracle/_ref/libpropgate_ref.so missing: run oracle/build_ref.sh")
     out = D.load() if os.path.exists(D.DIGESTS) else {}
@@ -65,6 +65,11 @@ def main(configs):
             inst = G.config_instance(cfg, seed)
             # cpu_seq on C3 takes ~50 s: its verdict is the same Converged
             e, par = entry(inst, seq_verdict=cfg != "c3")
+            if cfg in ("c2", "c3") and str(seed) in ("20090778", "3001"):
+                # ScalarMode::Narrow32: the reference's run_parallel<float>
+                f32 = EngineConfig(row_check=False, worker_count=THREADS,
+                                   scalar_mode=ScalarMode.Narrow32)
+                e["cpu_par_f32"] = D.result_digest(O.ref_propagate_parallel(inst, f32))
             if cfg == "c4":
                 lo, up = G.gen_nodes(inst, par.bounds.lower, par.bounds.upper, K=C4_NODES)
                 nodes = []

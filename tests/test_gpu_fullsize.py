@@ -154,3 +154,16 @@ def test_mps_fixtures_on_gpu():
         rc = propagate_gpu(inst, EngineConfig(row_check=True))
         seq_inf = int(z[f"{name}/seq/status"]) == int(PropagationStatus.Infeasible)
         assert (rc.status == PropagationStatus.Infeasible) == seq_inf, name
+
+
+@pytest.mark.parametrize("cfg_name,seed", [("c2", 20090778), ("c3", 3001)])
+def test_narrow32_full_vs_reference(cfg_name, seed):
+    """ScalarMode::Narrow32 at full size over the sliced-ELL copy: the
+    reference's run_parallel<float> (float activities and candidates, double
+    acceptance) bit for bit -- C3 in float is Infeasible in round 1, as the
+    reference says."""
+    from paper_2009_07785_b200.model import ScalarMode
+    inst = instance(cfg_name, seed)
+    r = propagate_gpu(inst, EngineConfig(row_check=False, scalar_mode=ScalarMode.Narrow32))
+    diffs = D.compare(r, want(cfg_name, seed)["cpu_par_f32"])
+    assert not diffs, diffs
