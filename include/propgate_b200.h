@@ -37,6 +37,7 @@ extern "C" {
 #define PG_ENCCL (-4)   /* NCCL error (row-sharded multi-GPU path) */
 #define PG_ENODEV (-5)  /* no usable sm_100 device */
 #define PG_ERANGE (-6)  /* index out of range; reference throws std::out_of_range (core/src/model.cpp:40-45) */
+#define PG_EPARSE (-7)  /* MPS parse / file error; reference throws MpsError / std::runtime_error (core/src/mps.cpp) */
 
 /* ---- statuses: same order as propgate::PropagationStatus (model.hpp:112) */
 #define PG_CONVERGED 0
@@ -247,6 +248,33 @@ int pg_session_attach_comm(pg_session* s, const uint8_t* uid128, int32_t rank,
 #define PG_MULTI_ROWS 0
 int pg_multi_propagate(const pg_problem* prob, const pg_config* cfg, int32_t ngpus,
                        int32_t mode, pg_result* res);
+
+/* ---- MPS ingest ------------------------------------
+ * Replaces parse_mps_file / parse_mps (core/include/propgate/mps.hpp:28-31,
+ * core/src/mps.cpp:336-407): the same sections, row / bound semantics,
+ * column numbering, integrality markers, infinity normalisation and error
+ * messages ("mps parse error at line N: ...", PG_EPARSE).  The text is parsed
+ * on host threads (threads <= 0: all hardware threads); the matrix comes out
+ * as the triplets in file order, and pg_mps_to_csr builds the CSR on the
+ * device (pg_csr_from_triplets: csr_from_triplets' order and sums).  A read
+ * without a GPU is fine; only pg_mps_to_csr needs one. */
+typedef struct pg_mps pg_mps;
+int pg_mps_read(const char* path, double infinity_threshold, int32_t threads, pg_mps** out);
+int pg_mps_read_buffer(const char* text, int64_t size, double infinity_threshold, int32_t threads,
+                       pg_mps** out);
+/* dimensions and the triplet count; the name (NAME section, else the file name) */
+int pg_mps_dims(const pg_mps* h, int32_t* num_rows, int32_t* num_cols, int64_t* num_triplets);
+const char* pg_mps_name(const pg_mps* h);
+/* borrowed views, valid until pg_mps_free: triplets [num_triplets], lhs / rhs
+ * [num_rows], lower / upper / integral [num_cols] */
+int pg_mps_arrays(const pg_mps* h, const int32_t** rows, const int32_t** cols, const double** values,
+                  const double** lhs, const double** rhs, const double** lower, const double** upper,
+                  const uint8_t** integral);
+/* CSR of the triplets on `device`: row_ptr [num_rows + 1], col_idx / values
+ * [num_triplets] caller-allocated; *nnz receives the entry count */
+int pg_mps_to_csr(const pg_mps* h, int32_t device, int32_t* row_ptr, int32_t* col_idx,
+                  double* values, int64_t* nnz);
+void pg_mps_free(pg_mps* h);
 
 /* Session statistics, in this order: m, n, nnz, slices (sliced-ELL, 32
  * chains each), split-candidate rows (> 16 entries), segments (chains of

@@ -17,6 +17,7 @@ REPO_DIR = os.path.dirname(PKG_DIR)
 LIB_PATH = os.path.join(PKG_DIR, "libpropgate_b200.so")
 
 PG_OK, PG_EINVAL, PG_ENOMEM, PG_ECUDA, PG_ENCCL, PG_ENODEV, PG_ERANGE = 0, -1, -2, -3, -4, -5, -6
+PG_EPARSE = -7
 PG_CONVERGED, PG_ROUNDLIMIT, PG_INFEASIBLE = 0, 1, 2
 PG_MULTI_ROWS = 0
 PG_WIDE64, PG_NARROW32 = 0, 1
@@ -128,6 +129,15 @@ PROTOTYPES = {
                                      C.POINTER(PgResult)]),
     "pg_csr_from_triplets": (C.c_int, [C.c_int32, C.c_int32, C.c_int64, _ip, _ip, _dp, C.c_int32,
                                        _ip, _ip, _dp, _lp]),
+    "pg_mps_read": (C.c_int, [C.c_char_p, C.c_double, C.c_int32, C.POINTER(C.c_void_p)]),
+    "pg_mps_read_buffer": (C.c_int, [C.c_char_p, C.c_int64, C.c_double, C.c_int32,
+                                     C.POINTER(C.c_void_p)]),
+    "pg_mps_dims": (C.c_int, [C.c_void_p, _ip, _ip, _lp]),
+    "pg_mps_name": (C.c_char_p, [C.c_void_p]),
+    "pg_mps_arrays": (C.c_int, [C.c_void_p] + [C.POINTER(_ip)] * 2 + [C.POINTER(_dp)] * 5 +
+                      [C.POINTER(_up)]),
+    "pg_mps_to_csr": (C.c_int, [C.c_void_p, C.c_int32, _ip, _ip, _dp, _lp]),
+    "pg_mps_free": (None, [C.c_void_p]),
     "pg_last_error": (C.c_char_p, []),
     "pg_abi_version": (C.c_int32, []),
 }
@@ -160,6 +170,11 @@ def load_library(path: str | None = None):
     return lib
 
 
+class MpsError(RuntimeError):
+    """propgate::MpsError (core/include/propgate/mps.hpp:12-23) / the
+    reference's std::runtime_error for unreadable files."""
+
+
 def check(rc: int, what: str):
     if rc != PG_OK:
         msg = load_library().pg_last_error()
@@ -168,4 +183,6 @@ def check(rc: int, what: str):
             raise ValueError(f"{what}: {msg}")
         if rc == PG_ERANGE:  # std::out_of_range in the reference
             raise IndexError(f"{what}: {msg}")
+        if rc == PG_EPARSE:  # MpsError / std::runtime_error in the reference
+            raise MpsError(msg)
         raise EngineError(f"{what} failed ({rc}): {msg}")

@@ -51,6 +51,7 @@
 #include "narrow.cuh"
 #include "narrow_sell.cuh"
 #include "ingest.cuh"
+#include "mps_reader.h"
 
 using namespace pgb;
 
@@ -2298,3 +2299,131 @@ const char* pg_last_error(void) { return g_err.c_str(); }
 int32_t pg_abi_version(void) { return PG_ABI_VERSION; }
 
 }  // extern "C"
+
+// ---- MPS ingest (mps_reader.h) -----------------------------------------------------
+struct pg_mps {
+  std::vector<char> text;
+  pgmps::Problem p;
+};
+
+namespace {
+int mps_parse(pg_mps* h, double thr, int32_t threads) {
+  pgmps::Reader r;
+  r.buf = h->text.data();
+  r.size = (int64_t)h->text.size();
+  r.thr = thr;
+  const unsigned hw = std::thread::hardware_concurrency();
+  r.threads = threads > 0 ? threads : (int)(hw ? hw : 1);
+  try {
+    r.run();
+  } catch (const pgmps::Error& e) {
+    g_err = "mps parse error at line " +
+            std::to_string(pgmps::line_of(r.buf, r.size, e.offset)) + ": " + e.message;
+    return PG_EPARSE;
+  } catch (const std::bad_alloc&) {
+    g_err = "out of host memory while parsing MPS";
+    return PG_ENOMEM;
+  }
+  h->p = std::move(r.out);
+  return PG_OK;
+}
+}  // namespace
+
+int pg_mps_read_buffer(const char* text, int64_t size, double infinity_threshold, int32_t threads,
+                       pg_mps** out) {
+  if (!out || (size > 0 && !text) || size < 0) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  *out = nullptr;
+  pg_mps* h = new (std::nothrow) pg_mps;
+  if (!h) return PG_ENOMEM;
+  h->text.assign(text, text + size);
+  const int rc = mps_parse(h, infinity_threshold, threads);
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return PG_OK;
+}
+
+int pg_mps_read(const char* path, double infinity_threshold, int32_t threads, pg_mps** out) {
+  // parse_mps_file (mps.cpp:409-420)
+  if (!out || !path) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  *out = nullptr;
+  std::ifstream in(path, std::ios::binary | std::ios::ate);
+  if (!in) {
+    g_err = std::string("cannot open '") + path + "'";
+    return PG_EPARSE;
+  }
+  pg_mps* h = new (std::nothrow) pg_mps;
+  if (!h) return PG_ENOMEM;
+  const std::streamsize sz = in.tellg();
+  in.seekg(0);
+  h->text.resize((size_t)std::max<std::streamsize>(sz, 0));
+  if (sz > 0 && !in.read(h->text.data(), sz)) {
+    delete h;
+    g_err = std::string("cannot read '") + path + "'";
+    return PG_EPARSE;
+  }
+  const int rc = mps_parse(h, infinity_threshold, threads);
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  if (h->p.name.empty()) {
+    const std::string sp(path);
+    const size_t slash = sp.find_last_of('/');
+    h->p.name = slash == std::string::npos ? sp : sp.substr(slash + 1);
+  }
+  *out = h;
+  return PG_OK;
+}
+
+int pg_mps_dims(const pg_mps* h, int32_t* num_rows, int32_t* num_cols, int64_t* num_triplets) {
+  if (!h || !num_rows || !num_cols || !num_triplets) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  *num_rows = h->p.m;
+  *num_cols = h->p.n;
+  *num_triplets = (int64_t)h->p.rows.size();
+  return PG_OK;
+}
+
+const char* pg_mps_name(const pg_mps* h) { return h ? h->p.name.c_str() : ""; }
+
+int pg_mps_arrays(const pg_mps* h, const int32_t** rows, const int32_t** cols, const double** values,
+                  const double** lhs, const double** rhs, const double** lower, const double** upper,
+                  const uint8_t** integral) {
+  if (!h) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  if (rows) *rows = h->p.rows.data();
+  if (cols) *cols = h->p.cols.data();
+  if (values) *values = h->p.vals.data();
+  if (lhs) *lhs = h->p.lhs.data();
+  if (rhs) *rhs = h->p.rhs.data();
+  if (lower) *lower = h->p.lower.data();
+  if (upper) *upper = h->p.upper.data();
+  if (integral) *integral = h->p.integral.data();
+  return PG_OK;
+}
+
+int pg_mps_to_csr(const pg_mps* h, int32_t device, int32_t* row_ptr, int32_t* col_idx,
+                  double* values, int64_t* nnz) {
+  if (!h) {
+    g_err = "NULL argument";
+    return PG_EINVAL;
+  }
+  return pg_csr_from_triplets(h->p.m, h->p.n, (int64_t)h->p.rows.size(), h->p.rows.data(),
+                              h->p.cols.data(), h->p.vals.data(), device, row_ptr, col_idx, values,
+                              nnz);
+}
+
+void pg_mps_free(pg_mps* h) { delete h; }

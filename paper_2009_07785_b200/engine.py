@@ -17,6 +17,7 @@ CUDA library; there is no CPU path.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -79,6 +80,75 @@ def propagate_gpu(instance: ProblemInstance, cfg: EngineConfig | None = None) ->
     r, lo, up, prc = new_c_result(instance.num_cols(), cfg.round_limit)
     abi.check(_lib().pg_propagate(C.byref(p), C.byref(c), C.byref(r)), "pg_propagate")
     return result_from_c(r, lo, up, prc)
+
+
+class MpsFile:
+    """pg_mps_read: an MPS file parsed on host threads (mps_reader.h), the
+    triplets still in file order.  .instance(device) builds the CSR on the
+    GPU (pg_mps_to_csr)."""
+
+    def __init__(self, path: str | None = None, text: bytes | None = None,
+                 infinity_threshold: float = 1e20, threads: int = 0):
+        self._h = C.c_void_p()
+        if text is not None:
+            abi.check(_lib().pg_mps_read_buffer(text, len(text), infinity_threshold, threads,
+                                                C.byref(self._h)), "parse_mps")
+        else:
+            abi.check(_lib().pg_mps_read(os.fsencode(path), infinity_threshold, threads,
+                                         C.byref(self._h)), "parse_mps_file")
+        m, n, t = C.c_int32(), C.c_int32(), C.c_int64()
+        abi.check(_lib().pg_mps_dims(self._h, C.byref(m), C.byref(n), C.byref(t)), "pg_mps_dims")
+        self.m, self.n, self.ntrip = m.value, n.value, t.value
+        self.name = (_lib().pg_mps_name(self._h) or b"").decode()
+        ptrs = [C.POINTER(C.c_int32)(), C.POINTER(C.c_int32)()] + \
+            [C.POINTER(C.c_double)() for _ in range(5)] + [C.POINTER(C.c_uint8)()]
+        abi.check(_lib().pg_mps_arrays(self._h, *[C.byref(p) for p in ptrs]), "pg_mps_arrays")
+
+        def view(p, count, dt):
+            return np.ctypeslib.as_array(p, shape=(count,)).astype(dt, copy=True) if count else \
+                np.zeros(0, dt)
+        self.rows = view(ptrs[0], self.ntrip, np.int32)
+        self.cols = view(ptrs[1], self.ntrip, np.int32)
+        self.values = view(ptrs[2], self.ntrip, np.float64)
+        self.lhs = view(ptrs[3], self.m, np.float64)
+        self.rhs = view(ptrs[4], self.m, np.float64)
+        self.lower = view(ptrs[5], self.n, np.float64)
+        self.upper = view(ptrs[6], self.n, np.float64)
+        self.integral = view(ptrs[7], self.n, np.uint8)
+
+    def instance(self, device: int = 0) -> ProblemInstance:
+        rp = np.zeros(self.m + 1, dtype=np.int32)
+        ci = np.empty(max(self.ntrip, 1), dtype=np.int32)
+        vo = np.empty(max(self.ntrip, 1), dtype=np.float64)
+        nnz = C.c_int64()
+        abi.check(_lib().pg_mps_to_csr(self._h, device, abi.ptr(rp, C.c_int32),
+                                       abi.ptr(ci, C.c_int32), abi.ptr(vo, C.c_double),
+                                       C.byref(nnz)), "pg_mps_to_csr")
+        k = int(nnz.value)
+        return ProblemInstance.from_arrays(rp, ci[:k], vo[:k], self.lhs, self.rhs, self.lower,
+                                           self.upper, self.integral, num_cols=self.n,
+                                           name=self.name)
+
+    def close(self):
+        if self._h:
+            _lib().pg_mps_free(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def read_mps(path: str, infinity_threshold: float = 1e20, device: int = 0,
+             threads: int = 0) -> ProblemInstance:
+    """parse_mps_file (core/src/mps.cpp:409-420): host-parallel parse, CSR on the GPU."""
+    f = MpsFile(path, infinity_threshold=infinity_threshold, threads=threads)
+    try:
+        return f.instance(device)
+    finally:
+        f.close()
 
 
 @dataclass
