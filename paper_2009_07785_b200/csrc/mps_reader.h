@@ -24,7 +24,10 @@
 
 #include <algorithm>
 #include <charconv>
+#include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstdint>
 #include <cstring>
 #include <fstream>
@@ -315,7 +318,13 @@ struct Reader {
       start_state[k] = st;
       if (last_marker[k] >= 0) st = last_marker[k] == 1;
     }
+    static const bool timing = std::getenv("PG_MPS_TIMING") != nullptr;
+    auto t0 = std::chrono::steady_clock::now();
     run_parallel(nchunk, [&](int k) { parse_columns_chunk(ch[k], start_state[k] != 0); });
+    auto t1 = std::chrono::steady_clock::now();
+    if (timing)
+      std::fprintf(stderr, "[mps] COLUMNS %.1f MB in %d chunks: %.3f s\n", bytes / 1e6, nchunk,
+                   std::chrono::duration<double>(t1 - t0).count());
     // the first error in file order (chunks are in file order)
     for (int k = 0; k < nchunk; ++k)
       if (ch[k].err) throw ch[k].error;
@@ -440,7 +449,11 @@ struct Reader {
       }
     }
     if (!endata) throw Error{-1, "missing ENDATA"};  // the line count (getline's last line)
+    auto f0 = std::chrono::steady_clock::now();
     finish();
+    if (std::getenv("PG_MPS_TIMING"))
+      std::fprintf(stderr, "[mps] finish %.3f s\n",
+                   std::chrono::duration<double>(std::chrono::steady_clock::now() - f0).count());
   }
 
   // finish (mps.cpp:232-330): sides by row type, RANGES, bounds in order

@@ -49,17 +49,17 @@ def write(inst, path):
             l, h = inst.lhs[i], inst.rhs[i]
             side = l if kinds[i] == "G" or kinds[i] == "E" else h
             if np.isfinite(side):
-                f.write(f"    rhs r{i} {side!r}\n")
+                f.write(f"    rhs r{i} {float(side)!r}\n")
         f.write("RANGES\n")
         for i in range(m):
             l, h = inst.lhs[i], inst.rhs[i]
             if kinds[i] == "L" and np.isfinite(l) and np.isfinite(h):
-                f.write(f"    rng r{i} {h - l!r}\n")
+                f.write(f"    rng r{i} {float(h - l)!r}\n")
         f.write("BOUNDS\n")
         for j in range(n):
             lo, up = inst.bounds.lower[j], inst.bounds.upper[j]
-            f.write(f" LO b x{j} {lo!r}\n" if np.isfinite(lo) else f" MI b x{j}\n")
-            f.write(f" UP b x{j} {up!r}\n" if np.isfinite(up) else f" PL b x{j}\n")
+            f.write(f" LO b x{j} {float(lo)!r}\n" if np.isfinite(lo) else f" MI b x{j}\n")
+            f.write(f" UP b x{j} {float(up)!r}\n" if np.isfinite(up) else f" PL b x{j}\n")
         f.write("ENDATA\n")
 
 
@@ -74,6 +74,9 @@ def main(out, cfg):
     t = time.perf_counter()
     ref = O.ref_parse_mps(path)
     ref_s = time.perf_counter() - t
+    # the CUDA context exists before the timed region (one tiny device CSR build)
+    from paper_2009_07785_b200.engine import csr_from_triplets_gpu
+    csr_from_triplets_gpu(np.zeros(1, np.int32), np.zeros(1, np.int32), np.ones(1), 1, 1)
     t = time.perf_counter()
     f = MpsFile(path)
     parse_s = time.perf_counter() - t
