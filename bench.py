@@ -599,8 +599,10 @@ def bench_rowshard(args, world, rank, local):
     info = rs.session.info()
     R = r.rounds_executed
     # parity: the row-sharded result against the reference cpu_par digest
-    # (= the 1-GPU result: merges are exact and rows are never split)
-    par, _ = parity("c5", seed, rs.run(download=True))
+    # (= the 1-GPU result: merges are exact and rows are never split); a
+    # collective solve, so every rank runs it
+    sharded = rs.run(download=True)
+    par, _ = parity("c5", seed, sharded)
 
     # e2e: a one-shot call per rank from pinned host arrays -- this rank's
     # shard uploaded, device setup, communicator, solve, bounds downloaded
@@ -663,7 +665,7 @@ def bench_rowshard(args, world, rank, local):
                 t1.append(s1.run().elapsed_ns / 1e6)
             r1 = s1.run(download=True)
             from instances import digest as D
-            same = D.result_digest(r1) == D.result_digest(rs.run(download=True))
+            same = D.result_digest(r1) == D.result_digest(sharded)
             single = {"value": round(float(np.mean(t1)), 4), "unit": "ms",
                       "rounds": r1.rounds_executed, "bit_identical_to_sharded": same}
             s1.close()

@@ -623,6 +623,16 @@ struct pg_session {
   // persistent round loop (loop.cuh): small instances and worklist solves,
   // whose rounds are launch-latency bound; never with a communicator (the
   // all-reduce is a host-enqueued NCCL call between phases)
+  // the hybrid loop: per-kernel rounds while they are full sweeps, then the
+  // persistent kernel for the worklist tail (instances above the persistent
+  // threshold, worklist on; PG_HYBRID=1 enables)
+  bool use_hybrid() const {
+    // measured slower on C2 / C5 (1.61 -> 1.78 ms, 10.1 -> 14.5 ms): opt-in
+    static const bool on = getenv("PG_HYBRID") && atoi(getenv("PG_HYBRID")) != 0;
+    return on && !comm && loop_grid > 0 && cfg.scalar_mode != PG_NARROW32 && dirty.enabled &&
+           !use_persistent();
+  }
+
   bool use_persistent() const {
     if (comm || loop_grid <= 0 || cfg.scalar_mode == PG_NARROW32) return false;
     static const long long thr = [] {
@@ -783,8 +793,21 @@ struct pg_session {
     PG_CUDA(cudaStreamBeginCaptureToGraph(stream, body, nullptr, nullptr, 0,
                                           cudaStreamCaptureModeThreadLocal));
     enqueue_round(true);
+    const bool hybrid = use_hybrid();
+    if (hybrid) {
+      k_hybrid_decide<<<1, 32, 0, stream>>>(d_st, dirty, cond);
+      PG_CUDA(cudaGetLastError());
+    }
     cudaGraph_t body2 = nullptr;
     PG_CUDA(cudaStreamEndCapture(stream, &body2));
+    if (hybrid) {
+      // node 3: the persistent kernel finishes the solve (returns at once if done)
+      cudaGraph_t g3 = nullptr;
+      PG_CUDA(cudaStreamBeginCaptureToGraph(stream, graph, &while_node, nullptr, 1,
+                                            cudaStreamCaptureModeThreadLocal));
+      enqueue_persistent();
+      PG_CUDA(cudaStreamEndCapture(stream, &g3));
+    }
     PG_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   }
 

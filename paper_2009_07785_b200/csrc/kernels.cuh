@@ -802,6 +802,17 @@ __global__ void k_shard_resume(DevState* __restrict__ st) {
   }
 }
 
+// Hybrid loop (engine.cu build_graph): the graph's WHILE rounds run while
+// the rounds are full sweeps; once the next round would be a worklist round
+// the loop hands over to the persistent kernel (k_loop), whose rounds are
+// separated by grid barriers instead of half a dozen launches.  Runs after
+// the round's marks, when the next round's kind is known.
+__global__ void k_hybrid_decide(DevState* __restrict__ st, const Dirty D,
+                                cudaGraphConditionalHandle cond) {
+  if (threadIdx.x == 0 && !ld_gpu(&st->done) && round_is_sparse(st, D))
+    cudaGraphSetConditional(cond, 0u);
+}
+
 // keys -> doubles (result download)
 __global__ void k_decode(const longlong2* __restrict__ key, double* __restrict__ lo,
                          double* __restrict__ up, int n) {
