@@ -157,29 +157,56 @@ __device__ __forceinline__ void ld_col(const RA& A, int32_t c, uint64_t pol, boo
 }
 
 // ---- filter words -----------------------------------------------------------------
-// |a| q rounded toward +inf to float; bit 0 = min contribution infinite,
-// bit 1 = max contribution infinite.  +inf / NaN terms read back as NaN,
-// which every threshold test passes.
-// (+inf keeps its exponent; decoding sets the low bits of a positive word,
-// so it reads back as NaN)
-__device__ __forceinline__ uint32_t filt_encode(double x, bool imin, bool imax) {
-  const uint32_t b = __float_as_uint(__double2float_ru(x));
-  return (b & ~3u) | (imin ? 1u : 0u) | (imax ? 2u : 0u);
+// Per entry a 32-bit word: the filter term x = |a| q rounded up to float as
+// a monotone int32 key (negative floats bit-reversed), the two low bits
+// replaced by the infinity flags (bit 0: min contribution infinite, bit 1:
+// max contribution infinite).  (w | 3) is the key of a float >= x, the row
+// thresholds are keyed after rounding down, so a test on a word is never
+// stricter than the exact one (kernels.cuh entry_may) and all tests are
+// integer compares.  A NaN term (a = 0 with an infinite bound, which never
+// yields a candidate) keys as -inf, so it cannot mask the row's maximum.
+__device__ __forceinline__ int32_t fkey_of(float f) {
+  const int32_t b = __float_as_int(f);
+  return b ^ ((b >> 31) & 0x7fffffff);
 }
-// a value >= the encoded term (low bits set for positive, cleared for negative)
-__device__ __forceinline__ double filt_term(uint32_t b) {
-  return (double)__uint_as_float((b & 0x80000000u) ? (b & ~3u) : (b | 3u));
+constexpr int32_t kFKeyMin = (int32_t)0x807fffff;  // key of -inf: the empty maximum
+__device__ __forceinline__ int32_t fword(double x, bool imin, bool imax) {
+  const float f = fmaxf(__double2float_ru(x), -CUDART_INF_F);
+  return (fkey_of(f) & ~3) | (imin ? 1 : 0) | (imax ? 2 : 0);
 }
-__device__ __forceinline__ bool filt_may(const RowFilter& f, uint32_t b) {
-  const double x = filt_term(b);
-  return ((f.mode & 1) && !(f.tr > x)) || ((f.mode & 2) && !(f.tl > x)) ||
-         ((f.mode & 4) && (b & 1u)) || ((f.mode & 8) && (b & 2u));
+// a double >= every term behind the largest word xk (+inf's key | 3 is a NaN pattern)
+__device__ __forceinline__ double fkey_bound(int32_t xk) {
+  const int32_t k = xk | 3;
+  const float f = __int_as_float(k ^ ((k >> 31) & 0x7fffffff));
+  return f == f ? (double)f : CUDART_INF;
 }
+// per-unit form of the row filter: each enabled side's threshold rounded
+// down to float and keyed (a disabled side keys above every word), and the
+// flag mask of the one-infinite-entry sides
+struct FTest {
+  int32_t tr, tl, fm;
+};
+__device__ __forceinline__ FTest ftest(const RowFilter& f) {
+  FTest r;
+  r.tr = (f.mode & 1) ? fkey_of(__double2float_rd(f.tr)) : 0x7fffffff;
+  r.tl = (f.mode & 2) ? fkey_of(__double2float_rd(f.tl)) : 0x7fffffff;
+  r.fm = ((f.mode & 4) ? 1 : 0) | ((f.mode & 8) ? 2 : 0);
+  return r;
+}
+__device__ __forceinline__ bool fpass(const FTest& t, int32_t w) {
+  const int32_t x = w | 3;
+  return x >= t.tr || x >= t.tl || (w & t.fm) != 0;
+}
+__device__ __forceinline__ bool frow_may(const FTest& t, int32_t xk) {
+  return t.fm != 0 || (xk | 3) >= min(t.tr, t.tl);
+}
+__device__ __forceinline__ bool is_inf(double x) { return fabs(x) == CUDART_INF; }
 
 // ---- per-warp shared state ----------------------------------------------------------
 struct SellWarpSmem {
   double min_f[32], max_f[32], lhs[32], rhs[32];
   int32_t min_i[32], max_i[32];
+  int32_t tkr[32], tkl[32], fmask[32];
   uint8_t mode[32], may[32];
   // entries that survive the filter: element offset in the slice, unit
   int32_t qe[64];
@@ -222,18 +249,18 @@ __device__ __forceinline__ bool sell_drain(const RA& A, const SellWarpSmem& W,
 // added in entry order (every lane of the unit forms the same sum).
 template <int LG>
 __device__ __forceinline__ void sell_step(double a, double lo, double up, double q, int u, Act& act,
-                                          double& xmax, uint32_t* pw) {
+                                          int32_t& xk, int32_t* pw) {
   constexpr int G = 1 << LG, H = 32 >> LG;
   const double bmin = a > 0 ? lo : up;
   const double bmax = a > 0 ? up : lo;
-  const bool imin = isinf(bmin), imax = isinf(bmax);
+  const bool imin = is_inf(bmin), imax = is_inf(bmax);
   const double pmin = imin ? 0.0 : __dmul_rn(a, bmin);
   const double pmax = imax ? 0.0 : __dmul_rn(a, bmax);
   act.min_i += imin;
   act.max_i += imax;
-  const double x = fabs(a) * q;
-  xmax = fmax(xmax, x);
-  *pw = filt_encode(x, imin, imax);
+  const int32_t w = fword(fabs(a) * q, imin, imax);
+  xk = max(xk, w);
+  *pw = w;
   if (LG == 0) {
     act.min_f = __dadd_rn(act.min_f, pmin);
     act.max_f = __dadd_rn(act.max_f, pmax);
@@ -270,19 +297,19 @@ __device__ __forceinline__ void chunk_done(const RoundArgs& A, const UnitDesc& u
 template <bool kRowCheck, int LG, class RA>
 __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const SliceDesc& sd,
                                            const UnitDesc& ud, bool active, int len, int lane,
-                                           Act act, double xmax, double lhs_r, double rhs_r,
+                                           Act act, int32_t xk, double lhs_r, double rhs_r,
                                            uint64_t pol_keep, bool& inf_flag, const DevCfg& cfg) {
   constexpr int H = 32 >> LG;
   const int j = lane >> (5 - LG), u = lane & (H - 1);
   const bool whole = ud.ref >= 0;
   const int steps = sd.steps;
-  uint32_t* sw = A.sw + sd.off + lane;
+  const int32_t* sw = reinterpret_cast<const int32_t*>(A.sw) + sd.off + lane;
   // order-free parts over the unit's lanes
 #pragma unroll
   for (int o = H; o < 32; o <<= 1) {
     act.min_i += __shfl_xor_sync(0xffffffffu, act.min_i, o);
     act.max_i += __shfl_xor_sync(0xffffffffu, act.max_i, o);
-    xmax = fmax(xmax, __shfl_xor_sync(0xffffffffu, xmax, o));
+    xk = max(xk, __shfl_xor_sync(0xffffffffu, xk, o));
   }
 
   // ---- row finish (owner lanes) ----------------------------------------------------
@@ -292,7 +319,11 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
       const double l = lhs_r, h = rhs_r;
       if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
       const RowFilter f = row_filter(act, l, h);
-      may = row_may(f, xmax);
+      const FTest ft = ftest(f);
+      may = frow_may(ft, xk);
+      W.tkr[u] = ft.tr;
+      W.tkl[u] = ft.tl;
+      W.fmask[u] = ft.fm;
       W.min_f[u] = act.min_f;
       W.max_f[u] = act.max_f;
       W.min_i[u] = act.min_i;
@@ -301,7 +332,7 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
       W.rhs[u] = h;
       W.mode[u] = f.mode;
     } else {
-      chunk_done<kRowCheck>(A, ud, act, xmax, inf_flag, cfg);
+      chunk_done<kRowCheck>(A, ud, act, fkey_bound(xk), inf_flag, cfg);
     }
   }
   if (j == 0) W.may[u] = may;
@@ -311,21 +342,20 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
   // ---- phase 2: filter words -> queue -> exact pipeline ------------------------------
   __syncwarp();
   const bool umay = W.may[u] != 0;
-  RowFilter f = {0.0, 0.0, 0};
-  // the row's filter again from its record (the same as at row finish)
-  if (umay) f = row_filter(Act{W.min_f[u], W.max_f[u], W.min_i[u], W.max_i[u]}, W.lhs[u], W.rhs[u]);
+  FTest ft = {0x7fffffff, 0x7fffffff, 0};
+  if (umay) ft = FTest{W.tkr[u], W.tkl[u], W.fmask[u]};
   int qn = 0;
   for (int t0 = 0; t0 < steps; t0 += kSellUnroll) {
-    uint32_t b[kSellUnroll];
+    int32_t b[kSellUnroll];
     bool in[kSellUnroll];
 #pragma unroll
     for (int k = 0; k < kSellUnroll; ++k) {
       in[k] = umay && ((t0 + k) << LG) + j < len;
-      b[k] = in[k] ? sw[32 * (t0 + k)] : 0u;
+      b[k] = in[k] ? sw[32 * (t0 + k)] : 0;
     }
 #pragma unroll
     for (int k = 0; k < kSellUnroll; ++k) {
-      const bool pass = in[k] && filt_may(f, b[k]);
+      const bool pass = in[k] && fpass(ft, b[k]);
       const unsigned m = __ballot_sync(0xffffffffu, pass);
       if (!m) continue;
       if (pass) {
@@ -376,20 +406,20 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
   const int len = active ? ud.len : 0;
   const double* sv = A.sv + sd.off + lane;
   const int32_t* sc = A.sc + sd.off + lane;
-  uint32_t* sw = A.sw + sd.off + lane;
+  int32_t* sw = reinterpret_cast<int32_t*>(A.sw) + sd.off + lane;
   const int steps = sd.steps;
   const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
 
   // ---- phase 1: the chains ------------------------------------------------------
   Act act = {0.0, 0.0, 0, 0};
-  double xmax = -CUDART_INF;
+  int32_t xk = kFKeyMin;
   if (kDense) {
     constexpr int UL = LG >= PG_SELL_LGU ? PG_SELL_ULONG : kSellUnroll;
     // every lane walks all `steps` of the slice: entries past a unit's end are
     // padding (value 0, the padding column with bounds [0, 0]) and add +0.0
     const double* pa = sv;
     const int32_t* pc = sc;
-    uint32_t* pw = sw;
+    int32_t* pw = sw;
     int t = 0;
     double a[UL];
     int32_t c[UL];
@@ -424,7 +454,7 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
       }
 #pragma unroll
       for (int k = 0; k < UL; ++k)
-        sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xmax, pw + 32 * k);
+        sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xk, pw + 32 * k);
 #pragma unroll
       for (int k = 0; k < UL; ++k) {
         a[k] = an[k];
@@ -439,7 +469,7 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
       const int32_t c1 = ld_stream_s32(pc, pol_stream);
       double lo1, up1, q1;
       ld_col(A, c1, pol_keep, frac_any, cfg, lo1, up1, q1);
-      sell_step<LG>(a1, lo1, up1, q1, u, act, xmax, pw);
+      sell_step<LG>(a1, lo1, up1, q1, u, act, xk, pw);
       pa += 32;
       pc += 32;
       pw += 32;
@@ -465,14 +495,14 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
         ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
 #pragma unroll
       for (int k = 0; k < kSellUnroll; ++k)
-        if (t0 + k < steps) sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xmax, sw + 32 * (t0 + k));
+        if (t0 + k < steps) sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xk, sw + 32 * (t0 + k));
     }
   }
   if (PG_SELL_DEBUG && (cfg.flags & 0x40000u)) {  // timing experiments only: chains alone
-    if (act.min_f == 12345.678 && xmax == 1.0) A.st->infeasible = 1;
+    if (act.min_f == 12345.678 && xk == 1) A.st->infeasible = 1;
     return;
   }
-  slice_tail<kRowCheck, LG>(A, W, sd, ud, active, len, lane, act, xmax, ud.ref >= 0 ? A.lhs[ud.ref] : 0.0,
+  slice_tail<kRowCheck, LG>(A, W, sd, ud, active, len, lane, act, xk, ud.ref >= 0 ? A.lhs[ud.ref] : 0.0,
                             ud.ref >= 0 ? A.rhs[ud.ref] : 0.0, pol_keep, inf_flag, cfg);
 }
 
@@ -507,11 +537,11 @@ __device__ __forceinline__ void sell_group(const RA& A, SellWarpSmem& W, int s0,
     }
   }
   Act act[R];
-  double xmax[R];
+  int32_t xk[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     act[r] = Act{0.0, 0.0, 0, 0};
-    xmax[r] = -CUDART_INF;
+    xk[r] = kFKeyMin;
   }
   const int tmax = steps[0];  // the group's first slice is its widest
   const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
@@ -543,7 +573,7 @@ __device__ __forceinline__ void sell_group(const RA& A, SellWarpSmem& W, int s0,
     }
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (t < steps[r]) sell_step<0>(a[r], lo[r], up[r], q[r], lane, act[r], xmax[r], A.sw + off[r] + 32 * t);
+      if (t < steps[r]) sell_step<0>(a[r], lo[r], up[r], q[r], lane, act[r], xk[r], reinterpret_cast<int32_t*>(A.sw) + off[r] + 32 * t);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       a[r] = an[r];
@@ -554,7 +584,7 @@ __device__ __forceinline__ void sell_group(const RA& A, SellWarpSmem& W, int s0,
   for (int r = 0; r < R; ++r) {
     if (r < nr) {
       const SliceDesc d = {off[r] - lane, 0, 0, steps[r], (int16_t)cnt[r], 0, 0};
-      slice_tail<kRowCheck, 0>(A, W, d, ud[r], lane < cnt[r], ud[r].len, lane, act[r], xmax[r],
+      slice_tail<kRowCheck, 0>(A, W, d, ud[r], lane < cnt[r], ud[r].len, lane, act[r], xk[r],
                                l[r], h[r], pol_keep, inf_flag, cfg);
     }
   }
@@ -735,9 +765,9 @@ __device__ __forceinline__ void sell_units(const RA& A, int par, uint64_t pol_ke
     const long long off = A.slices[A.lg0_sstart + (k >> 5)].off + (k & 31);
     const double* sv = A.sv + off;
     const int32_t* sc = A.sc + off;
-    uint32_t* sw = A.sw + off;
+    int32_t* sw = reinterpret_cast<int32_t*>(A.sw) + off;
     Act act = {0.0, 0.0, 0, 0};
-    double xmax = -CUDART_INF;
+    int32_t xk = kFKeyMin;
     for (int t0 = 0; t0 < ud.len; t0 += 4) {
       double a[4], lo[4], up[4], q[4];
       int32_t c[4];
@@ -754,23 +784,23 @@ __device__ __forceinline__ void sell_units(const RA& A, int par, uint64_t pol_ke
       for (int k = 0; k < 4; ++k) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        if (t0 + k < ud.len) sell_step<0>(a[k], lo[k], up[k], q[k], 0, act, xmax, sw + 32 * (t0 + k));
+        if (t0 + k < ud.len) sell_step<0>(a[k], lo[k], up[k], q[k], 0, act, xk, sw + 32 * (t0 + k));
     }
     if (ud.ref < 0) {
-      chunk_done<kRowCheck>(A, ud, act, xmax, inf_flag, cfg);
+      chunk_done<kRowCheck>(A, ud, act, fkey_bound(xk), inf_flag, cfg);
       continue;
     }
     const double l = A.lhs[ud.ref], h = A.rhs[ud.ref];
     if (kRowCheck && row_infeasible(act, l, h, cfg)) inf_flag = true;
-    const RowFilter f = row_filter(act, l, h);
-    if (!row_may(f, xmax)) continue;
+    const FTest ft = ftest(row_filter(act, l, h));
+    if (!frow_may(ft, xk)) continue;
     for (int t0 = 0; t0 < ud.len; t0 += 4) {
       // four entries' filter words, then the survivors' loads, then pipelines
       bool pass[4];
       double a[4], lo[4], up[4], q[4];
       int32_t c[4];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) pass[k] = t0 + k < ud.len && filt_may(f, sw[32 * (t0 + k)]);
+      for (int k = 0; k < 4; ++k) pass[k] = t0 + k < ud.len && fpass(ft, sw[32 * (t0 + k)]);
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         a[k] = 0.0;
