@@ -60,8 +60,13 @@ def main():
             ok = st[k] == int(ref.status) and np.array_equal(O.canon(blo[k]), O.canon(ref.bounds.lower))
             bad += not ok
         print(("ok  " if bad == 0 else "BAD ") + "nodes x12", flush=True)
-    f32 = EngineConfig(row_check=False, scalar_mode=ScalarMode.Narrow32)
-    bad += not same(propagate_gpu(r, f32), O.propagate_parallel(r, f32), "narrow32")
+    # the Narrow32 kernels (narrow_sell.cuh) use no shared memory, so
+    # racecheck has nothing to check there -- and its instrumentation of them
+    # takes the host process down (SIGSEGV inside the tool): skipped under
+    # racecheck only (PG_SANITIZE_NO_F32=1)
+    if not os.environ.get("PG_SANITIZE_NO_F32"):
+        f32 = EngineConfig(row_check=False, scalar_mode=ScalarMode.Narrow32)
+        bad += not same(propagate_gpu(r, f32), O.propagate_parallel(r, f32), "narrow32")
     try:
         from paper_2009_07785_b200.multi import RowShardedSession
         for delta in (False, True):
