@@ -158,6 +158,32 @@ struct PhaseTimer {
   }
 };
 
+// PG_TIMING: device-side timeline of a one-shot call (events on the
+// streams named at each mark), printed relative to the first mark
+struct GpuTrace {
+  bool on = getenv("PG_TIMING") != nullptr;
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+  void mark(const char* what, cudaStream_t q) {
+    if (!on) return;
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    cudaEventRecord(e, q);
+    ev.emplace_back(what, e);
+  }
+  void dump() {
+    if (!on || ev.empty()) return;
+    for (auto& x : ev) {
+      cudaEventSynchronize(x.second);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[0].second, x.second);
+      fprintf(stderr, "[pg gpu] %-28s %8.3f ms\n", x.first, ms);
+    }
+    for (auto& x : ev) cudaEventDestroy(x.second);
+    ev.clear();
+  }
+};
+thread_local GpuTrace g_trace;
+
 // NCCL, loaded on first use (the single-GPU engine has no NCCL dependency).
 // Values from nccl.h: ncclInt64 = 4, ncclMax = 2; ncclUniqueId = 128 bytes.
 constexpr int kNcclInt64 = 4;
@@ -206,9 +232,13 @@ Nccl g_nccl;
 // Streams and events of finished sessions, kept per device for the next
 // session (creating them costs ~0.1 ms per one-shot call).  Pending
 // stream-ordered work on a returned stream simply precedes the next user's.
+// The set also carries the session's pinned DevState mirror: cudaFreeHost
+// synchronises the whole device, so a one-shot call's reaper freeing it
+// would stall the next call's setup behind its own upload.
 struct StreamSet {
   cudaStream_t st = nullptr, st2 = nullptr;
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, fork = nullptr, join = nullptr;
+  DevState* h_st = nullptr;  // pinned
 };
 struct StreamPool {
   std::mutex mu;
@@ -229,13 +259,14 @@ struct StreamPool {
     PG_CUDA(cudaEventCreate(&x.ev1));
     PG_CUDA(cudaEventCreateWithFlags(&x.fork, cudaEventDisableTiming));
     PG_CUDA(cudaEventCreateWithFlags(&x.join, cudaEventDisableTiming));
+    PG_CUDA(cudaMallocHost(&x.h_st, sizeof(DevState)));
     return x;
   }
   void put(int dev, const StreamSet& x) {
     {
       std::lock_guard<std::mutex> lk(mu);
       if (dev >= 0 && dev < 64 && free_sets[dev].size() < 4 && x.st && x.st2 && x.ev0 && x.ev1 &&
-          x.fork && x.join) {
+          x.fork && x.join && x.h_st) {
         free_sets[dev].push_back(x);
         return;
       }
@@ -244,6 +275,7 @@ struct StreamPool {
       if (e) cudaEventDestroy(e);
     for (cudaStream_t q : {x.st, x.st2})
       if (q) cudaStreamDestroy(q);
+    if (x.h_st) cudaFreeHost(x.h_st);
   }
   static StreamPool& get() {
     static StreamPool* p = new StreamPool;  // never destroyed (reaper thread)
@@ -384,17 +416,33 @@ struct pg_session {
     destroy_shard_graphs();
 
     if (comm && !comm_aborted) g_nccl.comm_destroy(comm);  // an aborted one is freed already
-    for (void* p : {(void*)d_ctl, (void*)d_root_lo, (void*)d_root_up, (void*)d_keep_lo, (void*)d_keep_up, (void*)d_delta,
-                    (void*)d_delta_all, (void*)d_dcnt, (void*)d_dcnt_all})
-      dfree(p);
+    release_buffers();
     if (h_dcnt) cudaFreeHost(h_dcnt);
-    void* ptrs[] = {d_row_ptr, d_colx, d_vals, d_lhs, d_rhs, d_snap, d_integral, d_row_done, d_key_out, d_lo0, d_up0,
-                    d_lo_res, d_up_res, d_segs, d_srow, d_sfirst, d_partial,
-                    d_ract, d_wl_short, d_wl_long, d_f32_part, d_ractf, d_partf, d_split, d_bnd, d_units, d_slices, d_sv, d_sc, d_sw, d_st, d_per_round, d_col_ptr, d_col_item,
-                    d_flags, d_chg, d_row_unit, d_part_unit, d_unit_slice, d_wide_list, d_unit_list, d_tflag, d_tlist};
-    for (void* p : ptrs) dfree(p);  // stream-ordered: no device sync here
-    if (h_st) cudaFreeHost(h_st);
-    StreamPool::get().put(dev, StreamSet{stream, stream2, ev0, ev1, ev_fork, ev_join});
+    StreamPool::get().put(dev, StreamSet{stream, stream2, ev0, ev1, ev_fork, ev_join, h_st});
+  }
+
+  // device buffers back to the pool (stream-ordered, no device sync; a few
+  // microseconds of host time): a one-shot call does this itself so the next
+  // call's allocations reuse the memory instead of growing the pool while
+  // the reaper thread still holds the session
+  void release_buffers() {
+    t_alloc_stream = stream;
+    void** ptrs[] = {
+        (void**)&d_ctl, (void**)&d_root_lo, (void**)&d_root_up, (void**)&d_keep_lo, (void**)&d_keep_up,
+        (void**)&d_delta, (void**)&d_delta_all, (void**)&d_dcnt, (void**)&d_dcnt_all, (void**)&d_row_ptr,
+        (void**)&d_colx, (void**)&d_vals, (void**)&d_lhs, (void**)&d_rhs, (void**)&d_snap,
+        (void**)&d_integral, (void**)&d_row_done, (void**)&d_key_out, (void**)&d_lo0, (void**)&d_up0,
+        (void**)&d_lo_res, (void**)&d_up_res, (void**)&d_segs, (void**)&d_srow, (void**)&d_sfirst,
+        (void**)&d_partial, (void**)&d_ract, (void**)&d_wl_short, (void**)&d_wl_long,
+        (void**)&d_f32_part, (void**)&d_ractf, (void**)&d_partf, (void**)&d_split, (void**)&d_bnd,
+        (void**)&d_units, (void**)&d_slices, (void**)&d_sv, (void**)&d_sc, (void**)&d_sw, (void**)&d_st,
+        (void**)&d_per_round, (void**)&d_col_ptr, (void**)&d_col_item, (void**)&d_flags, (void**)&d_chg,
+        (void**)&d_row_unit, (void**)&d_part_unit, (void**)&d_unit_slice, (void**)&d_wide_list,
+        (void**)&d_unit_list, (void**)&d_tflag, (void**)&d_tlist};
+    for (void** p : ptrs) {
+      dfree(*p);
+      *p = nullptr;
+    }
   }
 
   int grid_for(int64_t items, int threads, int per_sm = 8) const {
@@ -825,8 +873,10 @@ struct pg_session {
       PG_CUDA(cudaEventRecord(ev1, stream));
     } else if (cfg.loop_mode == PG_LOOP_GRAPH && check_crossed && !delta_mode()) {
       PG_CUDA(cudaEventRecord(ev0, stream));
+      g_trace.mark("solve start", stream);
       PG_CUDA(cudaGraphLaunch(exec, stream));
       PG_CUDA(cudaEventRecord(ev1, stream));
+      g_trace.mark("solve end", stream);
       if (res && (res->lower || res->upper)) {
         k_decode<<<grid_for(n, 256), 256, 0, stream>>>(d_key_out, d_lo_res, d_up_res, n);
         PG_CUDA(cudaGetLastError());
@@ -842,6 +892,7 @@ struct pg_session {
           PG_CUDA(cudaMemcpyAsync(res->upper, d_up_res, sizeof(double) * n,
                                   cudaMemcpyDeviceToHost, stream));
         bounds_done = true;
+        g_trace.mark("download", stream);
       }
     } else {
       // host-driven loop: one sync per round (the paper's cpu_loop)
@@ -905,6 +956,9 @@ struct pg_session {
   void upload_bounds(const double* lo, const double* up) {
     PG_CUDA(cudaMemcpyAsync(d_lo0, lo, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
     PG_CUDA(cudaMemcpyAsync(d_up0, up, sizeof(double) * n, cudaMemcpyHostToDevice, stream));
+    normalize_bounds();
+  }
+  void normalize_bounds() {
     if (n) {
       k_normalize<<<grid_for(n, 256), 256, 0, stream>>>(d_lo0, n, cfg.infinity_threshold);
       k_normalize<<<grid_for(n, 256), 256, 0, stream>>>(d_up0, n, cfg.infinity_threshold);
@@ -1009,6 +1063,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       s->ev1 = x.ev1;
       s->ev_fork = x.fork;
       s->ev_join = x.join;
+      s->h_st = x.h_st;
     }
     t_alloc_stream = s->stream;
 
@@ -1033,15 +1088,22 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     int32_t* t_perm = dalloc<int32_t>(m);
     int32_t* slen = dalloc<int32_t>((size_t)m + 1);
     int32_t* counts = dalloc<int32_t>(kMaxClasses + 5);  // + u64 sum of len^2 at [kMaxClasses + 2], bad row_ptr flag at [+4]
-    PG_CUDA(cudaEventRecord(s->ev_fork, st));
-    PG_CUDA(cudaStreamWaitEvent(s2, s->ev_fork, 0));
-    // stream 1: the bulk of the upload (asynchronous from pinned memory)
+    g_trace.mark("start", st);
+    // row_ptr first, on stream 2, and the rest of the upload (stream 1,
+    // asynchronous from pinned memory) after it: stream 2's ordering starts
+    // as soon as row_ptr is in.  (Without the wait the matrix copies may
+    // reach the copy engine first and row_ptr lands behind all of them; an
+    // event after a copy on stream 1 can also fire only after the copies
+    // that follow it.)
     auto h2d = [&](void* dst, const void* src, size_t bytes, cudaStream_t q) {
       if (bytes) PG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, q));
     };
-    // row_ptr first: the ordering on stream 2 starts at once instead of
-    // queueing behind the matrix on the copy engine
+    PG_CUDA(cudaEventRecord(s->ev_fork, st));
+    PG_CUDA(cudaStreamWaitEvent(s2, s->ev_fork, 0));
     h2d(t_rp, p->row_ptr, sizeof(int32_t) * ((size_t)m + 1), s2);
+    PG_CUDA(cudaEventRecord(s->ev_join, s2));
+    PG_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+    g_trace.mark("row_ptr arrived (s2)", s2);
     h2d(t_cols, p->col_idx, sizeof(int32_t) * nnz, st);
     cudaEvent_t ev_cols = nullptr;
     PG_CUDA(cudaEventCreateWithFlags(&ev_cols, cudaEventDisableTiming));
@@ -1050,6 +1112,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     h2d(t_lhs, p->lhs, sizeof(double) * m, st);
     h2d(t_rhs, p->rhs, sizeof(double) * m, st);
     h2d(s->d_integral, p->integral, n, st);
+    g_trace.mark("h2d matrix done (st)", st);
 
     // stream 2, concurrently: row order.  Short rows (<= short_max entries)
     // grouped by exact length (stable radix sort), then the rows split into
@@ -1076,6 +1139,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       PG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, need, key, key2, idx, t_perm, m, 0, 5, s2));
       cub_tmp(need);
       PG_CUDA(cub::DeviceRadixSort::SortPairs(tmp, need, key, key2, idx, t_perm, m, 0, 5, s2));
+      g_trace.mark("row sort (s2)", s2);
       k_sorted_len<<<s->grid_for((int64_t)m + 1, 256), 256, 0, s2>>>(t_rp, t_perm, m, slen);
       PG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, need, slen, s->d_row_ptr, m + 1, s2));
       cub_tmp(need);
@@ -1083,8 +1147,10 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       k_class_counts<<<s->grid_for(m, 256), 256, 0, s2>>>(key2, m, counts);
       auto* len2 = reinterpret_cast<unsigned long long*>(counts + kMaxClasses + 2);
       k_len2_sum<<<s->grid_for(m, 256), 256, 0, s2>>>(t_rp, m, len2);
+      g_trace.mark("class counts (s2)", s2);
       PG_CUDA(cudaMemcpyAsync(cls.data(), counts, sizeof(int32_t) * (kMaxClasses + 5),
                               cudaMemcpyDeviceToHost, s2));
+      g_trace.mark("counts d2h (s2)", s2);
       PG_CUDA(cudaStreamSynchronize(s2));
       unsigned long long l2 = 0;
       if (cls[kMaxClasses + 4])
@@ -1175,10 +1241,15 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
     s->d_st = dalloc<DevState>(1);
     s->d_ctl = dalloc<NodeCtl>(1);
     s->d_per_round = dalloc<long long>(cfg->round_limit);
-    PG_CUDA(cudaMallocHost(&s->h_st, sizeof(DevState)));
     PG_CUDA(cudaMemsetAsync(s->d_ctl, 0, sizeof(NodeCtl), st));  // cold starts
     PG_CUDA(cudaMemsetAsync(s->d_st, 0, sizeof(DevState), st));
     PG_CUDA(cudaMemsetAsync(s->d_row_done, 0, sizeof(int32_t) * std::max<int32_t>(1, s->nsrow), st));
+    // the start bounds follow the matrix on the copy engine (stream 2) while
+    // stream 1 permutes the matrix and fills the sliced-ELL copy
+    cudaEvent_t ev_mat = nullptr, ev_bnd = nullptr;
+    PG_CUDA(cudaEventCreateWithFlags(&ev_mat, cudaEventDisableTiming));
+    PG_CUDA(cudaEventCreateWithFlags(&ev_bnd, cudaEventDisableTiming));
+    PG_CUDA(cudaEventRecord(ev_mat, st));
     t_alloc_stream = s2;
     s->d_split = dalloc<int32_t>(std::max<int32_t>(1, s->nsrow) + 1);
     if (s->nsrow) {
@@ -1276,20 +1347,29 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       t_alloc_stream = s2;
       int32_t* inv = dalloc<int32_t>(m);
       k_invert_perm<<<s->grid_for(m, 256), 256, 0, s2>>>(t_perm, m, inv);
+      g_trace.mark("ordering (s2)", s2);
       PG_CUDA(cudaStreamWaitEvent(s2, ev_cols, 0));
+      g_trace.mark("cols arrived (s2)", s2);
       s->build_col_index(t_rp, t_cols, inv, s2);
       dfree(inv);
       t_alloc_stream = st;
     }
     // the ordering (stream 2) must be complete before the permutation
+    g_trace.mark("ordering+colindex (s2)", s2);
     PG_CUDA(cudaEventRecord(s->ev_join, s2));
     PG_CUDA(cudaStreamWaitEvent(st, s->ev_join, 0));
+    PG_CUDA(cudaStreamWaitEvent(s2, ev_mat, 0));
+    h2d(s->d_lo0, p->lower, sizeof(double) * n, s2);
+    h2d(s->d_up0, p->upper, sizeof(double) * n, s2);
+    g_trace.mark("bounds h2d (s2)", s2);
+    PG_CUDA(cudaEventRecord(ev_bnd, s2));
     if (m) {
       k_permute_rows<<<s->grid_for(std::max<int64_t>(m, nnz * 32 / kWalkChunk + 1), 256, 16), 256, 0, st>>>(
           t_rp, t_cols, t_vals, t_lhs, t_rhs, t_perm, s->d_row_ptr, s->d_integral, s->d_colx,
           s->d_vals, s->d_lhs, s->d_rhs, m, n, cfg->infinity_threshold, s->d_st);
       PG_CUDA(cudaGetLastError());
     }
+    g_trace.mark("permute", st);
     if (cfg->scalar_mode == PG_NARROW32) {
       // the float working copy (engine_common.hpp:24-38) and chunk scratch
       k_to_f32<<<s->grid_for(nnz, 256), 256, 0, st>>>(s->d_vals, nnz);
@@ -1323,6 +1403,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
                     (void*)segs_in, (void*)skey, (void*)skey2, (void*)sidx, (void*)sorder,
                     tmp})
       dfree(q);
+    g_trace.mark("fill sell", st);
     tm.lap("H2D + permute (queued)");
     // worklist index: column -> work items (device counting sort by column)
     {
@@ -1370,7 +1451,10 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
             2e9, (double)m * (double)n / (4.0 * (double)std::max<int64_t>(nnz, 1)));
       }
     }
-    s->upload_bounds(p->lower, p->upper);
+    g_trace.mark("worklist maps", st);
+    PG_CUDA(cudaStreamWaitEvent(st, ev_bnd, 0));
+    s->normalize_bounds();
+    g_trace.mark("bounds normalised", st);
     PG_CUDA(cudaGetLastError());
     // everything after this point is ordered on the session stream: no host
     // sync (the graph is instantiated while the GPU finishes the setup)
@@ -1394,6 +1478,8 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       }
     }
     cudaEventDestroy(ev_cols);
+    cudaEventDestroy(ev_mat);
+    cudaEventDestroy(ev_bnd);
     if (cfg->loop_mode == PG_LOOP_GRAPH) s->build_graph();
     tm.lap("graph instantiate");
     return s;
@@ -1645,6 +1731,8 @@ int pg_propagate(const pg_problem* p, const pg_config* cfg, pg_result* res) {
   PhaseTimer tm;
   rc = pg_session_run(s, res);
   tm.lap("solve + download");
+  g_trace.dump();
+  s->release_buffers();
   if (!Reaper::reaper().push(s)) pg_session_destroy(s);
   tm.lap("destroy (handed off)");
   return rc;

@@ -73,11 +73,15 @@ def propagate_multi_gpu(instance: ProblemInstance, cfg: EngineConfig | None = No
     return result_from_c(r, lo, up, prc)
 
 
-def propagate_gpu(instance: ProblemInstance, cfg: EngineConfig | None = None) -> PropagationResult:
+def propagate_gpu(instance: ProblemInstance, cfg: EngineConfig | None = None,
+                  out=None) -> PropagationResult:
+    """pg_propagate.  `out` = (lower, upper): the caller's result buffers
+    (float64, n each; page-locked ones download at full PCIe speed), else
+    fresh arrays."""
     cfg = cfg or EngineConfig()
     c = cfg.to_c()
     p = instance.to_c()
-    r, lo, up, prc = new_c_result(instance.num_cols(), cfg.round_limit)
+    r, lo, up, prc = new_c_result(instance.num_cols(), cfg.round_limit, out)
     abi.check(_lib().pg_propagate(C.byref(p), C.byref(c), C.byref(r)), "pg_propagate")
     return result_from_c(r, lo, up, prc)
 
@@ -232,9 +236,9 @@ class Session:
         except Exception:
             pass
 
-    def propagate(self, lower=None, upper=None) -> PropagationResult:
+    def propagate(self, lower=None, upper=None, out=None) -> PropagationResult:
         n = self.instance.num_cols()
-        r, lo, up, prc = new_c_result(n, self.cfg.round_limit)
+        r, lo, up, prc = new_c_result(n, self.cfg.round_limit, out)
         lp = up_ = None
         if lower is not None:
             lower = np.ascontiguousarray(lower, dtype=np.float64)
@@ -258,11 +262,11 @@ class Session:
         snap.bounds_out = VariableBounds(lo, up)
         return RoundOutcome(bool(ch.value), bool(inf.value), int(cnt.value))
 
-    def run(self, download=False) -> PropagationResult:
+    def run(self, download=False, out=None) -> PropagationResult:
         """Solve from the device-resident start bounds (nothing crosses PCIe
-        unless download=True)."""
+        unless download=True; `out` as for propagate_gpu)."""
         n = self.instance.num_cols()
-        r, lo, up, prc = new_c_result(n, self.cfg.round_limit)
+        r, lo, up, prc = new_c_result(n, self.cfg.round_limit, out)
         if not download:
             r.lower = C.cast(None, C.POINTER(C.c_double))
             r.upper = C.cast(None, C.POINTER(C.c_double))

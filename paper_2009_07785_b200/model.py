@@ -186,10 +186,19 @@ class PropagationResult:
     elapsed_ns: int = 0
 
 
-def new_c_result(n: int, round_limit: int):
-    """Allocate output arrays and a PgResult pointing at them."""
-    lo = np.empty(n, dtype=np.float64)
-    up = np.empty(n, dtype=np.float64)
+def new_c_result(n: int, round_limit: int, out=None):
+    """Allocate output arrays (or take the caller's `out` = (lower, upper),
+    e.g. page-locked buffers reused across calls) and a PgResult pointing at
+    them."""
+    if out is None:
+        lo = np.empty(n, dtype=np.float64)
+        up = np.empty(n, dtype=np.float64)
+    else:
+        lo, up = out
+        for a in (lo, up):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.shape == (n,)
+                    and a.flags.c_contiguous and a.flags.writeable):
+                raise ValueError(f"out arrays must be writable contiguous float64 of shape ({n},)")
     prc = np.zeros(max(round_limit, 1), dtype=np.int64)
     r = abi.PgResult()
     r.lower = abi.ptr(lo, C.c_double)

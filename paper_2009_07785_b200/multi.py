@@ -99,11 +99,11 @@ class RowShardedSession:
         abi.check(abi.load_library().pg_session_attach_comm(self.session._h, buf, rank, world),
                   "pg_session_attach_comm")
 
-    def propagate(self, lower=None, upper=None) -> PropagationResult:
-        return self.session.propagate(lower, upper)
+    def propagate(self, lower=None, upper=None, out=None) -> PropagationResult:
+        return self.session.propagate(lower, upper, out)
 
-    def run(self, download=False) -> PropagationResult:
-        return self.session.run(download)
+    def run(self, download=False, out=None) -> PropagationResult:
+        return self.session.run(download, out)
 
     def close(self):
         self.session.close()
