@@ -903,9 +903,12 @@ struct pg_session {
       static const bool dbg = getenv("PG_DEBUG_ROUNDS") != nullptr;
       while (!h_st->done) {
         if (dbg)
-          fprintf(stderr, "[pg] round %d: full=%d nunit={%d,%d} nwide={%d,%d} nchg={%d,%d}\n",
+          fprintf(stderr,
+                  "[pg] round %d: full=%d nunit={%d,%d} nwide={%d,%d} nmid={%d,%d} nchg={%d,%d} "
+                  "deg={%lld,%lld}\n",
                   h_st->round + 1, h_st->full, h_st->nunit[0], h_st->nunit[1], h_st->nwide[0],
-                  h_st->nwide[1], h_st->nchg[0], h_st->nchg[1]);
+                  h_st->nwide[1], h_st->nmid[0], h_st->nmid[1], h_st->nchg[0], h_st->nchg[1],
+                  h_st->chg_deg[0], h_st->chg_deg[1]);
         enqueue_round(false);
         PG_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(DevState), cudaMemcpyDeviceToHost, stream));
         PG_CUDA(cudaStreamSynchronize(stream));
@@ -1426,11 +1429,34 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         s->d_wide_list = dalloc<int32_t>(2 * (size_t)s->nunits);
         s->d_unit_list = dalloc<int32_t>(2 * (size_t)s->nunits);
         PG_CUDA(cudaMemsetAsync(s->d_row_unit, 0xff, sizeof(int32_t) * std::max<int32_t>(m, 1), st));
+        // round-kind heuristics (tuned on C2 / C5; environment overrides for
+        // A/B).  per = the changed columns that mark about every row (mean
+        // column degree nnz / n).  The next round is a full sweep when more
+        // than per / PG_DENSE_DIV columns changed, or when the changed
+        // columns' entries times the mean unit weight exceed PG_DENSE_DEG x
+        // the unit count (marks and marked rows are cheap for C5's mid-length
+        // rows, dear for C2's lane units); a full sweep after more than
+        // PG_LIST_GATE x per changes builds no changed-column list.
+        const double per = (double)m * (double)n / (double)std::max<int64_t>(nnz, 1);
+        auto envd = [](const char* k, double d) { return getenv(k) ? atof(getenv(k)) : d; };
+        static const double div = envd("PG_DENSE_DIV", 1.0), fdeg = envd("PG_DENSE_DEG", 1.0),
+                            gate = envd("PG_LIST_GATE", 1.0);
+        D.dense_nchg = (int32_t)std::min<double>(2e9, per / div);
+        D.dense_deg = fdeg * (double)m;  // compared with entries x wsum / nunits
+        D.list_gate = (long long)std::min<double>(9e18, gate * per);
+        // a worklist round while the marked lane, long and mid units, weighted,
+        // stay below the weighted unit count (round_is_sparse)
+        int w[4] = {8, 32, 2, 1};
+        if (const char* e = getenv("PG_WL_WEIGHTS")) sscanf(e, "%d,%d,%d,%d", &w[0], &w[1], &w[2], &w[3]);
+        D.w_lane = w[0];
+        D.w_wide = w[1];
+        D.w_mid = w[2];
+        D.w_all = w[3];
         if (s->nunits) {
           k_unit_maps<<<s->grid_for(s->nunits, 256), 256, 0, st>>>(s->d_units, s->nunits, s->d_segs,
                                                                  s->d_row_unit, s->d_part_unit);
-          k_slice_units<<<s->grid_for(s->nslices, 256), 256, 0, st>>>(s->d_slices, s->nslices,
-                                                                     s->d_units, s->d_unit_slice);
+          k_slice_units<<<s->grid_for(s->nslices, 256), 256, 0, st>>>(
+              s->d_slices, s->nslices, s->d_units, s->d_unit_slice, D, s->d_st);
         }
         PG_CUDA(cudaGetLastError());
         D.row_unit = s->d_row_unit;
@@ -1445,10 +1471,6 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         D.nslices = s->nslices;
         D.unit_list = s->d_unit_list;
         D.nunits = s->nunits;
-        // changed columns above which ~1/4 of the rows are marked (mean column
-        // degree nnz / n): the next round is cheaper as a full sweep
-        D.dense_nchg = (int32_t)std::min<double>(
-            2e9, (double)m * (double)n / (4.0 * (double)std::max<int64_t>(nnz, 1)));
       }
     }
     g_trace.mark("worklist maps", st);

@@ -26,9 +26,6 @@
 namespace pgb {
 
 constexpr int kCommitThreads = 256;
-#ifndef PG_SPARSE_COST
-#define PG_SPARSE_COST 2
-#endif
 
 // Device-resident loop state.
 struct DevState {
@@ -50,7 +47,10 @@ struct DevState {
   int32_t frac_any;                  // an integral column has a fractional start bound
   int32_t frac_tmp;                  // k_reset's accumulator of frac_any
   int32_t nchg[2];                   // changed-column list lengths, by round parity
+  long long chg_deg[2];              // sum of the listed columns' degrees (rows to mark)
+  long long unit_wsum;               // sum of the units' worklist weights (set up once)
   int32_t nwide[2];                  // marked multi-lane unit list lengths, by round parity
+  int32_t nmid[2];                   //   of which mid-length units (at the list's back)
   int32_t nunit[2];                  // marked one-lane unit list lengths, by round parity
   int32_t ntouch;                    // columns merged into this (worklist) round
   int32_t sparse_commit;             // the last commit visited only the touched columns
@@ -111,6 +111,10 @@ struct Dirty {
   int32_t* unit_list;        // [2][nunits] marked one-lane units
   int32_t nslices, nunits;
   int32_t dense_nchg;        // more changed columns than this: next round is a full sweep
+  double dense_deg;          //   or when (entries to mark) x (mean unit weight) > dense_deg (F m)
+  long long list_gate;       // a full sweep after more changes than this builds no list
+  // a worklist round while w_lane nunit + w_wide nwide + w_mid nmid <= w_all nunits
+  int32_t w_lane, w_wide, w_mid, w_all;
   int32_t unrolled;          // row-shard graphs of unrolled rounds (round_off)
 };
 
@@ -127,8 +131,12 @@ __device__ __forceinline__ bool mark_row(uint8_t* flag, int r) {
 __device__ __forceinline__ void mark_row_units(const Dirty& D, int r, int par, DevState* st) {
   int32_t* ul = D.unit_list + (size_t)par * D.nunits;
   int32_t* wl = D.wide_list + (size_t)par * D.nunits;
+  // unit_slice: -1 one-lane unit, -2 mid-length unit (appended from the
+  // wide list's back), else a long unit
   auto one = [&](int u) {
-    if (D.unit_slice[u] < 0) ul[atomicAdd(&st->nunit[par], 1)] = u;
+    const int us = D.unit_slice[u];
+    if (us == -1) ul[atomicAdd(&st->nunit[par], 1)] = u;
+    else if (us == -2) wl[D.nunits - 1 - atomicAdd(&st->nmid[par], 1)] = u;
     else wl[atomicAdd(&st->nwide[par], 1)] = u;
   };
   const int u = D.row_unit[r];
@@ -504,10 +512,12 @@ __device__ __forceinline__ unsigned long long block_sum(unsigned long long v, in
 __device__ __forceinline__ bool round_is_sparse(DevState* st, const Dirty& D) {
   if (!D.enabled || ld_gpu(&st->full)) return false;
   const int par = (ld_gpu(&st->round) + 1) & 1;
-  // worklist round while the marked units (a long unit counts twice) stay
-  // below 1 / PG_SPARSE_COST of all units (tuned on C2 / C5)
-  const long long work = (long long)ld_gpu(&st->nunit[par]) + 2LL * ld_gpu(&st->nwide[par]);
-  return PG_SPARSE_COST * work <= (long long)D.nunits;
+  // worklist round while the marked units, weighted by their cost per unit
+  // against a full sweep's (tuned on C2 / C5), stay below the full sweep
+  const long long work = (long long)D.w_lane * ld_gpu(&st->nunit[par]) +
+                         (long long)D.w_wide * ld_gpu(&st->nwide[par]) +
+                         (long long)D.w_mid * ld_gpu(&st->nmid[par]);
+  return work <= (long long)D.w_all * D.nunits;
 }
 
 // kList: a worklist round -- only the columns on the touched list (their
@@ -532,7 +542,7 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
   // a full-sweep round after a round with many changes will have many too:
   // skip the changed-column list (the next round is a full sweep anyway)
   const bool list = D.enabled && (kList || !ld_gpu(&st->full) ||
-                                  ld_gpu(&st->last_changes) <= 4LL * D.dense_nchg);
+                                  ld_gpu(&st->last_changes) <= D.list_gate);
   // the loop bound is warp-uniform (j0 - lane is), so the warp stays
   // converged for the list appends
   for (int j0 = gtid; j0 - lane < nj; j0 += U * gstride) {
@@ -568,14 +578,20 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
         if (lo > __dadd_rn(up, cfg.imp_abs)) inf = 1;
       }
       if (list) {
-        // changed columns of this round -> list (one atomic per warp)
+        // changed columns of this round -> list (one atomic per warp), and
+        // the number of entries their marks will visit
         const unsigned chm = __ballot_sync(0xffffffffu, c != 0);
         if (chm) {
           int base = 0;
           if (lane == 0) base = atomicAdd(&st->nchg[cb], __popc(chm));
           base = __shfl_sync(0xffffffffu, base, 0);
           if (c) D.chg_list[(size_t)cb * D.n + base + __popc(chm & ((1u << lane) - 1u))] = j;
-        }
+          int deg = c ? D.col_ptr[j + 1] - D.col_ptr[j] : 0;
+#pragma unroll
+          for (int o = 16; o; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
+          if (lane == 0 && deg)
+            atomicAdd(reinterpret_cast<unsigned long long*>(&st->chg_deg[cb]), (unsigned long long)deg);
+      }
       }
     }
   }
@@ -617,10 +633,16 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
       st->work2 = 0;
       st->cand_work = 0;
       // many changed columns (or no list): the next round is a full sweep (no marks)
-      st->full = (!list || ld_gpu(&st->nchg[cb]) > D.dense_nchg) ? 1 : 0;
+      // marks cost about their entries, and the rows they mark cost their
+      // units' weights (round_is_sparse): with many, a full sweep is cheaper
+      st->full = (!list || ld_gpu(&st->nchg[cb]) > D.dense_nchg ||
+                  (double)ld_gpu(&st->chg_deg[cb]) * (double)ld_gpu(&st->unit_wsum) >
+                      D.dense_deg * (double)D.nunits) ? 1 : 0;
       st->last_changes = ch;
       st->nchg[nb] = 0;  // the list k_mark consumed after the previous commit
+      st->chg_deg[nb] = 0;
       st->nwide[cb] = 0;  // this round's unit lists
+      st->nmid[cb] = 0;
       st->nunit[cb] = 0;
       st->ntouch = 0;
       st->sparse_commit = kList;
@@ -703,10 +725,12 @@ __global__ void __launch_bounds__(kCommitThreads)
       // k_mark_vars marks (see NodeCtl)
       st->full = (D.enabled && ctl->warm) ? 0 : 1;
       st->nchg[0] = st->nchg[1] = 0;
+      st->chg_deg[0] = st->chg_deg[1] = 0;
       st->ntouch = 0;
       st->sparse_round = 0;
       st->last_changes = 0x7fffffffffffffffLL;  // round 1 is a full sweep: no list
       st->nwide[0] = st->nwide[1] = 0;
+      st->nmid[0] = st->nmid[1] = 0;
       st->nunit[0] = st->nunit[1] = 0;
       st->frac_any = atomicAdd(&st->frac_tmp, 0);
       st->frac_tmp = 0;
@@ -970,18 +994,17 @@ __device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__
   const int nchg = ld_gpu(&st->nchg[cb]);
   uint8_t* flag = D.row_flag + (size_t)nb * D.ms;
   const int lane = threadIdx.x & 31;
+  // one warp per changed column
   for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchg;
        w += (gridDim.x * blockDim.x) >> 5) {
     const int j = D.chg_list[(size_t)cb * D.n + w];
     for (int e = D.col_ptr[j] + lane; e < D.col_ptr[j + 1]; e += 32) {
       const int row = D.col_row[e];
-      // the common case -- a whole row in a one-lane slice -- is appended
-      // with one atomic per warp
       bool single = false;
       int u = -1;
       if (mark_row(flag, row)) {
         u = D.row_unit[row];
-        single = u >= 0 && D.unit_slice[u] < 0;
+        single = u >= 0 && D.unit_slice[u] == -1;
         if (!single) mark_row_units(D, row, nb, st);
       }
       const unsigned act = __activemask();

@@ -52,6 +52,9 @@ namespace pgb {
 #ifndef PG_SELL_LANEUNIT
 #define PG_SELL_LANEUNIT 32
 #endif
+#ifndef PG_SELL_MIDMAX
+#define PG_SELL_MIDMAX 128
+#endif
 #ifndef PG_SELL_DEBUG
 #define PG_SELL_DEBUG 0  // 1: cfg.flags 0x10000 skips phase 2 (timing experiments)
 #endif
@@ -75,6 +78,7 @@ constexpr int kSellThreads = 256;
 constexpr int kSellWarps = kSellThreads / 32;
 constexpr int kSellGroup = PG_SELL_GROUP;
 constexpr int kSellLaneUnit = PG_SELL_LANEUNIT;  // worklist rounds: longer units get a warp each
+constexpr int kSellMidMax = PG_SELL_MIDMAX;      //   (up to this length: 8 lanes each)
 // lanes per unit by unit length: > 256 -> 8, > 128 -> 4, > 64 -> 2, else 1
 constexpr int kSellG8 = 256, kSellG4 = 128, kSellG2 = 64;
 
@@ -602,7 +606,7 @@ template <bool kRowCheck, class RA>
 __device__ __forceinline__ void sell_wide(const RA& A, SellWarpSmem& W, int par,
                                           uint64_t pol_keep, bool& inf_flag, const DevCfg& cfg) {
   const int lane = threadIdx.x & 31;
-  const int nw = ld_gpu(&A.st->nwide[par]);
+  const int nw = ld_gpu(&A.st->nwide[par]);  // the list's front: long units
   const int32_t* wl = A.dirty.wide_list + (size_t)par * A.dirty.nunits;
   const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
   // static striding by warp (few, similar items: no ticket contention)
@@ -740,6 +744,126 @@ __device__ __forceinline__ void sell_wide(const RA& A, SellWarpSmem& W, int par,
   }
 }
 
+// Worklist round, mid-length units (longer than a lane unit, at most
+// kSellMidMax entries: C5's 50-entry rows, C2's medium rows): 8 lanes per
+// unit, four units per warp, over the unit's CSR entries.  Lane j of a group
+// holds entries j, j + 8, ..; every lane of the group adds the 8 products of
+// a step in entry order through shuffles (the reference's sequential chain,
+// as sell_step<3>), so the group's lanes all hold the row record.  Phase 2
+// re-reads the entries of a row that may tighten and applies the exact
+// filter per entry.
+template <bool kRowCheck, class RA>
+__device__ __forceinline__ void sell_mid(const RA& A, int par, uint64_t pol_keep, bool& inf_flag,
+                                         const DevCfg& cfg) {
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 3, j = lane & 7;
+  const int nm = ld_gpu(&A.st->nmid[par]);
+  const int32_t* ml = A.dirty.wide_list + (size_t)par * A.dirty.nunits + A.dirty.nunits - 1;
+  const bool frac_any = ld_gpu(&A.st->frac_any) != 0;
+  const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nwarps = (gridDim.x * blockDim.x) >> 5;
+  // warps count down from the last one, so the first warps (long units) and
+  // the mid units start at once
+  for (int b = nwarps - 1 - gw; 4 * b < nm; b += nwarps) {
+    const int t = 4 * b + g;
+    const bool have = t < nm;
+    UnitDesc ud = {0, -1};
+    int k0 = 0;
+    if (have) {
+      ud = A.units[ml[-t]];
+      k0 = ud.ref >= 0 ? A.row_ptr[ud.ref] : A.segs[-ud.ref - 1].k0;
+    }
+    const int len = have ? ud.len : 0;
+    int maxlen = len;
+#pragma unroll
+    for (int o = 8; o < 32; o <<= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
+    Act act = {0.0, 0.0, 0, 0};
+    double xm = -CUDART_INF;
+    // steps of 8 entries, two in flight: loads of steps s, s + 1, then their
+    // gathers, then the ordered adds
+    for (int s0 = 0; 8 * s0 < maxlen; s0 += 2) {
+      double a[2], lo[2], up[2], q[2];
+      int32_t c[2];
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int e = 8 * (s0 + k) + j;
+        a[k] = 0.0;
+        c[k] = A.pad_col;
+        if (e < len) {
+          a[k] = A.vals[k0 + e];
+          c[k] = A.colx[k0 + e];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 2; ++k) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        if (8 * (s0 + k) >= maxlen) break;  // warp-uniform
+        const bool in = 8 * (s0 + k) + j < len;
+        const double bmin = a[k] > 0 ? lo[k] : up[k];
+        const double bmax = a[k] > 0 ? up[k] : lo[k];
+        const bool imin = in && is_inf(bmin), imax = in && is_inf(bmax);
+        const double pmin = (!in || imin) ? 0.0 : __dmul_rn(a[k], bmin);
+        const double pmax = (!in || imax) ? 0.0 : __dmul_rn(a[k], bmax);
+        act.min_i += imin;
+        act.max_i += imax;
+        if (in) xm = fmax(xm, fabs(a[k]) * q[k]);
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) {
+          const double vmin = __shfl_sync(0xffffffffu, pmin, jj, 8);
+          const double vmax = __shfl_sync(0xffffffffu, pmax, jj, 8);
+          act.min_f = __dadd_rn(act.min_f, vmin);
+          act.max_f = __dadd_rn(act.max_f, vmax);
+        }
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 8; o <<= 1) {
+      act.min_i += __shfl_xor_sync(0xffffffffu, act.min_i, o);
+      act.max_i += __shfl_xor_sync(0xffffffffu, act.max_i, o);
+      xm = fmax(xm, __shfl_xor_sync(0xffffffffu, xm, o));
+    }
+    if (!have) continue;
+    if (ud.ref < 0) {
+      if (j == 0) chunk_done<kRowCheck>(A, ud, act, xm, inf_flag, cfg);
+      continue;
+    }
+    const double l = A.lhs[ud.ref], h = A.rhs[ud.ref];
+    if (kRowCheck && j == 0 && row_infeasible(act, l, h, cfg)) inf_flag = true;
+    const RowFilter f = row_filter(act, l, h);
+    if (!row_may(f, xm)) continue;
+    // phase 2 (no shuffles: the groups may diverge here)
+    for (int e0 = j; e0 < len; e0 += 32) {
+      double a[4], lo[4], up[4];
+      int32_t c[4];
+      unsigned pass = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int e = e0 + 8 * k;
+        a[k] = 0.0;
+        c[k] = A.pad_col;
+        if (e < len) {
+          a[k] = A.vals[k0 + e];
+          c[k] = A.colx[k0 + e];
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        double q;
+        ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q);
+        const double bmin = a[k] > 0 ? lo[k] : up[k];
+        const double bmax = a[k] > 0 ? up[k] : lo[k];
+        if (e0 + 8 * k < len && entry_may(f, fabs(a[k]) * q, isinf(bmin), isinf(bmax)))
+          pass |= 1u << k;
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if ((pass >> k) & 1u)
+          if (entry_pipeline(act, a[k], lo[k], up[k], l, h, c[k], A.key_out, cfg, &A.touch))
+            inf_flag = true;
+    }
+  }
+}
+
 // Worklist round, one-lane units: a warp takes 32 marked units (any slices),
 // one per lane; the chain reads the unit's column of its slice (entry i at
 // off + 32 i + position), then row finish and an in-lane phase 2 over the
@@ -837,6 +961,7 @@ __device__ __forceinline__ void sell_sweep(const RA& A, const DevCfg& cfg,
   if (!kDense) {
     // worklist round: only the units of the marked rows
     if (!(PG_SELL_DEBUG && (cfg.flags & 0x80000u))) sell_wide<kRowCheck>(A, W, par, pk, inf_flag, cfg);
+    sell_mid<kRowCheck>(A, par, pk, inf_flag, cfg);
     if (!(PG_SELL_DEBUG && (cfg.flags & 0x100000u))) sell_units<kRowCheck>(A, par, pk, inf_flag, cfg);
     if (__any_sync(0xffffffffu, inf_flag) && lane == 0) A.st->infeasible = 1;
     return;
@@ -1029,12 +1154,19 @@ __global__ void k_unit_maps(const UnitDesc* __restrict__ units, int nunits,
 // unit_slice < 0: a short one-lane unit, visited by a lane in worklist
 // rounds; otherwise (longer units) by a warp
 __global__ void k_slice_units(const SliceDesc* __restrict__ slices, int nslices,
-                              const UnitDesc* __restrict__ units, int32_t* __restrict__ unit_slice) {
+                              const UnitDesc* __restrict__ units, int32_t* __restrict__ unit_slice,
+                              const Dirty D, DevState* __restrict__ st) {
+  long long w = 0;
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < nslices; s += gridDim.x * blockDim.x) {
     const SliceDesc d = slices[s];
-    for (int i = 0; i < d.count; ++i)
-      unit_slice[d.first + i] = (d.lg == 0 && units[d.first + i].len <= kSellLaneUnit) ? -1 : s;
+    for (int i = 0; i < d.count; ++i) {
+      const int len = units[d.first + i].len;
+      const int k = (d.lg == 0 && len <= kSellLaneUnit) ? -1 : len <= kSellMidMax ? -2 : s;
+      unit_slice[d.first + i] = k;
+      w += k == -1 ? D.w_lane : k == -2 ? D.w_mid : D.w_wide;
+    }
   }
+  if (w) atomicAdd(reinterpret_cast<unsigned long long*>(&st->unit_wsum), (unsigned long long)w);
 }
 
 }  // namespace pgb
