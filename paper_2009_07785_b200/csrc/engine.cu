@@ -1491,8 +1491,11 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       if (want) {
         PG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
         cudaStreamAttrValue av = {};
-        av.accessPolicyWindow.base_ptr = s->d_snap;
-        av.accessPolicyWindow.num_bytes = std::min(sizeof(Snap) * ((size_t)n + 1), want);
+        // the array the full sweep gathers from: 16 B bounds or 32 B records
+        const bool b16 = s->gather16();
+        av.accessPolicyWindow.base_ptr = b16 ? (void*)s->d_bnd : (void*)s->d_snap;
+        av.accessPolicyWindow.num_bytes =
+            std::min((b16 ? sizeof(double2) : sizeof(Snap)) * ((size_t)n + 1), want);
         av.accessPolicyWindow.hitRatio = 1.0f;
         av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;

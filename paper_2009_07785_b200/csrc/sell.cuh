@@ -55,6 +55,9 @@ namespace pgb {
 #ifndef PG_SELL_MIDMAX
 #define PG_SELL_MIDMAX 128
 #endif
+#ifndef PG_SELL_XSMEM
+#define PG_SELL_XSMEM 1  // multi-lane chains: products to the owner lane through shared memory
+#endif
 #ifndef PG_SELL_DEBUG
 #define PG_SELL_DEBUG 0  // 1: cfg.flags 0x10000 skips phase 2 (timing experiments)
 #endif
@@ -215,6 +218,7 @@ struct SellWarpSmem {
   // entries that survive the filter: element offset in the slice, unit
   int32_t qe[64];
   uint8_t qu[64];
+  double2 xb[32];  // one step's {min, max} products of a multi-lane slice
   double2 wbuf[256];  // worklist rounds: {min, max} contributions of a wide unit's block
   double2 wbuf2[256];
 };
@@ -250,10 +254,13 @@ __device__ __forceinline__ bool sell_drain(const RA& A, const SellWarpSmem& W,
 // filter term and word.  Adding +0.0 (an infinite b, or a padding entry) is
 // exact: the sums start at +0.0 and never become -0.0.  With G = 2^LG lanes
 // per unit, the G entries of the step sit on lanes u, u + H, .. and are
-// added in entry order (every lane of the unit forms the same sum).
+// added in entry order: through the warp's shared step buffer by the owner
+// lane (j = 0) alone, the only lane whose sums are used (PG_SELL_XSMEM; one
+// store and G 16-byte loads instead of 2G shuffles, which made long-row
+// sweeps L1-bound), or through shuffles by every lane of the unit.
 template <int LG>
 __device__ __forceinline__ void sell_step(double a, double lo, double up, double q, int u, Act& act,
-                                          int32_t& xk, int32_t* pw) {
+                                          int32_t& xk, int32_t* pw, double2* xb = nullptr) {
   constexpr int G = 1 << LG, H = 32 >> LG;
   const double bmin = a > 0 ? lo : up;
   const double bmax = a > 0 ? up : lo;
@@ -268,6 +275,21 @@ __device__ __forceinline__ void sell_step(double a, double lo, double up, double
   if (LG == 0) {
     act.min_f = __dadd_rn(act.min_f, pmin);
     act.max_f = __dadd_rn(act.max_f, pmax);
+  } else if (PG_SELL_XSMEM) {
+    const int lane = threadIdx.x & 31;
+    __syncwarp();  // the previous step's loads are done
+    xb[lane] = make_double2(pmin, pmax);
+    __syncwarp();
+    if (lane < H) {
+      double2 v[G];
+#pragma unroll
+      for (int jj = 0; jj < G; ++jj) v[jj] = xb[u + H * jj];
+#pragma unroll
+      for (int jj = 0; jj < G; ++jj) {
+        act.min_f = __dadd_rn(act.min_f, v[jj].x);
+        act.max_f = __dadd_rn(act.max_f, v[jj].y);
+      }
+    }
   } else {
 #pragma unroll
     for (int jj = 0; jj < G; ++jj) {
@@ -458,7 +480,7 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
       }
 #pragma unroll
       for (int k = 0; k < UL; ++k)
-        sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xk, pw + 32 * k);
+        sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xk, pw + 32 * k, W.xb);
 #pragma unroll
       for (int k = 0; k < UL; ++k) {
         a[k] = an[k];
@@ -473,7 +495,7 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
       const int32_t c1 = ld_stream_s32(pc, pol_stream);
       double lo1, up1, q1;
       ld_col(A, c1, pol_keep, frac_any, cfg, lo1, up1, q1);
-      sell_step<LG>(a1, lo1, up1, q1, u, act, xk, pw);
+      sell_step<LG>(a1, lo1, up1, q1, u, act, xk, pw, W.xb);
       pa += 32;
       pc += 32;
       pw += 32;
@@ -499,7 +521,7 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
         ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
 #pragma unroll
       for (int k = 0; k < kSellUnroll; ++k)
-        if (t0 + k < steps) sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xk, sw + 32 * (t0 + k));
+        if (t0 + k < steps) sell_step<LG>(a[k], lo[k], up[k], q[k], u, act, xk, sw + 32 * (t0 + k), W.xb);
     }
   }
   if (PG_SELL_DEBUG && (cfg.flags & 0x40000u)) {  // timing experiments only: chains alone
