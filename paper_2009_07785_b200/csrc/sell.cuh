@@ -276,19 +276,31 @@ __device__ __forceinline__ void sell_step(double a, double lo, double up, double
     act.min_f = __dadd_rn(act.min_f, pmin);
     act.max_f = __dadd_rn(act.max_f, pmax);
   } else if (PG_SELL_XSMEM) {
+    // unit u's G products of the step land contiguously (min and max
+    // arrays); lane u runs the min chain, lane H + u the max chain
+    // (slice_max_to_owner hands it to lane u after the chains)
     const int lane = threadIdx.x & 31;
+    const int j = lane >> (5 - LG);
+    double* xmin = reinterpret_cast<double*>(xb);
+    double* xmax = xmin + 32;
     __syncwarp();  // the previous step's loads are done
-    xb[lane] = make_double2(pmin, pmax);
+    xmin[u * G + j] = pmin;
+    xmax[u * G + j] = pmax;
     __syncwarp();
-    if (lane < H) {
-      double2 v[G];
+    if (lane < 2 * H) {
+      const double2* src = reinterpret_cast<const double2*>((lane < H ? xmin : xmax) + u * G);
+      double v[G];
 #pragma unroll
-      for (int jj = 0; jj < G; ++jj) v[jj] = xb[u + H * jj];
-#pragma unroll
-      for (int jj = 0; jj < G; ++jj) {
-        act.min_f = __dadd_rn(act.min_f, v[jj].x);
-        act.max_f = __dadd_rn(act.max_f, v[jj].y);
+      for (int i = 0; i < G / 2; ++i) {
+        const double2 p = src[i];
+        v[2 * i] = p.x;
+        v[2 * i + 1] = p.y;
       }
+      double acc = lane < H ? act.min_f : act.max_f;
+#pragma unroll
+      for (int jj = 0; jj < G; ++jj) acc = __dadd_rn(acc, v[jj]);
+      if (lane < H) act.min_f = acc;
+      else act.max_f = acc;
     }
   } else {
 #pragma unroll
@@ -299,6 +311,17 @@ __device__ __forceinline__ void sell_step(double a, double lo, double up, double
       act.max_f = __dadd_rn(act.max_f, vmax);
     }
   }
+}
+
+// after the chains of a multi-lane slice (PG_SELL_XSMEM): the max chain ran
+// on lane H + u; the owner lane u takes it
+template <int LG>
+__device__ __forceinline__ void slice_max_to_owner(Act& act) {
+  if (LG == 0 || !PG_SELL_XSMEM) return;
+  constexpr int H = 32 >> LG;
+  const int lane = threadIdx.x & 31;
+  const double mx = __shfl_sync(0xffffffffu, act.max_f, (lane + H) & 31);
+  if (lane < H) act.max_f = mx;
 }
 
 // a chunk of a split row: its partial record; after the sweep,
@@ -528,6 +551,7 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
     if (act.min_f == 12345.678 && xk == 1) A.st->infeasible = 1;
     return;
   }
+  slice_max_to_owner<LG>(act);
   slice_tail<kRowCheck, LG>(A, W, sd, ud, active, len, lane, act, xk, ud.ref >= 0 ? A.lhs[ud.ref] : 0.0,
                             ud.ref >= 0 ? A.rhs[ud.ref] : 0.0, pol_keep, inf_flag, cfg);
 }
