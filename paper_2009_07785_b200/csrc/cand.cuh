@@ -126,7 +126,7 @@ __device__ __forceinline__ void cand_sweep(const RA& A, const DevCfg& cfg,
   bool inf_flag = false;
   for (;;) {
     int t = 0;
-    if (lane == 0) t = atomicAdd(&A.st->cand_work, 1);
+    if (lane == 0) t = ticket(&A.st->cand_work);
     t = __shfl_sync(0xffffffffu, t, 0);
     if (t >= nlong + nbatch) break;
     int qn = 0;

@@ -119,11 +119,11 @@ __global__ void __launch_bounds__(kSellThreads) k_sellf_act(const RoundArgs A, c
   const int lane = threadIdx.x & 31;
   bool inf_flag = false;
   int cur = 0;
-  if (lane == 0) cur = atomicAdd(&A.st->work, 1);
+  if (lane == 0) cur = ticket(&A.st->work);
   cur = __shfl_sync(0xffffffffu, cur, 0);
   while (cur < A.nslices) {
     int nxt = 0;
-    if (lane == 0) nxt = atomicAdd(&A.st->work, 1);
+    if (lane == 0) nxt = ticket(&A.st->work);
     const SliceDesc sd = A.slices[cur];
     if (sd.lg == 3) f32_slice_act<kRowCheck, 3>(A, sd, lane, ractf, partf, inf_flag, cfg);
     else if (sd.lg == 2) f32_slice_act<kRowCheck, 2>(A, sd, lane, ractf, partf, inf_flag, cfg);
@@ -261,11 +261,11 @@ __global__ void __launch_bounds__(kSellThreads) k_sellf_cand(const RoundArgs A, 
   const int lane = threadIdx.x & 31;
   bool inf_flag = false;
   int cur = 0;
-  if (lane == 0) cur = atomicAdd(&A.st->cand_work, 1);
+  if (lane == 0) cur = ticket(&A.st->cand_work);
   cur = __shfl_sync(0xffffffffu, cur, 0);
   while (cur < A.nslices) {
     int nxt = 0;
-    if (lane == 0) nxt = atomicAdd(&A.st->cand_work, 1);
+    if (lane == 0) nxt = ticket(&A.st->cand_work);
     const SliceDesc sd = A.slices[cur];
     if (sd.lg == 3) f32_slice_cand<3>(A, sd, lane, ractf, inf_flag, cfg);
     else if (sd.lg == 2) f32_slice_cand<2>(A, sd, lane, ractf, inf_flag, cfg);

@@ -73,6 +73,12 @@ namespace pgb {
 #ifndef PG_SELL_MINB_DENSE
 #define PG_SELL_MINB_DENSE 2  // resident CTAs per SM the full sweep is compiled for
 #endif
+#ifndef PG_SELL_DISCARD
+#define PG_SELL_DISCARD 1  // drop the filter words' L2 lines after phase 2 (no write-back)
+#endif
+#ifndef PG_SELL_GNA
+#define PG_SELL_GNA 1  // snapshot gathers with L1::no_allocate (C2 first round 179 -> 176 us)
+#endif
 #ifndef PG_SELL_MINB
 #define PG_SELL_MINB 2
 #endif
@@ -103,6 +109,13 @@ __device__ __forceinline__ void ld_snap_keep(const Snap* p, uint64_t pol, double
   return;
 #endif
   [[maybe_unused]] long long f;  // the flags word rides along in the 256-bit load
+#if PG_SELL_GNA
+  // no L1 allocation: the records have no reuse within an SM's L1 lifetime
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
+               : "=d"(lo), "=d"(up), "=d"(q), "=l"(f)
+               : "l"(p), "l"(pol));
+  return;
+#endif
   asm volatile("ld.global.nc.L2::cache_hint.v4.b64 {%0,%1,%2,%3}, [%4], %5;"
                : "=d"(lo), "=d"(up), "=d"(q), "=l"(f)
                : "l"(p), "l"(pol));
@@ -208,6 +221,17 @@ __device__ __forceinline__ bool frow_may(const FTest& t, int32_t xk) {
   return t.fm != 0 || (xk | 3) >= min(t.tr, t.tl);
 }
 __device__ __forceinline__ bool is_inf(double x) { return fabs(x) == CUDART_INF; }
+
+// The slice's filter words are dead once its phase 2 has read them (every
+// round writes them again before reading): their L2 lines are dropped
+// without a write-back (one 128 B line per step: 32 words of one step).
+// sw points at this lane's word of step 0.
+__device__ __forceinline__ void discard_words(const int32_t* sw, int steps, int lane) {
+  if (!PG_SELL_DISCARD) return;
+  const int32_t* p = sw - lane;
+  for (int t = lane; t < steps; t += 32)
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p + 32 * t) : "memory");
+}
 
 // ---- per-warp shared state ----------------------------------------------------------
 struct SellWarpSmem {
@@ -386,7 +410,10 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
   }
   if (j == 0) W.may[u] = may;
   if (PG_SELL_DEBUG && (cfg.flags & 0x10000u)) return;  // timing experiments only: no phase 2
-  if (!__any_sync(0xffffffffu, may)) return;
+  if (!__any_sync(0xffffffffu, may)) {
+    discard_words(sw, steps, lane);
+    return;
+  }
 
   // ---- phase 2: filter words -> queue -> exact pipeline ------------------------------
   __syncwarp();
@@ -431,6 +458,7 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
     inf_flag |= sell_drain(A, W, sd.off, qn, lane, pol_keep, cfg);
   }
   __syncwarp();
+  discard_words(sw, steps, lane);
 }
 
 // One slice by one warp.  LG = log2(lanes per unit); kDense: a full sweep
@@ -1015,13 +1043,13 @@ __device__ __forceinline__ void sell_sweep(const RA& A, const DevCfg& cfg,
   // work items by ticket, longest first; the next ticket is taken when an
   // item starts and read when it ends (its latency hides under the item)
   int next = 0;
-  if (lane == 0) next = atomicAdd(&A.st->work, 1);
+  if (lane == 0) next = ticket(&A.st->work);
   next = __shfl_sync(0xffffffffu, next, 0);
   const int nitems = A.group_start + (A.nslices - A.group_start + kSellGroup - 1) / kSellGroup;
   while (next < nitems) {
     const int s = next;
     int nxt = 0;
-    if (lane == 0) nxt = atomicAdd(&A.st->work, 1);
+    if (lane == 0) nxt = ticket(&A.st->work);
     if (s >= A.group_start) {
       // a group of narrow one-lane slices
       const int s0 = A.group_start + (s - A.group_start) * kSellGroup;
