@@ -284,7 +284,8 @@ void pg_mps_free(pg_mps* h);
  * the last solve that used the sparse delta exchange, host round trips of
  * the last row-sharded solve (one per graph of unrolled rounds), delta
  * rounds held by a capacity overflow and resumed with the dense all-reduce,
- * rounds per unrolled graph, graphs of delta rounds launched. */
+ * rounds per unrolled graph, graphs of delta rounds launched, bytes of the
+ * per-entry column record the round kernels gather (32, 16 or 8). */
 int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info);
 
 /* Thread-local message of the last failed call on this thread. */

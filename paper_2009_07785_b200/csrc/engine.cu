@@ -310,6 +310,7 @@ struct pg_session {
   double* d_rhs = nullptr;
   Snap* d_snap = nullptr;
   double2* d_bnd = nullptr;  // compact {lb, ub} records (sell.cuh gathers)
+  float2* d_bf = nullptr;    // float {lb, ub} records (DevCfg::bf), when the bounds are floats
   uint8_t* d_integral = nullptr;
   int32_t* d_row_done = nullptr;
   longlong2* d_key_out = nullptr;
@@ -369,13 +370,21 @@ struct pg_session {
   // precomputed, no per-entry recompute) when those fit in L2 beside the
   // streamed matrix
   double row_density = 0.0;
-  bool gather16() const {
+  // the 32 B records must also stay L2-resident next to the streamed matrix
+  // (C5: 5M columns = 160 MB of snapshot records, 80 MB of bounds records)
+  bool many_cols() const { return (double)n * sizeof(Snap) > 48e6; }
+  // gather record of the round kernels (RoundArgsG): 0 = 32 B snapshot
+  // records, 1 = 16 B bounds, 2 = 8 B float bounds (d_bf, kept when the
+  // sampled start bounds are floats of integral columns, whose tightened
+  // bounds stay integers; a bound that is not a float falls back to its
+  // 16 B record, so the choice is a matter of speed only)
+  int gather_kind() const {
     static const char* e = getenv("PG_SELL_GATHER");
-    if (e) return atoi(e) == 16;
-    // the 32 B records must also stay L2-resident next to the streamed matrix
-    // (C5: 5M columns = 160 MB of snapshot records, 80 MB of bounds)
-    return row_density > 0.05 || (double)n * sizeof(Snap) > 48e6;
+    if (e) return atoi(e) == 8 && d_bf ? 2 : atoi(e) == 16 ? 1 : 0;
+    if (many_cols() && d_bf) return 2;
+    return row_density > 0.05 || many_cols() ? 1 : 0;
   }
+  bool gather16() const { return gather_kind() != 0; }
   // sparse delta exchange (PG_FLAG_DELTA_EXCHANGE): this rank's items, every
   // rank's items, counts; rounds of the last solve that used it
   DeltaItem* d_delta = nullptr;
@@ -434,7 +443,7 @@ struct pg_session {
         (void**)&d_integral, (void**)&d_row_done, (void**)&d_key_out, (void**)&d_lo0, (void**)&d_up0,
         (void**)&d_lo_res, (void**)&d_up_res, (void**)&d_segs, (void**)&d_srow, (void**)&d_sfirst,
         (void**)&d_partial, (void**)&d_ract, (void**)&d_wl_short, (void**)&d_wl_long,
-        (void**)&d_f32_part, (void**)&d_ractf, (void**)&d_partf, (void**)&d_split, (void**)&d_bnd,
+        (void**)&d_f32_part, (void**)&d_ractf, (void**)&d_partf, (void**)&d_split, (void**)&d_bnd, (void**)&d_bf,
         (void**)&d_units, (void**)&d_slices, (void**)&d_sv, (void**)&d_sc, (void**)&d_sw, (void**)&d_st,
         (void**)&d_per_round, (void**)&d_col_ptr, (void**)&d_col_item, (void**)&d_flags, (void**)&d_chg,
         (void**)&d_row_unit, (void**)&d_part_unit, (void**)&d_unit_slice, (void**)&d_wide_list,
@@ -488,7 +497,7 @@ struct pg_session {
 
   // phase 1 over the sliced-ELL copy: the full sweep, and with the worklist
   // the worklist sweep (each returns at once when the round is of the other kind)
-  template <bool kB16>
+  template <int kB16>
   void launch_sell(const RoundArgsG<kB16>& G, int grid, bool rowcheck) {
     const int dgrid = std::max(1, std::min((nslices + 7) / 8, num_sms * sell_dense_per_sm));
     if (rowcheck)
@@ -538,10 +547,11 @@ struct pg_session {
       }
     } else if (nslices > 0) {
       const int grid = std::max(1, std::min((nslices + 7) / 8, num_sms * sell_per_sm));
-      if (gather16())
-        launch_sell(RoundArgsG<true>{A}, grid, rowcheck);
-      else
-        launch_sell(RoundArgsG<false>{A}, grid, rowcheck);
+      switch (gather_kind()) {
+        case 2: launch_sell(RoundArgsG<2>{A}, grid, rowcheck); break;
+        case 1: launch_sell(RoundArgsG<1>{A}, grid, rowcheck); break;
+        default: launch_sell(RoundArgsG<0>{A}, grid, rowcheck);
+      }
       if (nsplit > 0) {
         const int g = std::max(1, std::min((nsplit + kSplitWarps - 1) / kSplitWarps, num_sms * 8));
         if (rowcheck)
@@ -976,6 +986,23 @@ struct pg_session {
 
 namespace {
 
+// Whether the round kernels should gather 8 B float bound records: at least
+// 95 % of up to 4096 evenly spaced columns are integral with both start
+// bounds floats (their tightened bounds stay integers).  Speed only: a
+// column whose bounds are not floats is read from its exact record.
+static bool float_bounds_sample(const pg_problem* p) {
+  const int32_t n = p->num_cols;
+  if (n <= 0) return false;
+  const int32_t k = std::min<int32_t>(n, 4096);
+  int32_t ok = 0;
+  for (int32_t i = 0; i < k; ++i) {
+    const int32_t j = (int32_t)((int64_t)i * n / k);
+    const double l = p->lower[j], u = p->upper[j];
+    ok += p->integral[j] && (double)(float)l == l && (double)(float)u == u;
+  }
+  return ok >= k - k / 20;
+}
+
 pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
   PhaseTimer tm;
   check_problem(p);
@@ -1007,25 +1034,31 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       Occ& o = occ[s->dev];
       if (!o.ok) {
         for (const void* f :
-             {(const void*)k_sell<true, true, true>, (const void*)k_sell<false, true, true>,
-              (const void*)k_sell<true, false, true>, (const void*)k_sell<false, false, true>,
-              (const void*)k_sell<true, true, false>, (const void*)k_sell<false, true, false>,
-              (const void*)k_sell<true, false, false>, (const void*)k_sell<false, false, false>})
+             {(const void*)k_sell<true, true, 1>, (const void*)k_sell<false, true, 1>,
+              (const void*)k_sell<true, false, 1>, (const void*)k_sell<false, false, 1>,
+              (const void*)k_sell<true, true, 0>, (const void*)k_sell<false, true, 0>,
+              (const void*)k_sell<true, false, 0>, (const void*)k_sell<false, false, 0>,
+              (const void*)k_sell<true, true, 2>, (const void*)k_sell<false, true, 2>,
+              (const void*)k_sell<true, false, 2>, (const void*)k_sell<false, false, 2>})
           PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSellSmem));
         for (const void* f : {(const void*)k_loop<true>, (const void*)k_loop<false>})
           PG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)sizeof(LoopSmem)));
-        int o16 = 0, d32 = 0, d16 = 0;
-        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.sell, k_sell<true, false, false>,
+        int o16 = 0, o8 = 0, d32 = 0, d16 = 0, d8 = 0;
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.sell, k_sell<true, false, 0>,
                                                               kSellThreads, kSellSmem));
-        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o16, k_sell<true, false, true>,
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o16, k_sell<true, false, 1>,
                                                               kSellThreads, kSellSmem));
-        o.sell = std::min(o.sell, o16);
-        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d32, k_sell<true, true, false>,
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o8, k_sell<true, false, 2>,
+                                                              kSellThreads, kSellSmem));
+        o.sell = std::min(o.sell, std::min(o16, o8));
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d32, k_sell<true, true, 0>,
                                                               kSellThreads, kSellSmemDense));
-        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d16, k_sell<true, true, true>,
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d16, k_sell<true, true, 1>,
                                                               kSellThreads, kSellSmemDense));
-        o.sell_dense = std::min(d32, d16);
+        PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&d8, k_sell<true, true, 2>,
+                                                              kSellThreads, kSellSmemDense));
+        o.sell_dense = std::min(d32, std::min(d16, d8));
         PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o.cand, k_cand, kCandThreads, 0));
         int per = 0, per2 = 0;
         PG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_loop<true>, kSellThreads,
@@ -1228,6 +1261,12 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
       PG_CUDA(cudaMemcpyAsync(s->d_snap + n, &pad, sizeof(Snap), cudaMemcpyHostToDevice, st));
       s->d_bnd = dalloc<double2>((size_t)n + 1);
       PG_CUDA(cudaMemsetAsync(s->d_bnd + n, 0, sizeof(double2), st));
+      static const char* ge = getenv("PG_SELL_GATHER");  // "8": forced (tests, A/B)
+      if ((ge && atoi(ge) == 8) || (s->many_cols() && float_bounds_sample(p))) {
+        s->d_bf = dalloc<float2>((size_t)n + 1);
+        PG_CUDA(cudaMemsetAsync(s->d_bf + n, 0, sizeof(float2), st));
+        s->dcfg.bf = s->d_bf;
+      }
     }
     s->d_key_out = dalloc<longlong2>((size_t)n + 1);  // + infeasibility slot
     s->d_lo0 = dalloc<double>(n);
@@ -1492,10 +1531,10 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         PG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
         cudaStreamAttrValue av = {};
         // the array the full sweep gathers from: 16 B bounds or 32 B records
-        const bool b16 = s->gather16();
-        av.accessPolicyWindow.base_ptr = b16 ? (void*)s->d_bnd : (void*)s->d_snap;
+        const int gk = s->gather_kind();
+        av.accessPolicyWindow.base_ptr = gk == 2 ? (void*)s->d_bf : gk == 1 ? (void*)s->d_bnd : (void*)s->d_snap;
         av.accessPolicyWindow.num_bytes =
-            std::min((b16 ? sizeof(double2) : sizeof(Snap)) * ((size_t)n + 1), want);
+            std::min((gk == 2 ? sizeof(float2) : gk == 1 ? sizeof(double2) : sizeof(Snap)) * ((size_t)n + 1), want);
         av.accessPolicyWindow.hitRatio = 1.0f;
         av.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
         av.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
@@ -2425,7 +2464,8 @@ int pg_session_info(const pg_session* s, int64_t* info, int32_t n_info) {
   const int64_t v[] = {s->m, s->n, s->nnz, s->nslices, s->nsrow, s->nseg,
                        s->short_rows, s->short_nnz, s->seg_nnz, s->nunits, s->sell_elems,
                        s->nsplit, s->use_persistent() ? 1 : 0, s->delta_rounds,
-                       s->host_syncs, s->held_rounds, s->shard_rounds, s->delta_graphs};
+                       s->host_syncs, s->held_rounds, s->shard_rounds, s->delta_graphs,
+                       s->gather_kind() == 2 ? 8 : s->gather_kind() == 1 ? 16 : 32};
   for (int i = 0; i < n_info && i < (int)(sizeof(v) / sizeof(v[0])); ++i) info[i] = v[i];
   return PG_OK;
 }

@@ -411,14 +411,21 @@ struct RoundArgs {
 };
 
 // RoundArgs with the gather record fixed at compile time (sell.cuh ld_col):
-// 16 B bounds records for rows dense in the columns, else 32 B snapshot
-// records; plain RoundArgs gathers the snapshot records
-template <bool kB16>
+// kG = 0: 32 B snapshot records (q precomputed), 1: 16 B bounds records for
+// rows dense in the columns or columns too many for 32 B records in L2,
+// 2: 8 B float records (DevCfg::bf) when the bounds are floats (integral
+// columns; C5: 5M columns = 40 MB instead of 80 MB); plain RoundArgs
+// gathers the snapshot records
+template <int kG>
 struct RoundArgsG : RoundArgs {};
 template <class RA>
 constexpr bool gather16_v = false;
 template <>
-constexpr bool gather16_v<RoundArgsG<true>> = true;
+constexpr bool gather16_v<RoundArgsG<1>> = true;
+template <class RA>
+constexpr bool gather8_v = false;
+template <>
+constexpr bool gather8_v<RoundArgsG<2>> = true;
 // the persistent round loop (loop.cuh): snapshot and bounds records are
 // rewritten by the commit phase inside the same kernel, so its gathers use
 // coherent loads (never ld.global.nc)
@@ -585,6 +592,7 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
           const long long fl = snap[j].flags;
           snap[j] = Snap{lo, up, column_q(lo, up, fl & 1, cfg), fl};
           bnd[j] = make_double2(lo, up);
+          if (cfg.bf) cfg.bf[j] = fpair(lo, up);
         }
         if (lo > __dadd_rn(up, cfg.imp_abs)) inf = 1;
       }
@@ -705,6 +713,7 @@ __global__ void __launch_bounds__(kCommitThreads)
     const bool in = integral[j] != 0;
     snap[j] = Snap{l, u, column_q(l, u, in, cfg), in ? 1LL : 0LL};
     bnd[j] = make_double2(l, u);
+    if (cfg.bf) cfg.bf[j] = fpair(l, u);
     key_out[j] = make_longlong2(key_enc(l), -key_enc(u));
     if (l > __dadd_rn(u, cfg.imp_abs)) crossed = 1;
     if (in && (l != floor(l) || u != ceil(u))) frac = 1;  // floor(+-inf) = +-inf

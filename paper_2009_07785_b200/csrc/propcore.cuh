@@ -22,7 +22,18 @@ struct DevCfg {
   int32_t round_limit;
   uint32_t flags;
   int32_t pad;
+  // compact {lb, ub} records of the round's input bounds as floats, {NaN,
+  // NaN} where a bound is not a float (sell.cuh ld_col then reads the exact
+  // 16 B record); null when the session does not keep them
+  float2* bf;
 };
+
+// the compact record of [lo, up] (exact or the NaN marker)
+__device__ __forceinline__ float2 fpair(double lo, double up) {
+  const float fl = __double2float_rn(lo), fu = __double2float_rn(up);
+  if ((double)fl == lo && (double)fu == up) return make_float2(fl, fu);
+  return make_float2(__int_as_float(0x7fffffff), __int_as_float(0x7fffffff));
+}
 
 // ---- GPU-scope relaxed loads -------------------------------------------------
 // Device state written by other CTAs (earlier kernels, or before a grid

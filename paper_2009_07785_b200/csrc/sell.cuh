@@ -163,6 +163,25 @@ __device__ __forceinline__ void ld_col(const RA& A, int32_t c, uint64_t pol, boo
                                        const DevCfg& cfg, double& lo, double& up, double& q) {
   if constexpr (coherent_v<RA>) {
     ld_snap_coh(A.snap + (c & 0x7fffffff), lo, up, q);
+  } else if constexpr (gather8_v<RA>) {
+    const int32_t j = c & 0x7fffffff;
+    float2 f;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.f32 {%0,%1}, [%2], %3;"
+                 : "=f"(f.x), "=f"(f.y)
+                 : "l"(cfg.bf + j), "l"(pol));
+    if (f.x == f.x) {
+      lo = f.x;
+      up = f.y;
+    } else {
+      // a bound that is not a float: the exact record
+      double2 b;
+      asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
+                   : "=d"(b.x), "=d"(b.y)
+                   : "l"(A.bnd + j), "l"(pol));
+      lo = b.x;
+      up = b.y;
+    }
+    q = column_q_inline(lo, up, c < 0, frac_any, cfg);
   } else if constexpr (gather16_v<RA>) {
     double2 b;
     asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;"
@@ -1084,9 +1103,9 @@ __device__ __forceinline__ bool sell_dense_round(const RoundArgs& A) {
   return !round_is_sparse(A.st, A.dirty);
 }
 
-template <bool kRowCheck, bool kDense, bool kB16>
+template <bool kRowCheck, bool kDense, int kG>
 __global__ void __launch_bounds__(kSellThreads, kDense ? PG_SELL_MINB_DENSE : PG_SELL_MINB)
-    k_sell(const RoundArgsG<kB16> A,
+    k_sell(const RoundArgsG<kG> A,
                                                                      const DevCfg cfg) {
   extern __shared__ __align__(16) unsigned char sell_dyn[];  // kSellWarps x SellWarpSmem
   SellWarpSmem* smem = reinterpret_cast<SellWarpSmem*>(sell_dyn);

@@ -208,7 +208,8 @@ class Session:
 
     INFO_FIELDS = ("m", "n", "nnz", "slices", "seg_rows", "segments", "short_rows", "short_nnz",
                    "seg_nnz", "chains", "sell_elems", "split_rows", "persistent",
-                   "delta_rounds", "host_syncs", "held_rounds", "shard_rounds", "delta_graphs")
+                   "delta_rounds", "host_syncs", "held_rounds", "shard_rounds", "delta_graphs",
+                   "gather_bytes")
 
     def __init__(self, instance: ProblemInstance, cfg: EngineConfig | None = None):
         self.cfg = cfg or EngineConfig()

@@ -434,7 +434,8 @@ from paper_2009_07785_b200.model import EngineConfig
 PAR = EngineConfig(row_check=False)
 insts = [G.gen_powerlaw(100000, 100000, 20090778, cap=2000),
          G.gen_longrows(3000, 6000, 3001, long_every=100, long_min=1500, long_max=4000),
-         G.gen_random(20000, 20000, 5, mean_row_nnz=8.0, integral_fraction=0.5)]
+         G.gen_random(20000, 20000, 5, mean_row_nnz=8.0, integral_fraction=0.5),
+         G.gen_setpart(20000, 100000, 20, seed=5001)]
 for inst in insts:
     for wl in (False, True):
         g = propagate_gpu(inst, EngineConfig(row_check=False, worklist=wl))
@@ -448,10 +449,11 @@ print("ok")
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("gather", ["16", "32"])
+@pytest.mark.parametrize("gather", ["8", "16", "32"])
 def test_gather_record_modes(gather):
-    """both gather records (16 B bounds + recomputed q, 32 B snapshot) forced
-    on instances of either kind: bit-exact with the oracle"""
+    """every gather record (8 B float bounds with the exact 16 B record for
+    bounds that are not floats, 16 B bounds + recomputed q, 32 B snapshot)
+    forced on instances of every kind: bit-exact with the oracle"""
     import os
     import subprocess
     import sys
