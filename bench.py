@@ -299,11 +299,11 @@ def _common_line(args, world, ms, scaling, workload, extra_cfg):
 
 def solve_launches(info, worklist):
     """Our kernels per round and per solve (engine.cu enqueue_round /
-    enqueue_reset): k_sell (full sweep) + k_cand + k_commit, k_split_finish
+    enqueue_reset): k_sell (full sweep) + k_commit, k_split_finish + k_cand
     with split rows, and with the worklist the worklist k_sell +
     k_commit_list + k_mark; per solve k_reset (+ k_mark_vars).  The
     persistent loop is one kernel per solve (+ k_reset)."""
-    per_round = ((2 if info["slices"] else 0) + 1 + (1 if info["split_rows"] else 0) +
+    per_round = ((1 if info["slices"] else 0) + 1 + (2 if info["split_rows"] else 0) +
                  (3 if worklist else 0))
     if info["persistent"]:
         per_round = 0
@@ -314,12 +314,12 @@ def solve_launches(info, worklist):
 def shard_launches(info, worklist, delta):
     """Kernels of one row-sharded solve in unrolled graphs: every launched
     graph runs shard_rounds rounds (rounds past the decision return at once)
-    of k_sell (+ worklist variant), [k_split_finish], k_cand, the exchange
+    of k_sell (+ worklist variant), [k_split_finish, k_cand], the exchange
     kernels (k_flag_to_slot; or k_delta_compact + k_delta_apply), k_commit,
     [k_mark]; plus k_reset (+ k_mark_vars) and one k_shard_resume per held
     round.  NCCL's own kernels are not counted."""
-    base = ((2 if worklist else 1) if info["slices"] else 0) + (1 if info["split_rows"] else 0) + \
-        1 + 1 + (1 if worklist else 0)
+    base = ((2 if worklist else 1) if info["slices"] else 0) + (2 if info["split_rows"] else 0) + \
+        1 + (1 if worklist else 0)
     R = max(info["shard_rounds"], 1)
     dg = info["delta_graphs"]
     return ((info["host_syncs"] - dg) * R * (base + 1) + dg * R * (base + 2) +

@@ -559,7 +559,8 @@ struct pg_session {
         else
           k_split_finish<false><<<g, kSplitWarps * 32, 0, stream>>>(A, d_split, nsplit, dcfg);
       }
-      k_cand<<<num_sms * cand_per_sm, kCandThreads, 0, stream>>>(A, dcfg);
+      // phase 2 of split rows (their finisher queues them); none without
+      if (nsplit > 0) k_cand<<<num_sms * cand_per_sm, kCandThreads, 0, stream>>>(A, dcfg);
     }
     if (k1_end) PG_CUDA(cudaEventRecord(k1_end, stream));
     bool dense_exchange = comm != nullptr;

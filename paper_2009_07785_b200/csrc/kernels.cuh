@@ -573,7 +573,9 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
       jj[u] = i < nj ? (kList ? touch->list[i] : i) : -1;
       if (jj[u] >= 0) {
         kob[u] = key_out[jj[u]];
-        inb[u] = *reinterpret_cast<const double2*>(&snap[jj[u]].lo);
+        // the round's input bounds from the 16 B records (kept equal to
+        // the snapshot's lo/up): half the bytes of the 32 B records' sectors
+        inb[u] = bnd[jj[u]];
         if (kList) touch->flag[jj[u]] = 0u;
       }
     }

@@ -66,6 +66,19 @@ def test_shard_launch_count():
     import bench
     info = {"slices": 10, "split_rows": 0, "shard_rounds": 4, "host_syncs": 3, "delta_graphs": 1,
             "held_rounds": 1}
-    # 2 dense graphs x 4 rounds x (k_sell, k_cand, k_commit, k_flag_to_slot) + 1 delta graph x 4 x
-    # (k_sell, k_cand, k_commit, k_delta_compact, k_delta_apply) + k_reset + 1 resume
-    assert bench.shard_launches(info, False, True) == 2 * 4 * 4 + 4 * 5 + 1 + 1
+    # 2 dense graphs x 4 rounds x (k_sell, k_commit, k_flag_to_slot) + 1 delta graph x 4 x
+    # (k_sell, k_commit, k_delta_compact, k_delta_apply) + k_reset + 1 resume
+    assert bench.shard_launches(info, False, True) == 2 * 4 * 3 + 4 * 4 + 1 + 1
+    # split rows add k_split_finish and k_cand to every round
+    info["split_rows"] = 5
+    assert bench.shard_launches(info, False, True) == 2 * 4 * 5 + 4 * 6 + 1 + 1
+
+
+def test_solve_launch_count():
+    import bench
+    info = {"slices": 10, "split_rows": 0, "persistent": 0}
+    # k_sell + k_commit; the worklist adds its k_sell, k_commit_list, k_mark (+ k_mark_vars)
+    assert bench.solve_launches(info, False) == (2, 1)
+    assert bench.solve_launches(info, True) == (5, 2)
+    info["split_rows"] = 3  # + k_split_finish + k_cand
+    assert bench.solve_launches(info, True) == (7, 2)
