@@ -14,3 +14,5 @@ timeout 900 python bench.py --impl reference > gpurun_out/bench_${TAG}_ref.json 
 timeout 1800 python bench.py --config all --steps 5 > gpurun_out/bench_${TAG}_all.json 2> gpurun_out/bench_${TAG}_all.err; echo "bench all=$?"
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_${TAG}.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1 --loop host > gpurun_out/launches_${TAG}.log 2>&1; echo "launches=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sell -s 2 -c 1 -o gpurun_out/prof_${TAG} python tools/prof_round.py --reps 3 > gpurun_out/ncu_${TAG}.log 2>&1; echo "ncu_sell=$?"
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_sell -s 2 -c 1 -o gpurun_out/prof_${TAG}_c5 python tools/prof_round.py --config c5 --reps 3 > gpurun_out/ncu_${TAG}_c5.log 2>&1; echo "ncu_sell_c5=$?"
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_${TAG}_c5.csv python bench.py --config c5 --steps 1 --warmup 3 --no-cpu-baseline --e2e-steps 1 --loop host > gpurun_out/launches_${TAG}_c5.log 2>&1; echo "launches_c5=$?"
