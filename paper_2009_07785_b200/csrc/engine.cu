@@ -1484,6 +1484,7 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
         D.dense_nchg = (int32_t)std::min<double>(2e9, per / div);
         D.dense_deg = fdeg * (double)m;  // compared with entries x wsum / nunits
         D.list_gate = (long long)std::min<double>(9e18, gate * per);
+        D.mark_batch = getenv("PG_MARK_BATCH") ? std::max(1, atoi(getenv("PG_MARK_BATCH"))) : 1;
         // a worklist round while the marked lane, long and mid units, weighted,
         // stay below the weighted unit count (round_is_sparse)
         int w[4] = {8, 32, 2, 1};

@@ -116,6 +116,7 @@ struct Dirty {
   // a worklist round while w_lane nunit + w_wide nwide + w_mid nmid <= w_all nunits
   int32_t w_lane, w_wide, w_mid, w_all;
   int32_t unrolled;          // row-shard graphs of unrolled rounds (round_off)
+  int32_t mark_batch;        // k_mark: B columns per warp once there are mark_batch x B per warp
 };
 
 // Row r (sorted) becomes marked for the round of parity `par` (exactly once:
@@ -547,7 +548,7 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
                                             const DevCfg& cfg, const Dirty& D,
                                             cudaGraphConditionalHandle cond, int use_graph,
                                             const Touch* touch = nullptr) {
-  unsigned long long changes = 0;
+  unsigned long long changes = 0, deg = 0;
   int inf = 0;
   const int R = ld_gpu(&st->round);  // rounds before this one
   const int nb = R & 1;                             // buffer of the next round's lists
@@ -579,6 +580,7 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
         if (kList) touch->flag[jj[u]] = 0u;
       }
     }
+    int cu[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int j = jj[u];
@@ -598,21 +600,33 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
         }
         if (lo > __dadd_rn(up, cfg.imp_abs)) inf = 1;
       }
-      if (list) {
-        // changed columns of this round -> list (one atomic per warp), and
-        // the number of entries their marks will visit
-        const unsigned chm = __ballot_sync(0xffffffffu, c != 0);
-        if (chm) {
-          int base = 0;
-          if (lane == 0) base = atomicAdd(&st->nchg[cb], __popc(chm));
-          base = __shfl_sync(0xffffffffu, base, 0);
-          if (c) D.chg_list[(size_t)cb * D.n + base + __popc(chm & ((1u << lane) - 1u))] = j;
-          int deg = c ? D.col_ptr[j + 1] - D.col_ptr[j] : 0;
+      cu[u] = c;
+    }
+    if (list) {
+      // changed columns of this round -> list (one atomic per warp for its
+      // U columns per lane: the counter is a single address every warp of
+      // the grid appends to), and the number of entries their marks will
+      // visit (summed per thread, one atomic per CTA below)
+      unsigned chm[U];
+      int tot = 0;
 #pragma unroll
-          for (int o = 16; o; o >>= 1) deg += __shfl_xor_sync(0xffffffffu, deg, o);
-          if (lane == 0 && deg)
-            atomicAdd(reinterpret_cast<unsigned long long*>(&st->chg_deg[cb]), (unsigned long long)deg);
+      for (int u = 0; u < U; ++u) {
+        chm[u] = __ballot_sync(0xffffffffu, cu[u] != 0);
+        tot += __popc(chm[u]);
       }
+      if (tot) {
+        int base = 0;
+        if (lane == 0) base = atomicAdd(&st->nchg[cb], tot);
+        base = __shfl_sync(0xffffffffu, base, 0);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (cu[u]) {
+            const int j = jj[u];
+            D.chg_list[(size_t)cb * D.n + base + __popc(chm[u] & ((1u << lane) - 1u))] = j;
+            deg += (unsigned long long)(D.col_ptr[j + 1] - D.col_ptr[j]);
+          }
+          base += __popc(chm[u]);
+        }
       }
     }
   }
@@ -621,8 +635,11 @@ __device__ __forceinline__ void commit_body(Snap* __restrict__ snap, double2* __
     uint32_t* f = reinterpret_cast<uint32_t*>(D.row_flag + (size_t)cb * D.ms);
     for (int i = gtid; i < D.ms / 4; i += gstride) f[i] = 0u;
   }
+  int unused = 0;
+  deg = block_sum<kCommitThreads>(deg, unused);
   changes = block_sum<kCommitThreads>(changes, inf);
   if (threadIdx.x == 0) {
+    if (deg) atomicAdd(reinterpret_cast<unsigned long long*>(&st->chg_deg[cb]), deg);
     if (changes) atomicAdd(&st->round_changes, changes);
     if (inf) st->infeasible = 1;
     __threadfence();
@@ -1016,26 +1033,52 @@ __device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__
   const int nchg = ld_gpu(&st->nchg[cb]);
   uint8_t* flag = D.row_flag + (size_t)nb * D.ms;
   const int lane = threadIdx.x & 31;
-  // one warp per changed column
-  for (int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; w < nchg;
-       w += (gridDim.x * blockDim.x) >> 5) {
-    const int j = D.chg_list[(size_t)cb * D.n + w];
-    for (int e = D.col_ptr[j] + lane; e < D.col_ptr[j + 1]; e += 32) {
-      const int row = D.col_row[e];
+  // a warp takes B changed columns and walks their rows flattened over the
+  // lanes (a column has few rows: one column per warp leaves most lanes idle
+  // and pays one list append per column on the shared counters); B = 1 while
+  // the columns are fewer than the warps, up to 32 with many
+  const int nwarps = (gridDim.x * blockDim.x) >> 5;
+  int B = 1;
+  while (B < 32 && (long long)nchg >= (long long)max(D.mark_batch, 1) * 2 * B * nwarps) B <<= 1;
+  for (int w0 = B * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); w0 < nchg; w0 += B * nwarps) {
+    int e0 = 0, d = 0;
+    if (lane < B && w0 + lane < nchg) {
+      const int j = D.chg_list[(size_t)cb * D.n + w0 + lane];
+      e0 = D.col_ptr[j];
+      d = D.col_ptr[j + 1] - e0;
+    }
+    int incl = d;  // inclusive scan of the degrees
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    const int excl = incl - d;
+    for (int t0 = 0; t0 < total; t0 += 32) {
+      const int t = t0 + lane;
+      // the column of flattened entry t: the last lane whose start is <= t
+      // (fixed five steps, every lane shuffles)
+      int pos = 0;
+#pragma unroll
+      for (int b = 16; b; b >>= 1)
+        if (__shfl_sync(0xffffffffu, excl, pos + b) <= t) pos += b;
+      const int e = __shfl_sync(0xffffffffu, e0, pos) + t - __shfl_sync(0xffffffffu, excl, pos);
       bool single = false;
       int u = -1;
-      if (mark_row(flag, row)) {
-        u = D.row_unit[row];
-        single = u >= 0 && D.unit_slice[u] == -1;
-        if (!single) mark_row_units(D, row, nb, st);
+      if (t < total) {
+        const int row = D.col_row[e];
+        if (mark_row(flag, row)) {
+          u = D.row_unit[row];
+          single = u >= 0 && D.unit_slice[u] == -1;
+          if (!single) mark_row_units(D, row, nb, st);
+        }
       }
-      const unsigned act = __activemask();
-      const unsigned bal = __ballot_sync(act, single);
+      const unsigned bal = __ballot_sync(0xffffffffu, single);
       if (bal) {
-        const int leader = __ffs(act) - 1;
         int base = 0;
-        if (lane == leader) base = atomicAdd(&st->nunit[nb], __popc(bal));
-        base = __shfl_sync(act, base, leader);
+        if (lane == 0) base = atomicAdd(&st->nunit[nb], __popc(bal));
+        base = __shfl_sync(0xffffffffu, base, 0);
         if (single)
           D.unit_list[(size_t)nb * D.nunits + base + __popc(bal & ((1u << lane) - 1u))] = u;
       }
