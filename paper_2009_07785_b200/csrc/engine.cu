@@ -416,6 +416,7 @@ struct pg_session {
   double* d_keep_up = nullptr;
   double* d_root_up = nullptr;
   bool has_root = false;
+  bool l2_window = false;  // a persisting-L2 access window on the session stream
 
   ~pg_session() {
     if (dev >= 0) cudaSetDevice(dev);
@@ -425,6 +426,13 @@ struct pg_session {
     destroy_shard_graphs();
 
     if (comm && !comm_aborted) g_nccl.comm_destroy(comm);  // an aborted one is freed already
+    if (l2_window) {
+      // the pooled stream must not carry this session's window into the next
+      cudaStreamAttrValue av = {};
+      av.accessPolicyWindow.num_bytes = 0;
+      cudaStreamSetAttribute(stream, cudaStreamAttributeAccessPolicyWindow, &av);
+      cudaCtxResetPersistingL2Cache();
+    }
     release_buffers();
     if (h_dcnt) cudaFreeHost(h_dcnt);
     StreamPool::get().put(dev, StreamSet{stream, stream2, ev0, ev1, ev_fork, ev_join, h_st});
@@ -1525,11 +1533,21 @@ pg_session* create_session(const pg_problem* p, const pg_config* cfg) {
                     (void*)t_perm})
       dfree(q);
     tm.lap("worklist/bounds (queued)");
-    // keep the snapshot records (the per-entry random gathers) resident in a
-    // persisting L2 carve-out while the matrix streams through
-    if (const char* e = getenv("PG_L2_PERSIST_MB")) {
-      const size_t want = (size_t)atoi(e) << 20;
+    // keep the gathered records resident in a persisting L2 carve-out while
+    // the matrix streams through: by default for the 8 B float records (C5:
+    // a 40 MB window in a 42 MB carve-out, first round 931 -> 878 us, solve
+    // 7.47 -> 7.20 ms; a 64 MB carve-out 7.77 ms; the
+    // 32 B / 16 B records measured slower with one, section 4 of DESIGN.md)
+    {
+      size_t want = 0;
+      if (const char* e = getenv("PG_L2_PERSIST_MB")) want = (size_t)atoi(e) << 20;
+      else if (s->gather_kind() == 2) want = sizeof(float2) * ((size_t)n + 1) * 21 / 20;
+      int maxp = 0, maxw = 0;
+      PG_CUDA(cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, s->dev));
+      PG_CUDA(cudaDeviceGetAttribute(&maxw, cudaDevAttrMaxAccessPolicyWindowSize, s->dev));
+      want = std::min(want, (size_t)std::min(maxp, maxw));
       if (want) {
+        s->l2_window = true;
         PG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
         cudaStreamAttrValue av = {};
         // the array the full sweep gathers from: 16 B bounds or 32 B records

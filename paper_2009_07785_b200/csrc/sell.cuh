@@ -61,6 +61,9 @@ namespace pgb {
 #ifndef PG_SELL_DEBUG
 #define PG_SELL_DEBUG 0  // 1: cfg.flags 0x10000 skips phase 2 (timing experiments)
 #endif
+#ifndef PG_SELL_UL0
+#define PG_SELL_UL0 PG_SELL_UNROLL  // full sweeps, one-lane slices: steps in flight per lane
+#endif
 #ifndef PG_SELL_LGU
 #define PG_SELL_LGU 2  // slices with lg >= this use PG_SELL_ULONG steps per group
 #endif
@@ -86,6 +89,10 @@ constexpr int kSellUnroll = PG_SELL_UNROLL;
 constexpr int kSellThreads = 256;
 constexpr int kSellWarps = kSellThreads / 32;
 constexpr int kSellGroup = PG_SELL_GROUP;
+#ifndef PG_MID_UNROLL
+#define PG_MID_UNROLL 4  // C5 worklist rounds: 7.70 -> 7.46 ms (2: round-1 value, 8: 7.66)
+#endif
+constexpr int kMidU = PG_MID_UNROLL;  // worklist mid units: 8-entry steps in flight
 constexpr int kSellLaneUnit = PG_SELL_LANEUNIT;  // worklist rounds: longer units get a warp each
 constexpr int kSellMidMax = PG_SELL_MIDMAX;      //   (up to this length: 8 lanes each)
 // lanes per unit by unit length: > 256 -> 8, > 128 -> 4, > 64 -> 2, else 1
@@ -510,7 +517,7 @@ __device__ __forceinline__ void sell_slice(const RA& A, SellWarpSmem& W, const S
   Act act = {0.0, 0.0, 0, 0};
   int32_t xk = kFKeyMin;
   if (kDense) {
-    constexpr int UL = LG >= PG_SELL_LGU ? PG_SELL_ULONG : kSellUnroll;
+    constexpr int UL = LG >= PG_SELL_LGU ? PG_SELL_ULONG : LG == 0 ? PG_SELL_UL0 : kSellUnroll;
     // every lane walks all `steps` of the slice: entries past a unit's end are
     // padding (value 0, the padding column with bounds [0, 0]) and add +0.0
     const double* pa = sv;
@@ -871,13 +878,13 @@ __device__ __forceinline__ void sell_mid(const RA& A, int par, uint64_t pol_keep
     for (int o = 8; o < 32; o <<= 1) maxlen = max(maxlen, __shfl_xor_sync(0xffffffffu, maxlen, o));
     Act act = {0.0, 0.0, 0, 0};
     double xm = -CUDART_INF;
-    // steps of 8 entries, two in flight: loads of steps s, s + 1, then their
-    // gathers, then the ordered adds
-    for (int s0 = 0; 8 * s0 < maxlen; s0 += 2) {
-      double a[2], lo[2], up[2], q[2];
-      int32_t c[2];
+    // steps of 8 entries, kMidU in flight: loads of steps s .. s + kMidU - 1,
+    // then their gathers, then the ordered adds
+    for (int s0 = 0; 8 * s0 < maxlen; s0 += kMidU) {
+      double a[kMidU], lo[kMidU], up[kMidU], q[kMidU];
+      int32_t c[kMidU];
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < kMidU; ++k) {
         const int e = 8 * (s0 + k) + j;
         a[k] = 0.0;
         c[k] = A.pad_col;
@@ -887,9 +894,9 @@ __device__ __forceinline__ void sell_mid(const RA& A, int par, uint64_t pol_keep
         }
       }
 #pragma unroll
-      for (int k = 0; k < 2; ++k) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
+      for (int k = 0; k < kMidU; ++k) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
 #pragma unroll
-      for (int k = 0; k < 2; ++k) {
+      for (int k = 0; k < kMidU; ++k) {
         if (8 * (s0 + k) >= maxlen) break;  // warp-uniform
         const bool in = 8 * (s0 + k) + j < len;
         const double bmin = a[k] > 0 ? lo[k] : up[k];
