@@ -209,6 +209,7 @@ __device__ __forceinline__ void cand_sweep(const RA& A, const DevCfg& cfg,
 
 __global__ void __launch_bounds__(kCandThreads) k_cand(const RoundArgs A, const DevCfg cfg) {
   __shared__ CandWarpSmem smem[kCandWarps];
+  pdl_begin();
   if (compute_off(A.st, cfg)) return;
   cand_sweep(A, cfg, smem);
 }

@@ -503,20 +503,43 @@ struct pg_session {
     return A;
   }
 
+  // A round kernel on the session stream with programmatic dependent launch
+  // (PG_PDL, default on): its CTAs are scheduled while the previous
+  // kernel's last CTAs run and wait for its completion in pdl_begin()
+  // (kernels.cuh) -- the per-kernel launch gap of the round's chain
+  static bool use_pdl() {
+    static const bool on = !getenv("PG_PDL") || atoi(getenv("PG_PDL")) != 0;
+    return on;
+  }
+  template <typename... KArgs, typename... Args>
+  void pdl(void (*k)(KArgs...), int grid, int block, size_t smem, Args... args) {
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3((unsigned)grid);
+    c.blockDim = dim3((unsigned)block);
+    c.dynamicSmemBytes = smem;
+    c.stream = stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    c.attrs = at;
+    c.numAttrs = use_pdl() ? 1 : 0;
+    PG_CUDA(cudaLaunchKernelEx(&c, k, args...));
+  }
+
   // phase 1 over the sliced-ELL copy: the full sweep, and with the worklist
   // the worklist sweep (each returns at once when the round is of the other kind)
   template <int kB16>
   void launch_sell(const RoundArgsG<kB16>& G, int grid, bool rowcheck) {
     const int dgrid = std::max(1, std::min((nslices + 7) / 8, num_sms * sell_dense_per_sm));
     if (rowcheck)
-      k_sell<true, true, kB16><<<dgrid, kSellThreads, kSellSmemDense, stream>>>(G, dcfg);
+      pdl(k_sell<true, true, kB16>, dgrid, kSellThreads, kSellSmemDense, G, dcfg);
     else
-      k_sell<false, true, kB16><<<dgrid, kSellThreads, kSellSmemDense, stream>>>(G, dcfg);
+      pdl(k_sell<false, true, kB16>, dgrid, kSellThreads, kSellSmemDense, G, dcfg);
     if (dirty.enabled) {
       if (rowcheck)
-        k_sell<true, false, kB16><<<grid, kSellThreads, kSellSmem, stream>>>(G, dcfg);
+        pdl(k_sell<true, false, kB16>, grid, kSellThreads, kSellSmem, G, dcfg);
       else
-        k_sell<false, false, kB16><<<grid, kSellThreads, kSellSmem, stream>>>(G, dcfg);
+        pdl(k_sell<false, false, kB16>, grid, kSellThreads, kSellSmem, G, dcfg);
     }
   }
 
@@ -563,12 +586,12 @@ struct pg_session {
       if (nsplit > 0) {
         const int g = std::max(1, std::min((nsplit + kSplitWarps - 1) / kSplitWarps, num_sms * 8));
         if (rowcheck)
-          k_split_finish<true><<<g, kSplitWarps * 32, 0, stream>>>(A, d_split, nsplit, dcfg);
+          pdl(k_split_finish<true>, g, kSplitWarps * 32, 0, A, (const int32_t*)d_split, nsplit, dcfg);
         else
-          k_split_finish<false><<<g, kSplitWarps * 32, 0, stream>>>(A, d_split, nsplit, dcfg);
+          pdl(k_split_finish<false>, g, kSplitWarps * 32, 0, A, (const int32_t*)d_split, nsplit, dcfg);
       }
       // phase 2 of split rows (their finisher queues them); none without
-      if (nsplit > 0) k_cand<<<num_sms * cand_per_sm, kCandThreads, 0, stream>>>(A, dcfg);
+      if (nsplit > 0) pdl(k_cand, num_sms * cand_per_sm, kCandThreads, 0, A, dcfg);
     }
     if (k1_end) PG_CUDA(cudaEventRecord(k1_end, stream));
     bool dense_exchange = comm != nullptr;
@@ -627,13 +650,14 @@ struct pg_session {
     // commit / list / mark grids per SM (env overrides: A/B experiments)
     static const int commit_per_sm = getenv("PG_COMMIT_PER_SM") ? atoi(getenv("PG_COMMIT_PER_SM")) : 2;
     static const int list_per_sm = getenv("PG_LIST_PER_SM") ? atoi(getenv("PG_LIST_PER_SM")) : 2;
-    k_commit<<<grid_for(n, kCommitThreads, commit_per_sm), kCommitThreads, 0, stream>>>(
-        d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, cond,
+    pdl(k_commit, grid_for(n, kCommitThreads, commit_per_sm), kCommitThreads, 0, d_snap, d_bnd,
+        (const longlong2*)d_key_out, (int)n, d_st, d_per_round, dcfg, dirty, cond,
         use_graph && !unrolled ? 1 : 0, comm ? 0 : 1);
     if (dirty.enabled && !comm)
-      k_commit_list<<<num_sms * list_per_sm, kCommitThreads, 0, stream>>>(
-          d_snap, d_bnd, d_key_out, n, d_st, d_per_round, dcfg, dirty, touch, cond, use_graph ? 1 : 0);
-    if (dirty.enabled) k_mark<<<num_sms * list_per_sm, 256, 0, stream>>>(dirty, d_st);
+      pdl(k_commit_list, num_sms * list_per_sm, kCommitThreads, 0, d_snap, d_bnd,
+          (const longlong2*)d_key_out, (int)n, d_st, d_per_round, dcfg, dirty, touch, cond,
+          use_graph ? 1 : 0);
+    if (dirty.enabled) pdl(k_mark, num_sms * list_per_sm, 256, 0, dirty, d_st);
     PG_CUDA(cudaGetLastError());
   }
 

@@ -72,6 +72,16 @@ struct DevState {
 // Only those sessions pay the state loads (kUnrolledFlag in the kernel's
 // DevCfg); the other loops never launch a round after the decision.
 constexpr uint32_t kUnrolledFlag = 0x40000000u;
+// Programmatic dependent launch (engine.cu pdl()): wait until the previous
+// kernel of the stream has completed and its writes are visible, then let
+// the next kernel's CTAs be scheduled.  Both are no-ops for a kernel
+// launched without the attribute.  Every round kernel starts with this,
+// before any access to data an earlier kernel wrote.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 __device__ __forceinline__ bool round_off(DevState* st, const DevCfg& c) {
   return (c.flags & kUnrolledFlag) && (ld_gpu(&st->done) | ld_gpu(&st->stall)) != 0;
 }
@@ -697,6 +707,7 @@ __global__ void __launch_bounds__(kCommitThreads)
              const Dirty D, cudaGraphConditionalHandle cond, int use_graph, int allow_list) {
   // a worklist round of a single session is committed by k_commit_list; with
   // row shards every column may have moved on another rank: always in full
+  pdl_begin();
   if (round_off(st, cfg)) return;
   if (allow_list && ld_gpu(&st->sparse_round)) return;
   commit_body(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph);
@@ -708,6 +719,7 @@ __global__ void __launch_bounds__(kCommitThreads)
                   const longlong2* __restrict__ key_out, int n, DevState* __restrict__ st,
                   long long* __restrict__ per_round, const DevCfg cfg, const Dirty D, const Touch T,
                   cudaGraphConditionalHandle cond, int use_graph) {
+  pdl_begin();
   if (round_off(st, cfg) || !ld_gpu(&st->sparse_round)) return;
   commit_body<true>(snap, bnd, key_out, n, st, per_round, cfg, D, cond, use_graph, &T);
 }
@@ -1086,6 +1098,7 @@ __device__ __forceinline__ void mark_body(const Dirty& D, DevState* __restrict__
   }
 }
 __global__ void __launch_bounds__(256) k_mark(const Dirty D, DevState* __restrict__ st) {
+  pdl_begin();
   mark_body(D, st);
 }
 

@@ -1116,6 +1116,7 @@ __global__ void __launch_bounds__(kSellThreads, kDense ? PG_SELL_MINB_DENSE : PG
                                                                      const DevCfg cfg) {
   extern __shared__ __align__(16) unsigned char sell_dyn[];  // kSellWarps x SellWarpSmem
   SellWarpSmem* smem = reinterpret_cast<SellWarpSmem*>(sell_dyn);
+  pdl_begin();
   if (compute_off(A.st, cfg)) return;
   const bool dense = sell_dense_round(A);
   // the round's kind, for the commit kernels (written before any of them runs)

@@ -73,6 +73,7 @@ __global__ void __launch_bounds__(kSplitWarps * 32) k_split_finish(const RoundAr
                                                                    const int32_t* split, int nsplit,
                                                                    const DevCfg cfg) {
   __shared__ SplitSmem<256> smem[kSplitWarps];
+  pdl_begin();
   if (compute_off(A.st, cfg)) return;
   split_finish_body<kRowCheck, 256>(A, split, nsplit, smem, cfg);
 }
