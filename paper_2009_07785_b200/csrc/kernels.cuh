@@ -277,15 +277,17 @@ __device__ __forceinline__ void red_max(long long* p, long long k) {
   asm volatile("red.relaxed.gpu.global.max.s64 [%0], %1;" ::"l"(p), "l"(k) : "memory");
 }
 
-// A work ticket taken by one lane.  Plain atomicAdd in a one-lane branch is
-// turned by the compiler into a warp-aggregated atomic whose result is
-// shuffled to the active lanes right away, so the issuing warp waits for the
-// atomic's round trip there; the explicit atom leaves the result in a
-// register until the caller's shuffle, after the work it was taken under.
+// A work ticket taken by one lane.  An add of 1 in a one-lane branch (even
+// as inline PTX) is turned by ptxas into a warp-aggregated atomic whose
+// result is shuffled to the active lanes right away, so the issuing warp
+// waits for the atomic's round trip there (4-5 % of the full sweep's stall
+// samples); an increment with a wrap bound is not aggregated, and its result
+// waits in a register until the caller's shuffle, after the work it was
+// taken under.  (The counters are reset every round, far below the bound.)
 __device__ __forceinline__ int ticket(int32_t* p) {
-  int r;
-  asm volatile("atom.relaxed.gpu.global.add.s32 %0, [%1], 1;" : "=r"(r) : "l"(p) : "memory");
-  return r;
+  unsigned r;
+  asm volatile("atom.relaxed.gpu.global.inc.u32 %0, [%1], 0x7fffffff;" : "=r"(r) : "l"(p) : "memory");
+  return (int)r;
 }
 
 // Worklist rounds: the columns a round merged into, so the commit visits
