@@ -41,7 +41,11 @@ namespace pgb {
 #define PG_SELL_HINTS 1
 #endif
 #ifndef PG_SELL_PF
-#define PG_SELL_PF 1
+// lane 0 bulk-prefetching a slice's streams into L2 ahead of its loads:
+// measured slower on the final kernels (C2 first round 163.8 -> 161.6 us,
+// C3 687 -> 668 us without; long-row sweeps are L1-throughput-bound and each
+// prefetch is an LSU instruction), so off by default
+#define PG_SELL_PF 0
 #endif
 #ifndef PG_SELL_GROUP
 #define PG_SELL_GROUP 2  // narrow one-lane slices per work item
@@ -78,6 +82,9 @@ namespace pgb {
 #endif
 #ifndef PG_SELL_DISCARD
 #define PG_SELL_DISCARD 1  // drop the filter words' L2 lines after phase 2 (no write-back)
+#endif
+#ifndef PG_SELL_XPAD
+#define PG_SELL_XPAD 1  // padded step buffer of multi-lane chains (bank-conflict free loads)
 #endif
 #ifndef PG_SELL_GNA
 #define PG_SELL_GNA 1  // snapshot gathers with L1::no_allocate (C2 first round 179 -> 176 us)
@@ -268,7 +275,7 @@ struct SellWarpSmem {
   // entries that survive the filter: element offset in the slice, unit
   int32_t qe[64];
   uint8_t qu[64];
-  double2 xb[32];  // one step's {min, max} products of a multi-lane slice
+  double2 xb[48];  // one step's {min, max} products of a multi-lane slice (padded, sell_step)
   double2 wbuf[256];  // worklist rounds: {min, max} contributions of a wide unit's block
   double2 wbuf2[256];
 };
@@ -331,14 +338,18 @@ __device__ __forceinline__ void sell_step(double a, double lo, double up, double
     // (slice_max_to_owner hands it to lane u after the chains)
     const int lane = threadIdx.x & 31;
     const int j = lane >> (5 - LG);
+    // unit u's products at stride XS: with G >= 4 two doubles of padding
+    // put the owner lanes' 16-byte loads on disjoint banks (G = 8: the min
+    // and max lanes' loads are one conflict-free wavefront; unpadded, four)
+    constexpr int XS = (PG_SELL_XPAD && G >= 4) ? G + 2 : G;
     double* xmin = reinterpret_cast<double*>(xb);
-    double* xmax = xmin + 32;
+    double* xmax = xmin + H * XS;
     __syncwarp();  // the previous step's loads are done
-    xmin[u * G + j] = pmin;
-    xmax[u * G + j] = pmax;
+    xmin[u * XS + j] = pmin;
+    xmax[u * XS + j] = pmax;
     __syncwarp();
     if (lane < 2 * H) {
-      const double2* src = reinterpret_cast<const double2*>((lane < H ? xmin : xmax) + u * G);
+      const double2* src = reinterpret_cast<const double2*>((lane < H ? xmin : xmax) + u * XS);
       double v[G];
 #pragma unroll
       for (int i = 0; i < G / 2; ++i) {
