@@ -83,6 +83,9 @@ namespace pgb {
 #ifndef PG_SELL_DISCARD
 #define PG_SELL_DISCARD 1  // drop the filter words' L2 lines after phase 2 (no write-back)
 #endif
+#ifndef PG_SELL_WPF
+#define PG_SELL_WPF 0
+#endif
 #ifndef PG_SELL_XPAD
 #define PG_SELL_XPAD 1  // padded step buffer of multi-lane chains (bank-conflict free loads)
 #endif
@@ -458,13 +461,26 @@ __device__ __forceinline__ void slice_tail(const RA& A, SellWarpSmem& W, const S
   FTest ft = {0x7fffffff, 0x7fffffff, 0};
   if (umay) ft = FTest{W.tkr[u], W.tkl[u], W.fmask[u]};
   int qn = 0;
+  // PG_SELL_WPF: the next group's words are in flight while this group is
+  // tested (their latency was exposed once per group of every slice)
+  int32_t bn[kSellUnroll];
+  if (PG_SELL_WPF) {
+#pragma unroll
+    for (int k = 0; k < kSellUnroll; ++k) bn[k] = umay && (k << LG) + j < len ? sw[32 * k] : 0;
+  }
   for (int t0 = 0; t0 < steps; t0 += kSellUnroll) {
     int32_t b[kSellUnroll];
     bool in[kSellUnroll];
 #pragma unroll
     for (int k = 0; k < kSellUnroll; ++k) {
       in[k] = umay && ((t0 + k) << LG) + j < len;
-      b[k] = in[k] ? sw[32 * (t0 + k)] : 0;
+      if (PG_SELL_WPF) {
+        b[k] = bn[k];
+        const int tn = t0 + kSellUnroll + k;
+        bn[k] = umay && (tn << LG) + j < len ? sw[32 * tn] : 0;
+      } else {
+        b[k] = in[k] ? sw[32 * (t0 + k)] : 0;
+      }
     }
 #pragma unroll
     for (int k = 0; k < kSellUnroll; ++k) {
