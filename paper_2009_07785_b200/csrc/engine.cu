@@ -504,7 +504,7 @@ struct pg_session {
   }
 
   // A round kernel on the session stream with programmatic dependent launch
-  // (PG_PDL, default on): its CTAs are scheduled while the previous
+  // (PG_PDL, default on; single-GPU sessions): its CTAs are scheduled while the previous
   // kernel's last CTAs run and wait for its completion in pdl_begin()
   // (kernels.cuh) -- the per-kernel launch gap of the round's chain
   static bool use_pdl() {
@@ -522,7 +522,9 @@ struct pg_session {
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     c.attrs = at;
-    c.numAttrs = use_pdl() ? 1 : 0;
+    // not across a row shard's NCCL exchange: its collectives can only be
+    // exercised at world 1 here, so those graphs keep plain stream order
+    c.numAttrs = use_pdl() && !comm ? 1 : 0;
     PG_CUDA(cudaLaunchKernelEx(&c, k, args...));
   }
 
