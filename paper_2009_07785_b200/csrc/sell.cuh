@@ -106,7 +106,13 @@ constexpr int kMidU = PG_MID_UNROLL;  // worklist mid units: 8-entry steps in fl
 constexpr int kSellLaneUnit = PG_SELL_LANEUNIT;  // worklist rounds: longer units get a warp each
 constexpr int kSellMidMax = PG_SELL_MIDMAX;      //   (up to this length: 8 lanes each)
 // lanes per unit by unit length: > 256 -> 8, > 128 -> 4, > 64 -> 2, else 1
-constexpr int kSellG8 = 256, kSellG4 = 128, kSellG2 = 64;
+#ifndef PG_SELL_G8
+#define PG_SELL_G8 256
+#endif
+#ifndef PG_SELL_G4
+#define PG_SELL_G4 128
+#endif
+constexpr int kSellG8 = PG_SELL_G8, kSellG4 = PG_SELL_G4, kSellG2 = 64;
 
 // ---- memory access helpers ------------------------------------------------------
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
