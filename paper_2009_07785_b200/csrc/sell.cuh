@@ -10,12 +10,13 @@
 // warp carries a 1024-step dependent chain.
 //
 // Phase 1 (per slice, one warp): every lane loads its entries (coalesced,
-// one 256 B / 128 B request per step), gathers the column's 32 B snapshot
-// record (one L2 sector, kept resident with an evict_last policy while the
-// matrix streams through with evict_first), and forms the entry's min/max
-// contributions.  The G lanes of a unit hand their products to the unit's
-// owner lane in entry order (shuffles), so each sum is the reference's
-// sequential chain, bit for bit.  Each entry also stores a 4-byte filter
+// one 256 B / 128 B request per step), gathers the column's record (32 B
+// snapshot, 16 B bounds or 8 B float bounds, chosen per session; one L2
+// sector, kept resident with an evict_last policy while the matrix streams
+// through with evict_first), and forms the entry's min/max contributions.
+// The G lanes of a unit hand their products to the unit's owner lanes in
+// entry order (a padded shared-memory step buffer), so each sum is the
+// reference's sequential chain, bit for bit.  Each entry also stores a 4-byte filter
 // word: its filter term |a| q rounded up to float, with the two infinity
 // flags in the low mantissa bits (always >= the exact term, so a test on it
 // never drops an entry the exact test keeps).
