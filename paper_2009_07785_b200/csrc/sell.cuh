@@ -103,7 +103,11 @@ constexpr int kSellGroup = PG_SELL_GROUP;
 #ifndef PG_MID_UNROLL
 #define PG_MID_UNROLL 4  // C5 worklist rounds: 7.70 -> 7.46 ms (2: round-1 value, 8: 7.66)
 #endif
-constexpr int kMidU = PG_MID_UNROLL;  // worklist mid units: 8-entry steps in flight
+constexpr int kMidU = PG_MID_UNROLL;
+#ifndef PG_UNITS_UNROLL
+#define PG_UNITS_UNROLL 4
+#endif
+constexpr int kUnitsU = PG_UNITS_UNROLL;  // worklist lane units: chain steps in flight  // worklist mid units: 8-entry steps in flight
 constexpr int kSellLaneUnit = PG_SELL_LANEUNIT;  // worklist rounds: longer units get a warp each
 constexpr int kSellMidMax = PG_SELL_MIDMAX;      //   (up to this length: 8 lanes each)
 // lanes per unit by unit length: > 256 -> 8, > 128 -> 4, > 64 -> 2, else 1
@@ -1026,11 +1030,11 @@ __device__ __forceinline__ void sell_units(const RA& A, int par, uint64_t pol_ke
     int32_t* sw = reinterpret_cast<int32_t*>(A.sw) + off;
     Act act = {0.0, 0.0, 0, 0};
     int32_t xk = kFKeyMin;
-    for (int t0 = 0; t0 < ud.len; t0 += 4) {
-      double a[4], lo[4], up[4], q[4];
-      int32_t c[4];
+    for (int t0 = 0; t0 < ud.len; t0 += kUnitsU) {
+      double a[kUnitsU], lo[kUnitsU], up[kUnitsU], q[kUnitsU];
+      int32_t c[kUnitsU];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
+      for (int k = 0; k < kUnitsU; ++k) {
         a[k] = 0.0;
         c[k] = A.pad_col;
         if (t0 + k < ud.len) {
@@ -1039,9 +1043,9 @@ __device__ __forceinline__ void sell_units(const RA& A, int par, uint64_t pol_ke
         }
       }
 #pragma unroll
-      for (int k = 0; k < 4; ++k) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
+      for (int k = 0; k < kUnitsU; ++k) ld_col(A, c[k], pol_keep, frac_any, cfg, lo[k], up[k], q[k]);
 #pragma unroll
-      for (int k = 0; k < 4; ++k)
+      for (int k = 0; k < kUnitsU; ++k)
         if (t0 + k < ud.len) sell_step<0>(a[k], lo[k], up[k], q[k], 0, act, xk, sw + 32 * (t0 + k));
     }
     if (ud.ref < 0) {
